@@ -1,0 +1,362 @@
+"""Benchmark: the extruded-mesh column loop on B200 (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
+                    [--impl ours|reference]
+
+A "step" is one pass of the column loop (mass action y = M x with |det J|
+from the extruded coordinate field) over the whole workload.  Default
+workload: BASELINE config 2 (DG1 mass action, 256^2 split-square RCM base,
+50 layers, fp64) -- configs[1] of BASELINE.json.  Metric: valuable HBM
+bandwidth (input + output + coordinate field, each once)
+divided by the device time, plus cell-layers/s.
+
+``--impl reference`` times the reference algorithm's CPU restatement (the
+oracle's coloured-parallel column loop with literal quadrature,
+``oracle/``) on the host cores instead; the reference package itself has
+no par-loop implementation.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "valuable HBM bandwidth of the column loop (SPEC.md:467-475 bytes)"
+UNIT = "GB/s"
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, only without the file
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="C2")
+    p.add_argument("--schedule", default="auto")
+    p.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    p.add_argument("--cpu-seconds", type=float, default=8.0,
+                   help="CPU-baseline sample budget")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    summary (profiles/ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(config)
+    except (OSError, ValueError):
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,"
+         "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index),
+                     f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except (OSError, subprocess.SubprocessError):
+                return
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class CpuArm:
+    """The oracle's coloured column loop (literal quadrature, pthreads) on
+    a bounded sample of the workload: the first ``n`` base cells, all
+    layers.  Cells are taken in index order, so the sample keeps the RCM
+    locality of the full mesh."""
+
+    def __init__(self, w, fs, x, threads=0):
+        import oracle
+        from paper_1604_05937_b200.quadrature import element_for_layout
+        el = element_for_layout(fs.layout)
+        self.fs = fs
+        self.x = x
+        self.base = fs.mesh.base
+        self.prob = oracle.Problem(self.base, fs.mesh.layers,
+                                   fs.layout.counts, el.tri, el.line,
+                                   el.ncomp, *w.quad)
+        self.coloring = oracle.greedy_color(self.base)
+        self.threads = threads or oracle.max_threads()
+        self.n = self.base.num_cells
+
+    def run(self, n=None):
+        t0 = time.perf_counter()
+        self.prob.assemble_colored(self.x, threads=self.threads,
+                                   coloring=self.coloring,
+                                   n_cells=n or self.n)
+        return time.perf_counter() - t0
+
+    def calibrate(self, seconds):
+        n = max(64, self.base.num_cells // 200)
+        t = self.run(n)
+        self.n = int(min(self.base.num_cells,
+                         max(64, n * seconds / max(t, 1e-3))))
+
+    def value(self, t):
+        from paper_1604_05937_b200.perfbench import valuable_volume
+        frac = self.n / self.base.num_cells
+        return valuable_volume(self.fs) * frac / t / 1e9
+
+    def describe(self, t):
+        frac = self.n / self.base.num_cells
+        return (f"first {self.n} of {self.base.num_cells} base cells "
+                f"({100 * frac:.1f}%), all {self.fs.mesh.layers} layers, "
+                f"{t:.2f} s per pass; literal quadrature, coloured schedule, "
+                f"{self.threads} pthreads; bytes pro rata of the valuable "
+                f"volume")
+
+
+def cpu_baseline(w, fs, x, seconds):
+    arm = CpuArm(w, fs, x)
+    arm.calibrate(seconds)
+    t = arm.run()
+    return {"value": arm.value(t), "unit": UNIT, "cores": arm.threads,
+            "kind": "port", "sample": arm.describe(t)}
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from paper_1604_05937_b200 import configs
+    w = configs.WORKLOADS[args.config]
+    fs, quad, x, _ = configs.build(w)
+    arm = CpuArm(w, fs, x)
+    arm.calibrate(max(1.0, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        arm.run()
+    times = [arm.run() for _ in range(args.steps)]
+    t = float(np.mean(times))
+    value = arm.value(t)
+    line = {"impl": "reference", "metric": METRIC, "value": value,
+            "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.note}, fp64, seed {w.seed}",
+                       "base_cells": fs.mesh.base.num_cells,
+                       "layers": fs.mesh.layers, "layout": w.layout},
+            "cpu_baseline": {"value": value, "unit": UNIT,
+                             "cores": arm.threads, "kind": "port",
+                             "sample": arm.describe(t)},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1604_05937_b200 import configs
+    from paper_1604_05937_b200.extrusion import extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator, mass_action
+    from paper_1604_05937_b200.perfbench import map_bytes, valuable_volume
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    w = configs.WORKLOADS[args.config]
+    fs, quad, x_np, _ = configs.build(w)
+    m = fs.mesh
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    op = MassOperator(fs, quad, schedule=args.schedule)
+    x = torch.from_numpy(x_np).cuda()
+    y = torch.empty_like(x)
+    V = valuable_volume(fs)
+    n_cl = m.base.num_cells * m.layers
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        op.apply(x, coords, y)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device events, max over ranks ----------
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for i in range(args.steps):
+            op.apply(x, coords, y)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    launches = op.launches_per_apply
+
+    # ---- dominant kernel alone (accumulate: no memset in the launch) ----
+    ke = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    yk = torch.zeros_like(x)
+    op.apply(x, coords, yk, accumulate=True)
+    torch.cuda.synchronize()
+    ke[0].record(stream)
+    for _ in range(args.steps):
+        op.apply(x, coords, yk, accumulate=True)
+    ke[1].record(stream)
+    torch.cuda.synchronize()
+    kernel_ms = ke[0].elapsed_time(ke[1]) / args.steps
+    peak, peak_src = measured_peak()
+    achieved = V / (kernel_ms * 1e-3) / 1e9
+
+    # ---- end to end through the public API, pinned host buffers --------
+    x_host = torch.from_numpy(x_np).pin_memory()
+    y_host = torch.empty(x_np.shape[0], dtype=torch.float64).pin_memory()
+    mass_action(fs, x_host, coords, operator=op, out=y_host)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        mass_action(fs, x_host, coords, operator=op, out=y_host)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w, fs, x_np, args.cpu_seconds)
+
+    if rank == 0:
+        sm, l2 = None, None
+        from paper_1604_05937_b200 import _lib
+        sm, l2 = _lib.device_info()
+        line = {
+            "metric": METRIC, "value": world * V / (ms * 1e-3) / 1e9,
+            "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"{w.name}: {w.note}, fp64, seed {w.seed}",
+                "base_cells": m.base.num_cells, "layers": m.layers,
+                "layout": w.layout, "ordering": w.ordering,
+                "quadrature": list(w.quad),
+                "valuable_bytes": V, "map_bytes": map_bytes(fs),
+                "cell_layers_per_s": world * n_cl / (ms * 1e-3),
+                "step_ms_min": min(step_ms),
+                "pct_of_measured_hbm": 100 * (V / (ms * 1e-3) / 1e9) / peak,
+                "l2": (f"inputs larger than L2 ({V / 1e6:.0f} MB valuable vs "
+                       f"{(l2 or 0) / 1e6:.0f} MB L2): no flush"
+                       if V > (l2 or 0) else
+                       "L2-resident workload (no flush; reported, not held "
+                       "to the HBM target)"),
+                "schedule": args.schedule, "replicas": world,
+                "parallelism": f"{world} independent column-block replicas",
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": ncu_traffic(w.name),
+                         "kernel_ms": kernel_ms, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": V},
+            "cpu_baseline": cpu,
+            "e2e": {"value": world * V / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
+                    "h2d_bytes_per_step": int(x_np.nbytes),
+                    "d2h_bytes_per_step": int(x_np.nbytes),
+                    "ms_per_step": e2e_ms,
+                    "path": "kernels.mass_action(fs, pinned host x, "
+                            "out=pinned host y)"},
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+            "sm_count": sm,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

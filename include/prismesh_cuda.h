@@ -1,0 +1,155 @@
+/*
+ * prismesh_cuda.h -- C ABI of libprismesh_cuda.so (sm_100a).
+ *
+ * The drop-in boundary for the extruded-mesh column loop of
+ * Bercea et al. 2016 (arXiv:1604.05937).  Every entry point takes plain
+ * pointers and sizes; device pointers are CUDA global-memory addresses
+ * (e.g. torch.Tensor.data_ptr()), `stream` is a cudaStream_t (0 = legacy
+ * default stream).  Calls are asynchronous on `stream` unless stated.
+ * Every function returns 0 on success and a nonzero PM_E* code otherwise;
+ * pm_last_error() then returns a thread-local message.  Nothing throws
+ * across the ABI.
+ *
+ * Reference interfaces replaced (paths under the reference checkout):
+ *   pm_build_cell_map        <- pkg/src/prismesh/fspace.py:192-215 (build_cell_map)
+ *                               + fspace.py:218-229 (compute_offsets)
+ *                               + fspace.py:137-149 (FunctionSpace numbering)
+ *   pm_extrude_coordinates   <- pkg/src/prismesh/extrusion.py:66-85
+ *   pm_column_mass           <- SPEC.md:333-341 iterate_columns driving
+ *                               SPEC.md:412-420 assemble_residual
+ *                               (Algorithm 3)
+ *   pm_column_probe          <- SPEC.md:338-340 counting / gather kernels
+ *                               (verification.py:47-75 materialized maps)
+ *   pm_halo_pack / _unpack   <- PAPER.md:770-775 (halo exchange between
+ *                               base-mesh partitions; SPEC.md:9 leaves it out)
+ *   pm_column_mass_cells     <- SPEC.md:358-364 coloured-parallel schedule
+ *   pm_greedy_color_cells    <- SPEC.md:343-351 color_base_cells
+ *   pm_rcm_order             <- pkg/src/prismesh/ordering.py:45-90 (host BFS)
+ */
+#ifndef PRISMESH_CUDA_H
+#define PRISMESH_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PM_OK = 0,
+  PM_EINVAL = 1,   /* bad argument (shape / arity / layout)  -> ValueError   */
+  PM_ECUDA = 2,    /* CUDA runtime error                     -> RuntimeError */
+  PM_EOVERFLOW = 3 /* DoF numbers do not fit int32           -> ValueError   */
+};
+
+/* Column-loop element kinds (`elem` argument of pm_column_mass). */
+enum {
+  PM_SHARE_NONE = 0,       /* every DoF touched by one cell-layer (DG x DG)  */
+  PM_SHARE_VERTICAL = 1,   /* shared only along the column (DG x CG)         */
+  PM_SHARE_HORIZONTAL = 2  /* shared between columns (CG horizontally)       */
+};
+
+/* Schedules (`variant` argument of pm_column_mass). */
+enum {
+  PM_VARIANT_AUTO = 0,     /* pick the fastest implemented schedule         */
+  PM_VARIANT_ATOMIC = 1,   /* cell-layer threads, fp64 REDG for shared DoFs */
+  PM_VARIANT_PATCH = 2,    /* patch-owner gather through shared memory      */
+  PM_VARIANT_COLUMN = 3    /* warp-per-column, lanes = layers               */
+};
+
+const char *pm_last_error(void);
+int pm_version(void);
+
+/* --- K0: numbering / map generation (device) ---------------------------
+ * delta6[2*d1+d2] = DoFs per extruded entity (d1,d2).  Writes the int32
+ * bottom-layer map cell_map[n_cells*k] in the reference slot order and the
+ * int32 per-slot offsets[k].  Values are computed in int64 and truncated
+ * to int32 exactly like the reference numpy store (wraps past 2^31-1);
+ * *total_dofs (host) receives the exact int64 total. */
+int pm_build_cell_map(const int32_t *cell_vertices, const int32_t *cell_edges,
+                      int64_t n_cells, int64_t n_vertices, int64_t n_edges,
+                      const int32_t *delta6, int32_t layers, int32_t k,
+                      int32_t *cell_map, int32_t *offsets,
+                      int64_t *total_dofs, void *stream);
+
+/* Number of slots of a layout (host, no device work). */
+int pm_num_slots(const int32_t *delta6, int32_t *k_out);
+
+/* --- extruded coordinate field (device) --------------------------------
+ * out[3*(i*(layers+1)+l)+c] = (x_i, y_i, l*h)[c]. */
+int pm_extrude_coordinates(const double *base_coords, int64_t n_vertices,
+                           int32_t layers, double layer_height, double *out,
+                           void *stream);
+
+/* --- the column loop: y (+)= M x over every cell-layer -----------------
+ * k        : slots per cell of the field space (1,2,3,6,18)
+ * share    : PM_SHARE_*
+ * cell_map : device int32 [n_cells*k];   offsets: device int32 [k]
+ * coord_map: device int32 [n_cells*18];  coord_offsets: device int32 [18]
+ * coords   : device fp64 extruded coordinate field
+ * mref     : HOST fp64 [k*k] reference-prism mass matrix (slot order)
+ * x, y     : device fp64 fields of length n_dofs
+ * accumulate: 0 -> y = M x (y is overwritten), 1 -> y += M x
+ * plan     : device workspace from pm_patch_plan_build (PATCH variant) or
+ *            NULL
+ * Each cell-layer's |det J| comes from the six prism vertices read out of
+ * `coords`. */
+int pm_column_mass(int32_t k, int32_t share, int64_t n_cells, int32_t layers,
+                   const int32_t *cell_map, const int32_t *offsets,
+                   const int32_t *coord_map, const int32_t *coord_offsets,
+                   const double *coords, const double *mref,
+                   const double *x, double *y, int64_t n_dofs,
+                   int32_t accumulate, int32_t variant, const void *plan,
+                   void *stream);
+
+/* One colour of the base-cell colouring: y += M x over the listed cells
+ * only (device int32 cells[n_list]).  The colouring guarantees no two
+ * listed cells share a DoF, so the kernel uses plain read-add-stores and
+ * the result is bitwise deterministic. */
+int pm_column_mass_cells(int32_t k, const int32_t *cells, int64_t n_list,
+                         int32_t layers, const int32_t *cell_map,
+                         const int32_t *offsets, const int32_t *coord_map,
+                         const int32_t *coord_offsets, const double *coords,
+                         const double *mref, const double *x, double *y,
+                         void *stream);
+
+/* --- probes for the par-loop itself (exact integer checks) -------------
+ * mode 0: out_i64[(c*layers+l)*k + j] = cell_map[c*k+j] + l*offsets[j]
+ *         (the materialised per-(cell,layer) lists)
+ * mode 1: out_f64[dof] += 1 for every slot of every cell-layer (counting
+ *         kernel) -- out_f64 must be zeroed by the caller. */
+int pm_column_probe(int32_t mode, int32_t k, int64_t n_cells, int32_t layers,
+                    const int32_t *cell_map, const int32_t *offsets,
+                    int64_t *out_i64, double *out_f64, void *stream);
+
+/* --- multi-GPU halo (ghost vertex-column partial sums) ------------------
+ * pack:   buf[i*col + t] = y[cols[i] + t]   for i < n_cols, t < col
+ * unpack: y[cols[i] + t] += buf[i*col + t]
+ * (`cols` = device int64 DoF origins of the ghost / owned columns). */
+int pm_halo_pack(const double *y, const int64_t *cols, int64_t n_cols,
+                 int32_t col, double *buf, void *stream);
+int pm_halo_unpack_add(double *y, const int64_t *cols, int64_t n_cols,
+                       int32_t col, const double *buf, void *stream);
+
+/* --- host setup: reverse Cuthill-McKee BFS (no device work) -------------
+ * offsets[n+1], neighbours sorted by (degree, index) within each row.
+ * order_out[n] receives the Cuthill-McKee visit order (not reversed). */
+int pm_rcm_order(const int64_t *offsets, const int64_t *neighbours, int64_t n,
+                 int64_t *order_out);
+
+/* --- host setup: greedy base-cell colouring (no device work) ------------
+ * Cells in index order take the smallest colour not used by an already
+ * coloured cell sharing a vertex.  vc_offsets/vc_cells:
+ * vertex->cell CSR.  Returns the colour count in *n_colors. */
+int pm_greedy_color_cells(const int32_t *cell_vertices, int64_t n_cells,
+                          const int64_t *vc_offsets, const int32_t *vc_cells,
+                          int32_t *color_out, int32_t *n_colors);
+
+/* Device properties used to size grids (SM count, L2 bytes). */
+int pm_device_info(int32_t *sm_count, int64_t *l2_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRISMESH_CUDA_H */

@@ -1,0 +1,241 @@
+"""ctypes binding of libprismesh_cuda.so (the C ABI in include/prismesh_cuda.h).
+
+No fallback: if the library is missing or no CUDA device is present, the
+device entry points raise.  torch owns device memory and streams; the ABI
+receives ``data_ptr()`` values and ``torch.cuda.current_stream()``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_native", "libprismesh_cuda.so")
+
+PM_OK, PM_EINVAL, PM_ECUDA, PM_EOVERFLOW = 0, 1, 2, 3
+SHARE_NONE, SHARE_VERTICAL, SHARE_HORIZONTAL = 0, 1, 2
+VARIANT_AUTO, VARIANT_ATOMIC, VARIANT_PATCH, VARIANT_COLUMN = 0, 1, 2, 3
+
+_lib = None
+
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_f64 = ctypes.c_double
+
+#: name -> (restype, argtypes); mirrors include/prismesh_cuda.h
+SIGNATURES = {
+    "pm_last_error": (ctypes.c_char_p, []),
+    "pm_version": (ctypes.c_int, []),
+    "pm_build_cell_map": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i32p,
+                                         _i32, _i32, _vp, _vp, _i64p, _vp]),
+    "pm_num_slots": (ctypes.c_int, [_i32p, _i32p]),
+    "pm_extrude_coordinates": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp,
+                                              _vp]),
+    "pm_column_mass": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
+                                      _vp, _vp, ctypes.POINTER(_f64), _vp,
+                                      _vp, _i64, _i32, _i32, _vp, _vp]),
+    "pm_column_mass_cells": (ctypes.c_int, [_i32, _vp, _i64, _i32, _vp, _vp,
+                                            _vp, _vp, _vp,
+                                            ctypes.POINTER(_f64), _vp, _vp,
+                                            _vp]),
+    "pm_greedy_color_cells": (ctypes.c_int, [_i32p, _i64, _i64p, _i32p,
+                                             _i32p, _i32p]),
+    "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
+                                       _vp, _vp]),
+    "pm_halo_pack": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
+    "pm_halo_unpack_add": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
+    "pm_rcm_order": (ctypes.c_int, [_i64p, _i64p, _i64, _i64p]),
+    "pm_device_info": (ctypes.c_int, [_i32p, _i64p]),
+}
+
+
+class NativeLibraryMissing(RuntimeError):
+    pass
+
+
+def host_lib():
+    """Load the native library (also usable without a GPU for host setup)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryMissing(
+                f"{LIB_PATH} not built; run "
+                "`python -m paper_1604_05937_b200.build_native` "
+                "(or __graft_entry__.build())")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    msg = host_lib().pm_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int):
+    if rc == PM_OK:
+        return
+    msg = last_error()
+    if rc in (PM_EINVAL, PM_EOVERFLOW):
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def cuda_device():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "prismesh-b200 needs a CUDA device (sm_100a); there is no CPU "
+            "fallback")
+    host_lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+# ---------------------------------------------------------------------------
+# thin typed wrappers
+# ---------------------------------------------------------------------------
+
+def num_slots(layout) -> int:
+    d = layout.delta6()
+    k = ctypes.c_int32(0)
+    check(host_lib().pm_num_slots(d.ctypes.data_as(_i32p), ctypes.byref(k)))
+    return k.value
+
+
+def mesh_device_arrays(base, device):
+    """Cached device copies of the base connectivity (int32)."""
+    import torch
+    cache = getattr(base, "__dict__", {}).get("_pm_device")
+    if cache is not None and cache["device"] == device:
+        return cache
+    cv = torch.from_numpy(np.ascontiguousarray(base.cell_vertices,
+                                               dtype=np.int32)).to(device)
+    ce = torch.from_numpy(np.ascontiguousarray(base.cell_edges,
+                                               dtype=np.int32)).to(device)
+    cache = {"device": device, "cv": cv, "ce": ce}
+    try:
+        base.__dict__["_pm_device"] = cache
+    except (AttributeError, TypeError):
+        pass
+    return cache
+
+
+def build_cell_map_device(fs, stream=None):
+    """K0 on the device: (cell_map (N2,k) int32, offsets (k,) int32)."""
+    import torch
+    dev = cuda_device()
+    base = fs.mesh.base
+    k = num_slots(fs.layout)
+    arrs = mesh_device_arrays(base, dev)
+    n_cells = base.num_cells
+    cmap = torch.empty((n_cells, k), dtype=torch.int32, device=dev)
+    offs = torch.empty((k,), dtype=torch.int32, device=dev)
+    total = ctypes.c_int64(0)
+    d = fs.layout.delta6()
+    rc = host_lib().pm_build_cell_map(
+        ptr(arrs["cv"]), ptr(arrs["ce"]), n_cells, base.num_vertices,
+        base.num_edges, d.ctypes.data_as(_i32p), fs.mesh.layers, k,
+        ptr(cmap), ptr(offs), ctypes.byref(total), stream_ptr(stream))
+    check(rc)
+    if total.value != fs.total_dofs:
+        raise RuntimeError(
+            f"device total {total.value} != closed form {fs.total_dofs}")
+    return cmap, offs
+
+
+def extrude_coordinates_device(d_base, layers, h, stream=None):
+    import torch
+    n = d_base.shape[0]
+    out = torch.empty(3 * n * (layers + 1), dtype=torch.float64,
+                      device=d_base.device)
+    check(host_lib().pm_extrude_coordinates(ptr(d_base), n, layers, float(h),
+                                            ptr(out), stream_ptr(stream)))
+    return out
+
+
+def column_probe(mode, fs, out, stream=None):
+    cmap = fs.device_cell_map()
+    offs = fs.device_offsets()
+    k = cmap.shape[1]
+    i64 = ptr(out) if mode == 0 else None
+    f64 = ptr(out) if mode == 1 else None
+    check(host_lib().pm_column_probe(mode, k, fs.mesh.base.num_cells,
+                                     fs.mesh.layers, ptr(cmap), ptr(offs),
+                                     i64, f64, stream_ptr(stream)))
+
+
+def column_mass(k, share, n_cells, layers, cmap, offs, xmap, xoffs, coords,
+                mref, x, y, n_dofs, accumulate=False, variant=VARIANT_AUTO,
+                plan=None, stream=None):
+    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    if m.shape[0] != k * k:
+        raise ValueError(f"mref must be {k}x{k}")
+    rc = host_lib().pm_column_mass(
+        k, share, n_cells, layers, ptr(cmap), ptr(offs), ptr(xmap),
+        ptr(xoffs), ptr(coords), m.ctypes.data_as(ctypes.POINTER(_f64)),
+        ptr(x), ptr(y), n_dofs, 1 if accumulate else 0, variant,
+        ptr(plan) if plan is not None else None, stream_ptr(stream))
+    check(rc)
+
+
+def column_mass_cells(k, cells, layers, cmap, offs, xmap, xoffs, coords,
+                      mref, x, y, stream=None):
+    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    if m.shape[0] != k * k:
+        raise ValueError(f"mref must be {k}x{k}")
+    rc = host_lib().pm_column_mass_cells(
+        k, ptr(cells), cells.shape[0], layers, ptr(cmap), ptr(offs),
+        ptr(xmap), ptr(xoffs), ptr(coords),
+        m.ctypes.data_as(ctypes.POINTER(_f64)), ptr(x), ptr(y),
+        stream_ptr(stream))
+    check(rc)
+
+
+def greedy_color_cells(cell_vertices, vc_offsets, vc_cells):
+    cv = np.ascontiguousarray(cell_vertices, dtype=np.int32)
+    off = np.ascontiguousarray(vc_offsets, dtype=np.int64)
+    vcc = np.ascontiguousarray(vc_cells, dtype=np.int32)
+    n = cv.shape[0]
+    color = np.empty(n, dtype=np.int32)
+    nc = ctypes.c_int32(0)
+    check(host_lib().pm_greedy_color_cells(
+        cv.ctypes.data_as(_i32p), n, off.ctypes.data_as(_i64p),
+        vcc.ctypes.data_as(_i32p), color.ctypes.data_as(_i32p),
+        ctypes.byref(nc)))
+    return color, nc.value
+
+
+def halo_pack(y, cols, col, buf, stream=None):
+    check(host_lib().pm_halo_pack(ptr(y), ptr(cols), cols.shape[0], col,
+                                  ptr(buf), stream_ptr(stream)))
+
+
+def halo_unpack_add(y, cols, col, buf, stream=None):
+    check(host_lib().pm_halo_unpack_add(ptr(y), ptr(cols), cols.shape[0],
+                                        col, ptr(buf), stream_ptr(stream)))
+
+
+def device_info():
+    sm = ctypes.c_int32(0)
+    l2 = ctypes.c_int64(0)
+    check(host_lib().pm_device_info(ctypes.byref(sm), ctypes.byref(l2)))
+    return sm.value, l2.value

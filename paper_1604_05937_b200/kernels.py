@@ -1,0 +1,283 @@
+"""Element kernels on triangle x interval prisms, executed on the GPU.
+
+Drop-in for the SPEC's ``kernels`` module:
+
+* ``prism_quadrature(tri_degree, line_degree)``   (``quadrature.py``)
+* ``assemble_residual(fs, f, coords)``  -- ``b_j = int f v_j dx`` with ``f``
+  in ``fs``: the mass-matrix action ``b = M f`` (SPEC.md:412-420,
+  PAPER.md:629-642 integral I_1)
+* ``count_flops(layout, quadrature)``   -- analytic profile
+
+plus the device operator ``MassOperator`` (prepared maps, reusable) that
+the benchmark and the sharded driver call, and the probe kernels used to
+check the par-loop's addressing.
+
+Fields are flat float64 arrays in the space's global numbering.  Numpy in
+-> numpy out (host<->device copies happen inside the call); CUDA tensor in
+-> CUDA tensor out.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .fspace import COORDS_LAYOUT, FunctionSpace, number_dofs
+from .quadrature import (PrismElement, QuadratureRule, element_for_layout,
+                         prism_quadrature, reference_mass_matrix,
+                         sharing_class)
+
+__all__ = ["Field", "KernelProfile", "MassKernel", "MassOperator",
+           "CountingKernel", "ListProbeKernel", "assemble_residual",
+           "mass_action", "count_flops", "prism_quadrature",
+           "default_quadrature"]
+
+
+@dataclass
+class Field:
+    """Values of one function space."""
+
+    space: FunctionSpace
+    values: object
+
+    def __post_init__(self):
+        if len(self.values) != self.space.total_dofs:
+            raise ValueError(
+                f"field has {len(self.values)} values, space has "
+                f"{self.space.total_dofs}")
+
+
+@dataclass(frozen=True)
+class KernelProfile:
+    adds: int
+    muls: int
+    fmas: int
+    vector_flops: int
+
+    @property
+    def total_flops(self) -> int:
+        return self.adds + self.muls + 2 * self.fmas
+
+
+def count_flops(layout, quadrature: QuadratureRule) -> KernelProfile:
+    """Per cell-layer: per point k muls + (k-1) adds (f . phi), 1 mul
+    (w|detJ|), k muls + k adds (scatter) -- SPEC.md:425."""
+    from .fspace import slot_table
+    k = len(slot_table(layout))
+    q = quadrature.num_points
+    return KernelProfile(adds=q * (2 * k - 1), muls=q * (2 * k + 1), fmas=0,
+                         vector_flops=0)
+
+
+def default_quadrature(element: PrismElement) -> QuadratureRule:
+    """SPEC default (2,2), raised to the exact degree for P2 elements."""
+    deg = {"P0": 0, "P1": 1, "P2": 2}
+    return prism_quadrature(max(2, 2 * deg[element.tri]),
+                            max(2, 2 * deg[element.line]))
+
+
+def _as_device(a, dev):
+    import torch
+    if isinstance(a, Field):
+        a = a.values
+    if isinstance(a, torch.Tensor):
+        if a.dtype != torch.float64:
+            raise ValueError(f"fields are float64, got {a.dtype}")
+        if a.device.type != "cuda":
+            return a.to(dev, non_blocking=a.is_pinned()), True
+        return a.contiguous(), False
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    return torch.from_numpy(arr).to(dev, non_blocking=False), True
+
+
+class MassOperator:
+    """``y = |det J| M_ref x`` over every cell-layer of ``fs`` (device).
+
+    Holds the device-resident bottom-layer maps (K0), the coordinate
+    space's maps and the pre-integrated reference matrix.
+    """
+
+    def __init__(self, fs: FunctionSpace, quadrature: QuadratureRule = None,
+                 element: PrismElement = None, schedule: str = "auto"):
+        if not fs.fits_int32:
+            raise ValueError(
+                f"{fs!r}: {fs.total_dofs} DoFs overflow the int32 cell map")
+        self.fs = fs
+        self.coord_fs = number_dofs(fs.mesh, COORDS_LAYOUT)
+        self.element = element or element_for_layout(fs.layout)
+        self.quadrature = quadrature or default_quadrature(self.element)
+        self.mref = reference_mass_matrix(self.element, self.quadrature)
+        self.share = sharing_class(fs.layout)
+        self.k = fs.num_slots
+        self.schedule = schedule
+        self._coloring = None
+        self._dev = _lib.cuda_device()
+        self.cmap = fs.device_cell_map()
+        self.offs = fs.device_offsets()
+        self.xmap = self.coord_fs.device_cell_map()
+        self.xoffs = self.coord_fs.device_offsets()
+
+    @property
+    def launches_per_apply(self) -> int:
+        """Column-loop kernel launches one ``apply`` issues."""
+        if self.schedule in ("colored", "sequential") and self.share != 0:
+            return self._color_lists()[1].shape[0] - 1
+        return 1
+
+    @property
+    def n_cells(self):
+        return self.fs.mesh.base.num_cells
+
+    @property
+    def layers(self):
+        return self.fs.mesh.layers
+
+    def _color_lists(self):
+        if self._coloring is None:
+            import torch
+            col = _color(self.fs.mesh)
+            order, ptr = col.cells_by_color()
+            d_order = torch.from_numpy(order).to(self._dev)
+            self._coloring = (d_order, ptr)
+        return self._coloring
+
+    def apply(self, x, coords, y=None, accumulate=False, schedule=None,
+              stream=None):
+        """Device tensors in/out; returns ``y``."""
+        import torch
+        sched = schedule or self.schedule
+        n = self.fs.total_dofs
+        if x.shape[0] != n:
+            raise ValueError(f"x has {x.shape[0]} values, space has {n}")
+        if coords.shape[0] != self.coord_fs.total_dofs:
+            raise ValueError("coordinate field does not match the mesh")
+        if y is None:
+            y = torch.empty(n, dtype=torch.float64, device=x.device)
+            accumulate = False
+        if sched in ("colored", "sequential") and self.share != 0:
+            if not accumulate:
+                y.zero_()
+            order, ptr = self._color_lists()
+            for c in range(len(ptr) - 1):
+                _lib.column_mass_cells(
+                    self.k, order[ptr[c]:ptr[c + 1]], self.layers, self.cmap,
+                    self.offs, self.xmap, self.xoffs, coords, self.mref, x, y,
+                    stream=stream)
+            return y
+        variant = {"auto": _lib.VARIANT_AUTO, "atomic": _lib.VARIANT_ATOMIC,
+                   "column": _lib.VARIANT_COLUMN, "colored": _lib.VARIANT_AUTO,
+                   "sequential": _lib.VARIANT_AUTO}[sched]
+        if sched == "column" and self.share != 0:
+            raise ValueError("the column schedule needs a DG (2,1) layout")
+        _lib.column_mass(self.k, self.share, self.n_cells, self.layers,
+                         self.cmap, self.offs, self.xmap, self.xoffs, coords,
+                         self.mref, x, y, n, accumulate=accumulate,
+                         variant=variant, stream=stream)
+        return y
+
+
+_COLORINGS = {}
+
+
+def _color(mesh):
+    from .iterate import color_base_cells
+    key = id(mesh.base)
+    hit = _COLORINGS.get(key)
+    if hit is None or hit[0] is not mesh.base:
+        hit = (mesh.base, color_base_cells(mesh))
+        _COLORINGS[key] = hit
+    return hit[1]
+
+
+class MassKernel:
+    """Stencil kernel ``I_1``: arity (k of the field space, 18 coords)."""
+
+    def __init__(self, fs: FunctionSpace, quadrature=None, element=None):
+        self.fs = fs
+        self.element = element or element_for_layout(fs.layout)
+        self.quadrature = quadrature or default_quadrature(self.element)
+        self.arity = (fs.num_slots, 18)
+        self._op = None
+
+    def launch(self, fs_list, fields, schedule, stream=None):
+        if len(fields) != 3:
+            raise ValueError("mass kernel fields are [f, coords, out]")
+        if fs_list[1].layout.counts != COORDS_LAYOUT.counts:
+            raise ValueError("second space must be the coordinate space")
+        if self._op is None or self._op.fs is not fs_list[0]:
+            self._op = MassOperator(fs_list[0], self.quadrature, self.element)
+        f, coords, out = fields
+        self._op.apply(f, coords, out, accumulate=True, schedule=schedule,
+                       stream=stream)
+
+
+class CountingKernel:
+    """Adds 1 to every output DoF a cell-layer touches."""
+
+    def __init__(self, fs):
+        self.arity = (fs.num_slots,)
+
+    def launch(self, fs_list, fields, schedule, stream=None):
+        (out,) = fields
+        _lib.column_probe(1, fs_list[0], out, stream=stream)
+
+
+class ListProbeKernel:
+    """Writes each cell-layer's DoF list (N2, layers, k) int64: the
+    materialised maps of verification.py:47-75, produced by the loop."""
+
+    def __init__(self, fs):
+        self.arity = (fs.num_slots,)
+
+    def launch(self, fs_list, fields, schedule, stream=None):
+        (out,) = fields
+        _lib.column_probe(0, fs_list[0], out, stream=stream)
+
+
+def _coords_device(fs, coords, dev):
+    import torch
+    if coords is None:
+        from .extrusion import extrude_coordinates
+        m = fs.mesh
+        return extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    c, _ = _as_device(coords, dev)
+    return c
+
+
+def mass_action(fs, x, coords=None, quadrature=None, schedule="auto",
+                operator: MassOperator = None, out=None):
+    """``y = M x`` on ``fs``.
+
+    numpy in -> numpy out; CUDA tensor in -> CUDA tensor out; a host torch
+    tensor ``out`` (ideally pinned) receives the result in place.
+    """
+    import torch
+    op = operator or MassOperator(fs, quadrature)
+    if op.fs is not fs:
+        raise ValueError("operator was prepared for another space")
+    dev = op._dev
+    d_x, x_host = _as_device(x, dev)
+    d_c = _coords_device(fs, coords, dev)
+    y = op.apply(d_x, d_c, schedule=schedule)
+    if out is not None:
+        out.copy_(y, non_blocking=out.device.type == "cpu" and out.is_pinned())
+        torch.cuda.current_stream().synchronize()
+        return out
+    if x_host:
+        return y.cpu().numpy()
+    return y
+
+
+def assemble_residual(fs, f, coords=None, quadrature=None, schedule="auto",
+                      operator: MassOperator = None):
+    """``b_j = sum_{c,l} sum_q w_q |det J| phi_j(q) f(q)``.
+
+    ``coords`` is the extruded coordinate field (default: built on the
+    device from the base mesh).  Returns a Field if ``f`` is a Field.
+    """
+    vals = f.values if isinstance(f, Field) else f
+    if isinstance(f, Field) and f.space is not fs:
+        raise ValueError("f does not live on fs")
+    out = mass_action(fs, vals, coords, quadrature, schedule, operator)
+    return Field(fs, out) if isinstance(f, Field) else out

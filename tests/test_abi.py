@@ -1,0 +1,56 @@
+"""The C-ABI library loads without a GPU and exports every symbol that
+include/prismesh_cuda.h declares; argument errors come back as codes."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1604_05937_b200 import _lib, builtin_layout, P2_LAYOUT
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(
+    os.path.abspath(__file__))), "include", "prismesh_cuda.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(pm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.host_lib()
+    names = declared_functions()
+    assert len(names) >= 10
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
+
+
+def test_num_slots_and_errors():
+    assert _lib.num_slots(builtin_layout("CG1", "CG1")) == 6
+    assert _lib.num_slots(P2_LAYOUT) == 18
+    lib = _lib.host_lib()
+    d = np.array([1, 0, 0, 0, 0, 0], dtype=np.int32)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    rc = lib.pm_build_cell_map(None, None, 1, 3, 3, d.ctypes.data_as(i32p),
+                               0, 6, None, None, None, None)
+    assert rc == _lib.PM_EINVAL and "layer" in _lib.last_error()
+    bad = np.array([-1, 0, 0, 0, 0, 0], dtype=np.int32)
+    k = ctypes.c_int32(0)
+    assert lib.pm_num_slots(bad.ctypes.data_as(i32p), ctypes.byref(k)) == \
+        _lib.PM_EINVAL
+    with pytest.raises(ValueError):
+        _lib.check(_lib.PM_EINVAL)
+    rc = lib.pm_column_mass(7, 2, 10, 3, None, None, None, None, None, None,
+                            None, None, 0, 0, 0, None, None)
+    assert rc == _lib.PM_EINVAL
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(RuntimeError):
+        _lib.cuda_device()

@@ -1,0 +1,267 @@
+"""CUDA path vs the oracle / reference golden vectors (needs a B200).
+
+Bars (BASELINE.json north_star): bit-exact for maps and numbering; 1e-12
+relative for DG (deterministic); 1e-10 relative for CG (re-ordered
+increments).  "Relative" = max-norm error / max-norm of the oracle.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import LAYOUT_COUNTS, families, quad_degrees
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _space(base, layers, lname):
+    from paper_1604_05937_b200 import DofLayout, ExtrudedMesh, number_dofs
+    return number_dofs(ExtrudedMesh(base, layers),
+                       DofLayout(lname, LAYOUT_COUNTS[lname]))
+
+
+def _tol(lname):
+    from paper_1604_05937_b200.quadrature import sharing_class
+    from paper_1604_05937_b200 import DofLayout
+    return 1e-12 if sharing_class(DofLayout(lname, LAYOUT_COUNTS[lname])) \
+        == 0 else 1e-10
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+# ------------------------------------------------------------- K0 maps
+@pytest.mark.parametrize("mname", ("one", "two", "sq5", "sq4rcm", "sq4rnd"))
+@pytest.mark.parametrize("layers", (1, 3, 4))
+@pytest.mark.parametrize("lname", sorted(LAYOUT_COUNTS))
+def test_device_maps_bit_exact(golden, gmesh, mname, layers, lname):
+    fs = _space(gmesh(mname), layers, lname)
+    key = f"fs/{mname}/L{layers}/{lname}"
+    np.testing.assert_array_equal(fs.cell_map, golden[key + "/cell_map"])
+    np.testing.assert_array_equal(fs.offsets, golden[key + "/offsets"])
+    assert fs.total_dofs == int(golden[key + "/total"])
+
+
+def test_device_maps_large_vs_oracle():
+    from paper_1604_05937_b200 import configs
+    for w in (configs.WORKLOADS["C2"], configs.WORKLOADS["C3"]):
+        fs, _, _, _ = configs.build(w)
+        m, off, total = oracle.cell_map(fs.mesh.base, fs.mesh.layers,
+                                        fs.layout.counts)
+        assert np.array_equal(fs.cell_map, m)
+        assert np.array_equal(fs.offsets, off) and total == fs.total_dofs
+
+
+def test_device_map_wraps_like_reference():
+    """fspace.py:203/214 store int64 origins into int32 (wraps)."""
+    from paper_1604_05937_b200 import (BaseMesh, DofLayout, ExtrudedMesh,
+                                       number_dofs)
+    one = BaseMesh([[0, 1, 2]], [[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]])
+    lay = DofLayout("big", {(0, 0): 1, (2, 1): 1})
+    fs = number_dofs(ExtrudedMesh(one, 800_000_000), lay)
+    m, _, total = oracle.cell_map(one, 800_000_000, lay.counts)
+    assert total == fs.total_dofs > 2**31
+    np.testing.assert_array_equal(fs.cell_map, m)
+    assert not fs.fits_int32
+
+
+@pytest.mark.parametrize("mname", ("one", "two", "sq5", "sq4rcm"))
+@pytest.mark.parametrize("layers", (1, 3, 4))
+def test_device_extrude_bit_exact(golden, gmesh, mname, layers):
+    from paper_1604_05937_b200 import extrude_coordinates
+    got = extrude_coordinates(gmesh(mname).coords, layers, 1.0 / layers,
+                              device="cpu")
+    np.testing.assert_array_equal(got, golden[f"coords/{mname}/L{layers}"])
+
+
+# ------------------------------------------------------------- par-loop
+@pytest.mark.parametrize("mname", ("one", "two", "sq4rcm"))
+@pytest.mark.parametrize("layers", (1, 3))
+@pytest.mark.parametrize("lname", sorted(LAYOUT_COUNTS))
+def test_loop_addresses_equal_materialised(golden, gmesh, mname, layers,
+                                           lname):
+    """The device loop's per-(cell,layer) lists == verification.py:47-75."""
+    from paper_1604_05937_b200.iterate import iterate_columns
+    from paper_1604_05937_b200.kernels import ListProbeKernel
+    fs = _space(gmesh(mname), layers, lname)
+    out = torch.empty((fs.mesh.base.num_cells, layers, fs.num_slots),
+                      dtype=torch.int64, device="cuda")
+    iterate_columns([fs], ListProbeKernel(fs), [out])
+    np.testing.assert_array_equal(
+        out.cpu().numpy(), golden[f"fs/{mname}/L{layers}/{lname}/materialized"])
+
+
+def test_counting_kernel(gmesh):
+    """DG0xDG0 counting kernel -> all ones, sum N2*layers."""
+    from paper_1604_05937_b200.iterate import iterate_columns
+    from paper_1604_05937_b200.kernels import CountingKernel
+    fs = _space(gmesh("sq5"), 4, "DG0xDG0")
+    out = torch.zeros(fs.total_dofs, dtype=torch.float64, device="cuda")
+    iterate_columns([fs], CountingKernel(fs), [out])
+    o = out.cpu().numpy()
+    assert np.all(o == 1.0) and o.sum() == fs.mesh.base.num_cells * 4
+
+
+def test_arity_and_mesh_mismatch_rejected(gmesh):
+    from paper_1604_05937_b200 import COORDS_LAYOUT, ExtrudedMesh, number_dofs
+    from paper_1604_05937_b200.iterate import iterate_columns
+    from paper_1604_05937_b200.kernels import MassKernel
+    fs = _space(gmesh("sq5"), 3, "CG1xCG1")
+    other = _space(gmesh("sq5"), 3, "P2xP2")
+    xfs = number_dofs(fs.mesh, COORDS_LAYOUT)
+    k = MassKernel(fs)
+    with pytest.raises(ValueError):
+        iterate_columns([other, xfs], k, [None, None, None])
+    xfs2 = number_dofs(ExtrudedMesh(gmesh("sq5"), 3), COORDS_LAYOUT)
+    with pytest.raises(ValueError):
+        iterate_columns([fs, xfs2], k, [None, None, None])
+
+
+SCHEDULES = ("auto", "atomic", "colored")
+
+
+@pytest.mark.parametrize("mname", ("one", "two", "sq5", "sq4rnd"))
+@pytest.mark.parametrize("layers", (1, 3, 5))
+@pytest.mark.parametrize("lname", sorted(set(LAYOUT_COUNTS) - {"coords"}))
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_mass_action_matches_oracle(gmesh, mname, layers, lname, schedule):
+    from paper_1604_05937_b200.kernels import mass_action
+    from paper_1604_05937_b200.quadrature import prism_quadrature
+    base = gmesh(mname)
+    fs = _space(base, layers, lname)
+    tri, line, nc = families(lname)
+    qd = quad_degrees(lname)
+    prob = oracle.Problem(base, layers, LAYOUT_COUNTS[lname], tri, line, nc,
+                          *qd)
+    f = np.random.default_rng(layers).uniform(-1, 1, fs.total_dofs)
+    ref = prob.assemble(f)
+    got = mass_action(fs, f, quadrature=prism_quadrature(*qd),
+                      schedule=schedule)
+    assert _rel(got, ref) <= _tol(lname), (lname, schedule)
+
+
+@pytest.mark.parametrize("lname", ("CG1xCG1", "P2xP2", "DG1xCG1", "VP1"))
+def test_iterate_columns_accumulates(gmesh, lname):
+    """iterate_columns adds into the output."""
+    from paper_1604_05937_b200 import COORDS_LAYOUT, number_dofs
+    from paper_1604_05937_b200 import extrude_coordinates
+    from paper_1604_05937_b200.iterate import iterate_columns
+    from paper_1604_05937_b200.kernels import MassKernel
+    base = gmesh("sq5")
+    fs = _space(base, 3, lname)
+    xfs = number_dofs(fs.mesh, COORDS_LAYOUT)
+    coords = extrude_coordinates(base.coords, 3, 1 / 3)
+    f = torch.rand(fs.total_dofs, dtype=torch.float64, device="cuda")
+    out = torch.zeros_like(f)
+    k = MassKernel(fs)
+    iterate_columns([fs, xfs], k, [f, coords, out])
+    once = out.clone()
+    iterate_columns([fs, xfs], k, [f, coords, out], schedule="colored")
+    assert _rel(out.cpu().numpy(), 2 * once.cpu().numpy()) < 1e-12
+
+
+@pytest.mark.parametrize("lname", ("CG1xCG1", "P2xP2", "VP1", "CG1xDG1"))
+def test_colored_schedule_is_deterministic(gmesh, lname):
+    from paper_1604_05937_b200.kernels import mass_action
+    fs = _space(gmesh("sq5"), 4, lname)
+    f = torch.rand(fs.total_dofs, dtype=torch.float64, device="cuda")
+    a = mass_action(fs, f, schedule="colored")
+    b = mass_action(fs, f, schedule="colored")
+    assert torch.equal(a, b)
+
+
+def test_residual_field_api_and_conservation(gmesh):
+    from paper_1604_05937_b200.kernels import Field, assemble_residual
+    for lname in sorted(set(LAYOUT_COUNTS) - {"coords", "VP1"}):
+        fs = _space(gmesh("sq5"), 4, lname)
+        b = assemble_residual(fs, Field(fs, np.ones(fs.total_dofs)))
+        assert isinstance(b, Field)
+        assert abs(b.values.sum() - 1.0) < 1e-12, lname
+
+
+# ------------------------------------------------------- BASELINE configs
+def _config_case(name, schedule="auto"):
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator
+    w = configs.WORKLOADS[name]
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    op = MassOperator(fs, quad, schedule=schedule)
+    y = op.apply(torch.from_numpy(x).cuda(), coords)
+    return w, fs, x, y.cpu().numpy()
+
+
+def _oracle_for(w, fs):
+    from paper_1604_05937_b200.quadrature import element_for_layout
+    el = element_for_layout(fs.layout)
+    return oracle.Problem(fs.mesh.base, fs.mesh.layers, fs.layout.counts,
+                          el.tri, el.line, el.ncomp, *w.quad)
+
+
+@pytest.mark.parametrize("name", ("C1", "C2"))
+def test_config_full_size_vs_oracle(name):
+    w, fs, x, y = _config_case(name)
+    ref = _oracle_for(w, fs).assemble_colored(x)
+    assert _rel(y, ref) <= (1e-12 if w.layout.startswith("DG") else 1e-10)
+
+
+def test_config3_reduced_vs_oracle():
+    """C3's space and degree-6 quadrature on a 64^2 base, 12 layers."""
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator
+    w = configs.Workload("C3-small", 64, 12, "P2xP2", (6, 6))
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    for sched in ("auto", "colored"):
+        y = MassOperator(fs, quad, schedule=sched).apply(
+            torch.from_numpy(x).cuda(), coords).cpu().numpy()
+        assert _rel(y, _oracle_for(w, fs).assemble_colored(x)) <= 1e-10
+
+
+@pytest.mark.parametrize("layout", ("CG1xCG1", "DG1xDG1"))
+@pytest.mark.parametrize("ordering", ("rcm", "random"))
+@pytest.mark.parametrize("layers", (1, 2, 5))
+def test_config4_sweep_points_vs_oracle(layout, ordering, layers):
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator
+    w = configs.sweep_workload(layout, layers, ordering)
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    y = MassOperator(fs, quad).apply(torch.from_numpy(x).cuda(),
+                                     coords).cpu().numpy()
+    ref = _oracle_for(w, fs).assemble_colored(x)
+    assert _rel(y, ref) <= (1e-12 if layout.startswith("DG") else 1e-10)
+
+
+def test_config3_full_size_properties():
+    """C3 at full size: schedules agree, conservation, symmetry."""
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator
+    w = configs.WORKLOADS["C3"]
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    xa = torch.from_numpy(x).cuda()
+    ya = MassOperator(fs, quad, schedule="atomic").apply(xa, coords)
+    yc = MassOperator(fs, quad, schedule="colored").apply(xa, coords)
+    assert _rel(ya.cpu().numpy(), yc.cpu().numpy()) <= 1e-10
+    one = torch.ones_like(xa)
+    s = MassOperator(fs, quad).apply(one, coords).sum().item()
+    assert abs(s - 1.0) < 1e-10
+    z = torch.rand_like(xa)
+    op = MassOperator(fs, quad)
+    lhs = torch.dot(z, op.apply(xa, coords)).item()
+    rhs = torch.dot(xa, op.apply(z, coords)).item()
+    assert abs(lhs - rhs) <= 1e-11 * abs(lhs)
