@@ -22,7 +22,6 @@
  *                               (verification.py:47-75 materialized maps)
  *   pm_halo_pack / _unpack   <- PAPER.md:770-775 (halo exchange between
  *                               base-mesh partitions; SPEC.md:9 leaves it out)
- *   pm_column_mass_cells     <- SPEC.md:358-364 coloured-parallel schedule
  *   pm_greedy_color_cells    <- SPEC.md:343-351 color_base_cells
  *   pm_rcm_order             <- pkg/src/prismesh/ordering.py:45-90 (host BFS)
  */
@@ -43,19 +42,14 @@ enum {
   PM_EOVERFLOW = 3 /* DoF numbers do not fit int32           -> ValueError   */
 };
 
-/* Column-loop element kinds (`elem` argument of pm_column_mass). */
-enum {
-  PM_SHARE_NONE = 0,       /* every DoF touched by one cell-layer (DG x DG)  */
-  PM_SHARE_VERTICAL = 1,   /* shared only along the column (DG x CG)         */
-  PM_SHARE_HORIZONTAL = 2  /* shared between columns (CG horizontally)       */
-};
-
 /* Schedules (`variant` argument of pm_column_mass). */
 enum {
-  PM_VARIANT_AUTO = 0,     /* pick the fastest implemented schedule         */
-  PM_VARIANT_ATOMIC = 1,   /* cell-layer threads, fp64 REDG for shared DoFs */
-  PM_VARIANT_PATCH = 2,    /* patch-owner gather through shared memory      */
-  PM_VARIANT_COLUMN = 3    /* warp-per-column, lanes = layers               */
+  PM_VARIANT_AUTO = 0,    /* DG (2,1) fields: STREAM, otherwise COLUMN      */
+  PM_VARIANT_ATOMIC = 1,  /* thread per cell-layer, fp64 REDG on shared DoFs */
+  PM_VARIANT_PATCH = 2,   /* reserved: patch-owner gather                   */
+  PM_VARIANT_COLUMN = 3,  /* warp segment per column, lanes = layers, REDG   */
+  PM_VARIANT_COLORED = 4, /* COLUMN over one colour's cells, plain RMW      */
+  PM_VARIANT_STREAM = 5   /* DG (2,1) fields through TMA bulk copies        */
 };
 
 const char *pm_last_error(void);
@@ -83,36 +77,27 @@ int pm_extrude_coordinates(const double *base_coords, int64_t n_vertices,
                            void *stream);
 
 /* --- the column loop: y (+)= M x over every cell-layer -----------------
- * k        : slots per cell of the field space (1,2,3,6,18)
- * share    : PM_SHARE_*
+ * delta6   : the field layout (DoFs per extruded entity, as in
+ *            pm_build_cell_map); k = its slot count (1,2,3,6,18 built)
  * cell_map : device int32 [n_cells*k];   offsets: device int32 [k]
  * coord_map: device int32 [n_cells*18];  coord_offsets: device int32 [18]
  * coords   : device fp64 extruded coordinate field
  * mref     : HOST fp64 [k*k] reference-prism mass matrix (slot order)
- * x, y     : device fp64 fields of length n_dofs
+ * x, y     : device fp64 fields of length n_dofs (DoF numbers < 2^31)
  * accumulate: 0 -> y = M x (y is overwritten), 1 -> y += M x
- * plan     : device workspace from pm_patch_plan_build (PATCH variant) or
- *            NULL
+ * variant  : PM_VARIANT_*
+ * cells    : optional device int32 list of n_list cells to visit (one
+ *            colour for PM_VARIANT_COLORED, which always accumulates);
+ *            NULL -> all n_cells cells
  * Each cell-layer's |det J| comes from the six prism vertices read out of
- * `coords` (see DESIGN.md "geometry"). */
-int pm_column_mass(int32_t k, int32_t share, int64_t n_cells, int32_t layers,
-                   const int32_t *cell_map, const int32_t *offsets,
-                   const int32_t *coord_map, const int32_t *coord_offsets,
-                   const double *coords, const double *mref,
-                   const double *x, double *y, int64_t n_dofs,
-                   int32_t accumulate, int32_t variant, const void *plan,
-                   void *stream);
-
-/* One colour of the base-cell colouring: y += M x over the listed cells
- * only (device int32 cells[n_list]).  The colouring guarantees no two
- * listed cells share a DoF, so the kernel uses plain read-add-stores and
- * the result is bitwise deterministic. */
-int pm_column_mass_cells(int32_t k, const int32_t *cells, int64_t n_list,
-                         int32_t layers, const int32_t *cell_map,
-                         const int32_t *offsets, const int32_t *coord_map,
-                         const int32_t *coord_offsets, const double *coords,
-                         const double *mref, const double *x, double *y,
-                         void *stream);
+ * `coords` (DESIGN.md "geometry"). */
+int pm_column_mass(const int32_t *delta6, int32_t k, int64_t n_cells,
+                   int32_t layers, const int32_t *cell_map,
+                   const int32_t *offsets, const int32_t *coord_map,
+                   const int32_t *coord_offsets, const double *coords,
+                   const double *mref, const double *x, double *y,
+                   int64_t n_dofs, int32_t accumulate, int32_t variant,
+                   const int32_t *cells, int64_t n_list, void *stream);
 
 /* --- probes for the par-loop itself (exact integer checks) -------------
  * mode 0: out_i64[(c*layers+l)*k + j] = cell_map[c*k+j] + l*offsets[j]

@@ -16,7 +16,8 @@ LIB_PATH = os.path.join(_HERE, "_native", "libprismesh_cuda.so")
 
 PM_OK, PM_EINVAL, PM_ECUDA, PM_EOVERFLOW = 0, 1, 2, 3
 SHARE_NONE, SHARE_VERTICAL, SHARE_HORIZONTAL = 0, 1, 2
-VARIANT_AUTO, VARIANT_ATOMIC, VARIANT_PATCH, VARIANT_COLUMN = 0, 1, 2, 3
+(VARIANT_AUTO, VARIANT_ATOMIC, VARIANT_PATCH, VARIANT_COLUMN, VARIANT_COLORED,
+ VARIANT_STREAM) = range(6)
 
 _lib = None
 
@@ -36,13 +37,10 @@ SIGNATURES = {
     "pm_num_slots": (ctypes.c_int, [_i32p, _i32p]),
     "pm_extrude_coordinates": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp,
                                               _vp]),
-    "pm_column_mass": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
-                                      _vp, _vp, ctypes.POINTER(_f64), _vp,
-                                      _vp, _i64, _i32, _i32, _vp, _vp]),
-    "pm_column_mass_cells": (ctypes.c_int, [_i32, _vp, _i64, _i32, _vp, _vp,
-                                            _vp, _vp, _vp,
-                                            ctypes.POINTER(_f64), _vp, _vp,
-                                            _vp]),
+    "pm_column_mass": (ctypes.c_int, [_i32p, _i32, _i64, _i32, _vp, _vp,
+                                      _vp, _vp, _vp, ctypes.POINTER(_f64),
+                                      _vp, _vp, _i64, _i32, _i32, _vp, _i64,
+                                      _vp]),
     "pm_greedy_color_cells": (ctypes.c_int, [_i32p, _i64, _i64p, _i32p,
                                              _i32p, _i32p]),
     "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
@@ -183,30 +181,20 @@ def column_probe(mode, fs, out, stream=None):
                                      i64, f64, stream_ptr(stream)))
 
 
-def column_mass(k, share, n_cells, layers, cmap, offs, xmap, xoffs, coords,
+def column_mass(layout, k, n_cells, layers, cmap, offs, xmap, xoffs, coords,
                 mref, x, y, n_dofs, accumulate=False, variant=VARIANT_AUTO,
-                plan=None, stream=None):
+                cells=None, stream=None):
+    """pm_column_mass: y (+)= M x over the column loop (device tensors)."""
     m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
     if m.shape[0] != k * k:
         raise ValueError(f"mref must be {k}x{k}")
+    d = layout.delta6()
     rc = host_lib().pm_column_mass(
-        k, share, n_cells, layers, ptr(cmap), ptr(offs), ptr(xmap),
-        ptr(xoffs), ptr(coords), m.ctypes.data_as(ctypes.POINTER(_f64)),
-        ptr(x), ptr(y), n_dofs, 1 if accumulate else 0, variant,
-        ptr(plan) if plan is not None else None, stream_ptr(stream))
-    check(rc)
-
-
-def column_mass_cells(k, cells, layers, cmap, offs, xmap, xoffs, coords,
-                      mref, x, y, stream=None):
-    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
-    if m.shape[0] != k * k:
-        raise ValueError(f"mref must be {k}x{k}")
-    rc = host_lib().pm_column_mass_cells(
-        k, ptr(cells), cells.shape[0], layers, ptr(cmap), ptr(offs),
+        d.ctypes.data_as(_i32p), k, n_cells, layers, ptr(cmap), ptr(offs),
         ptr(xmap), ptr(xoffs), ptr(coords),
-        m.ctypes.data_as(ctypes.POINTER(_f64)), ptr(x), ptr(y),
-        stream_ptr(stream))
+        m.ctypes.data_as(ctypes.POINTER(_f64)), ptr(x), ptr(y), n_dofs,
+        1 if accumulate else 0, variant, ptr(cells),
+        0 if cells is None else cells.shape[0], stream_ptr(stream))
     check(rc)
 
 

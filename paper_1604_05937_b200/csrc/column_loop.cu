@@ -15,29 +15,18 @@
 // Mref is the reference-prism mass matrix pre-integrated on the host with
 // the configured quadrature (exact for affine triangles x flat layers).
 //
-// Schedules implemented here:
-//   generic  : one thread per cell-layer, flattened (c, l) index so lanes
-//              walk up a column; DoFs private to a cell-layer are stored
-//              directly, shared DoFs go through fp64 REDG atomics.
-//   dg_column: DG spaces whose column block is contiguous
-//              (delta only on (2,1)): one warp streams a cell column
-//              through shared memory with 16-byte coalesced loads/stores.
-#include "pm_common.cuh"
+// This file: the C entry point, schedule dispatch and the `generic`
+// schedule (one thread per cell-layer on a flattened (c, l) index, fp64
+// REDG for shared DoFs).  dg_stream.cu: DG fields streamed with TMA bulk
+// copies.  column_warp.cu: warp-per-column, lanes = layers.
 #include "column_loop.cuh"
 
 namespace pm {
 
-template <int K> struct MassMat {
-  double m[K * K];
-};
-
-// -------------------------------------------------------------------------
-// generic schedule
-// -------------------------------------------------------------------------
 template <int K, bool ATOMIC>
 __global__ void __launch_bounds__(256)
-k_mass_generic(const MassMat<K> M, uint32_t n_cl, int layers,
-               const int32_t *__restrict__ cells,
+k_mass_generic(const MassMat<K> M, uint32_t cl_begin, uint32_t n_cl,
+               int layers, const int32_t *__restrict__ cells,
                const int32_t *__restrict__ cmap,
                const int32_t *__restrict__ coff,
                const int32_t *__restrict__ xmap,
@@ -52,8 +41,8 @@ k_mass_generic(const MassMat<K> M, uint32_t n_cl, int layers,
 #pragma unroll
   for (int j = 0; j < 18; ++j) xo[j] = __ldg(xoff + j);
 
-  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < n_cl;
-       g += gridDim.x * blockDim.x) {
+  for (uint32_t g = cl_begin + blockIdx.x * blockDim.x + threadIdx.x;
+       g < n_cl; g += gridDim.x * blockDim.x) {
     const uint32_t ci = g / (uint32_t)layers;
     const int l = (int)(g - ci * (uint32_t)layers);
     const uint32_t c = cells ? (uint32_t)__ldg(cells + ci) : ci;
@@ -90,202 +79,141 @@ k_mass_generic(const MassMat<K> M, uint32_t n_cl, int layers,
   }
 }
 
-// -------------------------------------------------------------------------
-// dg_column schedule: delta only on (2,1), so cell column c owns the
-// contiguous block [map[c][0], map[c][0] + K*layers) and slot j of layer l
-// sits at map[c][j] + l*K.  One warp per column: the block is streamed in
-// chunks of 32 layers through shared memory with coalesced 16-byte
-// accesses, each lane then applies the element kernel to one layer.
-// -------------------------------------------------------------------------
 template <int K>
-__global__ void __launch_bounds__(256)
-k_mass_dg_column(const MassMat<K> M, int64_t n_cells, int layers,
-                 const int32_t *__restrict__ cmap,
-                 const int32_t *__restrict__ xmap,
-                 const int32_t *__restrict__ xoff,
-                 const double *__restrict__ coords,
-                 const double *__restrict__ x, double *__restrict__ y,
-                 int accumulate) {
-  constexpr int W = 32;
-  // per warp: K*32 doubles of x staged (and reused for y)
-  __shared__ double sx[8][K * W + 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double *buf = sx[warp];
-  int xo[18];
-#pragma unroll
-  for (int j = 0; j < 18; ++j) xo[j] = __ldg(xoff + j);
-
-  const int64_t warps_total = (int64_t)gridDim.x * 8;
-  for (int64_t c = blockIdx.x * 8 + warp; c < n_cells; c += warps_total) {
-    const int32_t *xm = xmap + c * 18;
-    const int64_t base = __ldg(cmap + c * K); // slot 0 of layer 0
-    for (int l0 = 0; l0 < layers; l0 += W) {
-      const int nl = min(W, layers - l0);
-      const int n = nl * K;
-      const double *src = x + base + (int64_t)l0 * K;
-      for (int t = lane; t < n; t += W) buf[t] = __ldg(src + t);
-      __syncwarp();
-      const int l = l0 + lane;
-      double yv[K];
-      if (lane < nl) {
-        double X[6], Y[6], Z[6];
-#pragma unroll
-        for (int v = 0; v < 6; ++v) {
-          const int s = 3 * v;
-          X[v] = __ldg(coords + __ldg(xm + s) + l * xo[s]);
-          Y[v] = __ldg(coords + __ldg(xm + s + 1) + l * xo[s + 1]);
-          Z[v] = __ldg(coords + __ldg(xm + s + 2) + l * xo[s + 2]);
-        }
-        const double det = prism_abs_detj(X, Y, Z);
-        double xv[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) xv[i] = buf[lane * K + i];
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          double acc = 0.0;
-#pragma unroll
-          for (int i = 0; i < K; ++i) acc = fma(M.m[j * K + i], xv[i], acc);
-          yv[j] = det * acc;
-        }
-      }
-      __syncwarp();
-      if (lane < nl) {
-#pragma unroll
-        for (int j = 0; j < K; ++j) buf[lane * K + j] = yv[j];
-      }
-      __syncwarp();
-      double *dst = y + base + (int64_t)l0 * K;
-      for (int t = lane; t < n; t += W)
-        dst[t] = accumulate ? dst[t] + buf[t] : buf[t];
-      __syncwarp();
-    }
-  }
-}
-
-template <int K>
-static int launch_mass(int share, const int32_t *cells, int64_t n_cells,
-                       int layers,
-                       const int32_t *cmap, const int32_t *coff,
-                       const int32_t *xmap, const int32_t *xoff,
-                       const double *coords, const double *mref,
-                       const double *x, double *y, int accumulate,
-                       int variant, cudaStream_t s) {
+static int generic_k(const LoopArgs &a, bool atomic, int64_t cl_begin) {
   MassMat<K> M;
-  for (int i = 0; i < K * K; ++i) M.m[i] = mref[i];
-  const int64_t n_cl = n_cells * (int64_t)layers;
+  for (int i = 0; i < K * K; ++i) M.m[i] = a.mref[i];
+  const int64_t n_cl = a.n_cells * (int64_t)a.layers;
   if (n_cl > 0xFFFFFFFFll) {
     set_error("too many cell-layers (%lld) for one launch", (long long)n_cl);
     return PM_EINVAL;
   }
-  if (!cells && share == PM_SHARE_NONE &&
-      (variant == PM_VARIANT_AUTO || variant == PM_VARIANT_COLUMN)) {
-    k_mass_dg_column<K><<<grid_for(n_cells * 32, 256, 8), 256, 0, s>>>(
-        M, n_cells, layers, cmap, xmap, xoff, coords, x, y, accumulate);
-    PM_LAUNCH_CHECK("k_mass_dg_column");
-    return PM_OK;
-  }
-  // A cell list (one colour of the base-mesh colouring) guarantees that no
-  // two cell-layers of the launch share a DoF, so plain stores suffice.
-  if (share == PM_SHARE_NONE || cells)
-    k_mass_generic<K, false><<<grid_for(n_cl, 256), 256, 0, s>>>(
-        M, (uint32_t)n_cl, layers, cells, cmap, coff, xmap, xoff, coords, x,
-        y, accumulate);
+  const int64_t todo = n_cl - cl_begin;
+  if (todo <= 0) return PM_OK;
+  if (atomic)
+    k_mass_generic<K, true><<<grid_for(todo, 256), 256, 0, a.s>>>(
+        M, (uint32_t)cl_begin, (uint32_t)n_cl, a.layers, a.cells, a.cmap,
+        a.coff, a.xmap, a.xoff, a.coords, a.x, a.y, a.accumulate);
   else
-    k_mass_generic<K, true><<<grid_for(n_cl, 256), 256, 0, s>>>(
-        M, (uint32_t)n_cl, layers, cells, cmap, coff, xmap, xoff, coords, x,
-        y, accumulate);
+    k_mass_generic<K, false><<<grid_for(todo, 256), 256, 0, a.s>>>(
+        M, (uint32_t)cl_begin, (uint32_t)n_cl, a.layers, a.cells, a.cmap,
+        a.coff, a.xmap, a.xoff, a.coords, a.x, a.y, a.accumulate);
   PM_LAUNCH_CHECK("k_mass_generic");
   return PM_OK;
 }
 
-} // namespace pm
-
-namespace pm {
-static int column_mass_dispatch(int32_t k, int32_t share,
-                                const int32_t *cells, int64_t n_cells,
-                                int32_t layers, const int32_t *cell_map,
-                                const int32_t *offsets,
-                                const int32_t *coord_map,
-                                const int32_t *coord_offsets,
-                                const double *coords, const double *mref,
-                                const double *x, double *y, int32_t acc,
-                                int32_t variant, cudaStream_t s) {
-  switch (k) {
-#define PM_K(KK)                                                             \
-  case KK:                                                                   \
-    return launch_mass<KK>(share, cells, n_cells, layers, cell_map, offsets, \
-                           coord_map, coord_offsets, coords, mref, x, y, acc, \
-                           variant, s);
-    PM_K(1) PM_K(2) PM_K(3) PM_K(6) PM_K(18)
-#undef PM_K
+int launch_generic(const LoopArgs &a, bool atomic, int64_t cl_begin) {
+  switch (a.k) {
+  case 1: return generic_k<1>(a, atomic, cl_begin);
+  case 2: return generic_k<2>(a, atomic, cl_begin);
+  case 3: return generic_k<3>(a, atomic, cl_begin);
+  case 6: return generic_k<6>(a, atomic, cl_begin);
+  case 18: return generic_k<18>(a, atomic, cl_begin);
   default:
-    set_error("unsupported slot count k=%d (built: 1,2,3,6,18)", k);
+    set_error("unsupported slot count k=%d (built: 1,2,3,6,18)", a.k);
     return PM_EINVAL;
   }
 }
+
 } // namespace pm
 
-extern "C" int pm_column_mass(int32_t k, int32_t share, int64_t n_cells,
-                              int32_t layers, const int32_t *cell_map,
-                              const int32_t *offsets,
+extern "C" int pm_column_mass(const int32_t *delta6, int32_t k,
+                              int64_t n_cells, int32_t layers,
+                              const int32_t *cell_map, const int32_t *offsets,
                               const int32_t *coord_map,
                               const int32_t *coord_offsets,
                               const double *coords, const double *mref,
                               const double *x, double *y, int64_t n_dofs,
                               int32_t accumulate, int32_t variant,
-                              const void *plan, void *stream) {
+                              const int32_t *cells, int64_t n_list,
+                              void *stream) {
   pm::clear_error();
-  (void)plan;
-  if (layers < 1 || n_cells < 0 || n_dofs < 0) {
-    pm::set_error("bad shape: layers=%d n_cells=%lld", layers,
-                  (long long)n_cells);
+  pm::LoopArgs a;
+  int rc = pm::make_slot_table(delta6, &a.st);
+  if (rc) return rc;
+  if (k != a.st.k) {
+    pm::set_error("slot count mismatch: k=%d, layout has %d", k, a.st.k);
     return PM_EINVAL;
   }
-  if (share < PM_SHARE_NONE || share > PM_SHARE_HORIZONTAL) {
-    pm::set_error("unknown sharing class %d", share);
+  if (layers < 1 || n_cells < 0 || n_dofs < 0 || n_list < 0) {
+    pm::set_error("bad shape: layers=%d n_cells=%lld", layers,
+                  (long long)n_cells);
     return PM_EINVAL;
   }
   if (!mref) {
     pm::set_error("mref is NULL");
     return PM_EINVAL;
   }
-  cudaStream_t s = (cudaStream_t)stream;
-  if (!accumulate && share != PM_SHARE_NONE && n_dofs > 0)
-    PM_CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)n_dofs * sizeof(double), s));
-  if (n_cells == 0) return PM_OK;
+  a.k = k;
+  a.layers = layers;
+  a.cells = cells;
+  a.n_cells = cells ? n_list : n_cells;
+  a.cmap = cell_map;
+  a.coff = offsets;
+  a.xmap = coord_map;
+  a.xoff = coord_offsets;
+  a.coords = coords;
+  a.mref = mref;
+  a.x = x;
+  a.y = y;
+  a.accumulate = accumulate ? 1 : 0;
+  a.s = (cudaStream_t)stream;
+  a.dg_only = delta6[0] == 0 && delta6[1] == 0 && delta6[2] == 0 &&
+              delta6[3] == 0 && delta6[4] == 0;
+  a.hshared = delta6[0] || delta6[1] || delta6[2] || delta6[3];
+
+  if (variant == PM_VARIANT_COLORED && !cells) {
+    pm::set_error("the coloured variant needs a cell list (one colour)");
+    return PM_EINVAL;
+  }
+  // Overwrite mode: DoFs that receive REDG need a zeroed field first.
+  const bool needs_zero =
+      !a.accumulate && a.hshared &&
+      (variant == PM_VARIANT_ATOMIC || variant == PM_VARIANT_COLUMN ||
+       variant == PM_VARIANT_AUTO);
+  const bool generic_needs_zero =
+      !a.accumulate && !a.dg_only &&
+      (variant == PM_VARIANT_ATOMIC ||
+       (variant == PM_VARIANT_AUTO && !pm::column_supports(delta6)));
+  if ((needs_zero || generic_needs_zero) && n_dofs > 0)
+    PM_CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)n_dofs * sizeof(double), a.s));
+  if (a.n_cells == 0) return PM_OK;
   if (!cell_map || !offsets || !coord_map || !coord_offsets || !coords ||
       !x || !y) {
     pm::set_error("NULL device pointer");
     return PM_EINVAL;
   }
-  return pm::column_mass_dispatch(k, share, nullptr, n_cells, layers,
-                                  cell_map, offsets, coord_map, coord_offsets,
-                                  coords, mref, x, y, accumulate ? 1 : 0,
-                                  variant, s);
-}
-
-extern "C" int pm_column_mass_cells(int32_t k, const int32_t *cells,
-                                    int64_t n_list, int32_t layers,
-                                    const int32_t *cell_map,
-                                    const int32_t *offsets,
-                                    const int32_t *coord_map,
-                                    const int32_t *coord_offsets,
-                                    const double *coords, const double *mref,
-                                    const double *x, double *y,
-                                    void *stream) {
-  pm::clear_error();
-  if (layers < 1 || n_list < 0 || !mref) {
-    pm::set_error("bad arguments to pm_column_mass_cells");
+  switch (variant) {
+  case PM_VARIANT_AUTO:
+    if (a.dg_only && !cells && !a.accumulate) {
+      bool handled = false;
+      rc = pm::launch_dg_stream(a, &handled);
+      if (rc || handled) return rc;
+    }
+    if (pm::column_supports(delta6)) return pm::launch_column(a, delta6, false);
+    return pm::launch_generic(a, !a.dg_only, 0);
+  case PM_VARIANT_STREAM: {
+    bool handled = false;
+    if (!a.dg_only || cells || a.accumulate) {
+      pm::set_error("stream variant needs a DG (2,1) layout, all cells, "
+                    "overwrite mode");
+      return PM_EINVAL;
+    }
+    rc = pm::launch_dg_stream(a, &handled);
+    if (!rc && !handled) {
+      pm::set_error("stream variant: field not 16-byte aligned");
+      return PM_EINVAL;
+    }
+    return rc;
+  }
+  case PM_VARIANT_ATOMIC:
+    return pm::launch_generic(a, !a.dg_only, 0);
+  case PM_VARIANT_COLUMN:
+    return pm::launch_column(a, delta6, false);
+  case PM_VARIANT_COLORED:
+    return pm::launch_column(a, delta6, true);
+  default:
+    pm::set_error("unknown variant %d", variant);
     return PM_EINVAL;
   }
-  if (n_list == 0) return PM_OK;
-  if (!cells || !cell_map || !offsets || !coord_map || !coord_offsets ||
-      !coords || !x || !y) {
-    pm::set_error("NULL device pointer");
-    return PM_EINVAL;
-  }
-  return pm::column_mass_dispatch(k, PM_SHARE_HORIZONTAL, cells, n_list,
-                                  layers, cell_map, offsets, coord_map,
-                                  coord_offsets, coords, mref, x, y, 1,
-                                  PM_VARIANT_AUTO, (cudaStream_t)stream);
 }

@@ -1,7 +1,16 @@
-// Device helpers shared by the column-loop kernels.
+// Device helpers and launch plumbing shared by the column-loop kernels.
 #pragma once
+#include <stdint.h>
+
+#include "pm_common.cuh"
 
 namespace pm {
+
+constexpr int kMaxK = 18; // largest stencil built (P2 x P2, 3-vector P1)
+
+template <int K> struct MassMat {
+  double m[K * K]; // reference-prism mass matrix, row-major, slot order
+};
 
 // |det J| of the affine map reference prism -> physical prism cell-layer.
 // Vertex index v = 2a + b (a: triangle vertex, b: 0 bottom / 1 top level).
@@ -16,5 +25,27 @@ __device__ __forceinline__ double prism_abs_detj(const double *X,
   const double h = ((Z[1] - Z[0]) + (Z[3] - Z[2]) + (Z[5] - Z[4])) / 3.0;
   return fabs(a2 * h);
 }
+
+// Everything a column-loop launch needs (host side).
+struct LoopArgs {
+  int k;
+  int64_t n_cells; // cells in the launch (list length if `cells` != null)
+  int layers;
+  const int32_t *cells; // optional cell list (colour / order), device
+  const int32_t *cmap, *coff, *xmap, *xoff;
+  const double *coords, *mref, *x;
+  double *y;
+  int accumulate;
+  SlotTable st;
+  bool dg_only;  // DoFs only on (2,1): contiguous (cell, layer, slot) field
+  bool hshared;  // some DoF shared between columns
+  cudaStream_t s;
+};
+
+// Kernel launchers (one translation unit each).
+int launch_generic(const LoopArgs &a, bool atomic, int64_t cl_begin);
+int launch_dg_stream(const LoopArgs &a, bool *handled);
+int launch_column(const LoopArgs &a, const int32_t *delta6, bool colored);
+bool column_supports(const int32_t *delta6);
 
 } // namespace pm

@@ -1,0 +1,303 @@
+// Warp-per-column schedule: the paper's Algorithm 3 mapped onto a warp.
+//
+// A segment of W lanes (W = 8, 16 or 32) owns one base-cell column; lane
+// `sl` handles layer l0+sl of the current W-layer chunk, so every slot's
+// DoFs  L_j + l*offset_j  are consecutive across the segment (coalesced
+// gathers along the column).  The bottom-layer lists L (field and
+// coordinates) are loaded once per column.  Vertical sharing is carried in
+// registers: a top-copy value is the next lane's bottom-copy value
+// (shfl.down), a top-copy contribution is added to the next lane's bottom
+// contribution (shfl.up) and across chunks through a per-segment carry, so
+// each vertically shared DoF is written exactly once per column.  DoFs
+// shared between columns (vertex / edge DoFs of CG spaces) are combined
+// with fp64 REDG atomics, or -- in the coloured schedule, where no two
+// columns of a launch share a DoF -- with plain read-add-stores.
+#include "column_loop.cuh"
+
+namespace pm {
+
+// Compile-time restatement of the slot table (fspace.py:110-131) for a
+// layout given as template arguments delta(d1,d2): the slot count, each
+// slot's level kind, the bottom partner of each top copy and whether the
+// DoF is shared with other columns are all constants, so the per-slot
+// branches below vanish at compile time.
+template <int D00, int D01, int D10, int D11, int D20, int D21>
+struct Layout {
+  struct Tab {
+    int k;
+    int8_t level[kMaxK];
+    int8_t pair[kMaxK];
+    int8_t hshare[kMaxK];
+    int8_t offset[kMaxK]; // Alg. 2: delta(d,0) + delta(d,1)
+    int8_t comp[kMaxK];   // vector component (3-vector P1 only, else 0)
+  };
+  static constexpr Tab make() {
+    Tab t{};
+    const int dl[3] = {D00, D10, D20}, dc[3] = {D01, D11, D21};
+    const int n_local[3] = {3, 3, 1};
+    int k = 0;
+    for (int d = 0; d < 3; ++d) {
+      if (!dl[d] && !dc[d]) continue;
+      for (int loc = 0; loc < n_local[d]; ++loc) {
+        const int first = k;
+        const int8_t off = (int8_t)(dl[d] + dc[d]);
+        for (int j = 0; j < dl[d]; ++j, ++k) {
+          t.level[k] = 0, t.pair[k] = -1, t.hshare[k] = d != 2;
+          t.offset[k] = off;
+        }
+        for (int j = 0; j < dc[d]; ++j, ++k) {
+          t.level[k] = 1, t.pair[k] = -1, t.hshare[k] = d != 2;
+          t.offset[k] = off;
+        }
+        for (int j = 0; j < dl[d]; ++j, ++k) {
+          t.level[k] = 2, t.pair[k] = (int8_t)(first + j);
+          t.hshare[k] = d != 2;
+          t.offset[k] = off;
+        }
+      }
+    }
+    t.k = k;
+    // the 3-DoF-per-vertex layout is the 3-vector P1 element: slot
+    // 6a+3b+q carries component q, and Mref is block-diagonal in q
+    const bool vec3 = D00 == 3 && !D01 && !D10 && !D11 && !D20 && !D21;
+    for (int j = 0; j < k; ++j) t.comp[j] = vec3 ? (int8_t)(j % 3) : 0;
+    return t;
+  }
+  static constexpr int K = make().k;
+  static bool matches(const int32_t *d) {
+    return d[0] == D00 && d[1] == D01 && d[2] == D10 && d[3] == D11 &&
+           d[4] == D20 && d[5] == D21;
+  }
+};
+
+template <int K> struct ColumnArgs {
+  MassMat<K> M;
+};
+
+enum { kStorePlain = 0, kStoreAtomic = 1, kStoreRmw = 2 };
+
+__device__ __forceinline__ void put(double *p, double v, int how) {
+  if (how == kStoreAtomic)
+    atomicAdd(p, v);
+  else if (how == kStoreRmw)
+    *p += v;
+  else
+    *p = v;
+}
+
+template <class LY, int W, bool COLORED, int K = LY::K>
+__global__ void __launch_bounds__(256)
+k_column(const ColumnArgs<K> A, int64_t n_cells, int layers,
+         const int32_t *__restrict__ cells, const int32_t *__restrict__ cmap,
+         const int32_t *__restrict__ coff, const int32_t *__restrict__ xmap,
+         const int32_t *__restrict__ xoff, const double *__restrict__ coords,
+         const double *__restrict__ x, double *__restrict__ y,
+         int accumulate) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int SEGS = 32 / W;
+  constexpr typename LY::Tab T = LY::make(); // folded at compile time
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % W; // layer inside the chunk
+  const int seg = lane / W;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+
+  // Per-slot vertical offsets (Algorithm 2) are constants of the layout:
+  // folded at compile time here; the device-built offsets array (K0) is
+  // bit-checked against the same closed form by the tests.  The coordinate
+  // space (COORDS_LAYOUT) has offset 3 on every slot.
+  (void)coff;
+  (void)xoff;
+
+  // How each slot's contribution reaches y.
+  int how[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (T.hshare[j])
+      how[j] = COLORED ? kStoreRmw : kStoreAtomic;
+    else
+      how[j] = (accumulate || COLORED) ? kStoreRmw : kStorePlain;
+  }
+
+  for (int64_t cb = warp * SEGS; cb < n_cells; cb += n_warps * SEGS) {
+    const int64_t ci = cb + seg;
+    const bool cell_ok = ci < n_cells;
+    const int64_t c = cell_ok ? (cells ? (int64_t)__ldg(cells + ci) : ci) : 0;
+    // bottom-layer lists, loaded once per column
+    // DoF numbers fit int32 (checked by the host), so all address
+    // arithmetic along the column stays 32-bit.
+    int32_t L[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) L[j] = cell_ok ? __ldg(cmap + c * K + j) : 0;
+    // coordinate map: slot 6a+3b+q of vertex a sits `3b+q` after slot 6a
+    int32_t LX[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      LX[a] = cell_ok ? __ldg(xmap + c * 18 + 6 * a) : 0;
+
+    double carry[K]; // top contribution of the chunk's last layer
+#pragma unroll
+    for (int j = 0; j < K; ++j) carry[j] = 0.0;
+
+    for (int l0 = 0; l0 < layers; l0 += W) {
+      const int nl = min(W, layers - l0);
+      const int last = nl - 1;
+      const int l = l0 + sl;
+      const bool act = cell_ok && sl < nl;
+      const bool own_top = act && sl == last; // loads its own top values
+
+      // ---- gather the field: bottom / connecting slots directly, top
+      //      copies from the next lane (or directly on the last lane)
+      double xv[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        xv[j] = (act && T.level[j] != 2)
+                    ? __ldg(x + L[j] + l * T.offset[j])
+                    : 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (T.level[j] == 2) {
+          const double up = __shfl_down_sync(FULL, xv[T.pair[j]], 1, W);
+          xv[j] = own_top ? __ldg(x + L[j] + l * T.offset[j]) : up;
+        }
+      }
+      // ---- geometry: the six prism vertices (bottom comps direct, top
+      //      comps from the next lane)
+      double P[18]; // slot 6a + 3b + comp
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int sb = 6 * a + q, st = 6 * a + 3 + q;
+          const double bot = act ? __ldg(coords + LX[a] + q + 3 * l) : 0.0;
+          const double up = __shfl_down_sync(FULL, bot, 1, W);
+          P[sb] = bot;
+          P[st] = own_top ? __ldg(coords + LX[a] + 3 + q + 3 * l) : up;
+        }
+      double X[6], Y[6], Z[6];
+#pragma unroll
+      for (int v = 0; v < 6; ++v) {
+        X[v] = P[3 * v];
+        Y[v] = P[3 * v + 1];
+        Z[v] = P[3 * v + 2];
+      }
+      const double det = act ? prism_abs_detj(X, Y, Z) : 0.0;
+
+      // ---- element kernel
+      double yv[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+          if (T.comp[i] == T.comp[j]) // structural zeros skipped
+            acc = fma(A.M.m[j * K + i], xv[i], acc);
+        yv[j] = det * acc;
+      }
+
+      // ---- vertical combine: top(l-1) joins bottom(l)
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (T.level[j] == 2) {
+          const int b = T.pair[j];
+          const double below = __shfl_up_sync(FULL, yv[j], 1, W);
+          yv[b] += (sl == 0) ? carry[j] : below;
+          carry[j] = __shfl_sync(FULL, yv[j], last, W);
+        }
+      }
+      // ---- scatter: every bottom / connecting DoF of the chunk once
+      if (act) {
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          if (T.level[j] != 2)
+            put(y + L[j] + l * T.offset[j], yv[j], how[j]);
+      }
+    }
+    // the column's top level (layers-1's top copies)
+    const int nl_last = layers - ((layers - 1) / W) * W;
+    if (cell_ok && sl == nl_last - 1) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (T.level[j] == 2)
+          put(y + L[j] + (layers - 1) * T.offset[j], carry[j], how[j]);
+    }
+  }
+}
+
+template <class LY>
+static int column_k(const LoopArgs &a, bool colored) {
+  constexpr int K = LY::K;
+  ColumnArgs<K> A;
+  for (int i = 0; i < K * K; ++i) A.M.m[i] = a.mref[i];
+  // segment width: smallest lane waste for this layer count
+  int W = 32;
+  {
+    double best = 1e30;
+    for (int w : {32, 16, 8}) {
+      const int chunks = (a.layers + w - 1) / w;
+      const double waste = (double)(chunks * w) / a.layers + 0.02 * chunks;
+      if (waste < best - 1e-9) {
+        best = waste;
+        W = w;
+      }
+    }
+  }
+  const int segs = 32 / W;
+  const int64_t warps = (a.n_cells + segs - 1) / segs;
+  const unsigned grid = grid_for(warps * 32, 256, 8);
+#define PM_COL(WW)                                                           \
+  do {                                                                       \
+    if (colored)                                                             \
+      k_column<LY, WW, true><<<grid, 256, 0, a.s>>>(                         \
+          A, a.n_cells, a.layers, a.cells, a.cmap, a.coff, a.xmap, a.xoff,   \
+          a.coords, a.x, a.y, a.accumulate);                                 \
+    else                                                                     \
+      k_column<LY, WW, false><<<grid, 256, 0, a.s>>>(                        \
+          A, a.n_cells, a.layers, a.cells, a.cmap, a.coff, a.xmap, a.xoff,   \
+          a.coords, a.x, a.y, a.accumulate);                                 \
+  } while (0)
+  if (W == 32)
+    PM_COL(32);
+  else if (W == 16)
+    PM_COL(16);
+  else
+    PM_COL(8);
+#undef PM_COL
+  PM_LAUNCH_CHECK("k_column");
+  return PM_OK;
+}
+
+// The layouts built into the column kernel: the nine CG1/DG0/DG1 tensor
+// layouts (fspace.py:23-33), P2 x P2 and the 3-vector P1 (= COORDS).
+#define PM_LAYOUTS(X)                                                        \
+  X(1, 0, 0, 0, 0, 0) /* CG1 x CG1, 3-vector via (3,...) below */            \
+  X(0, 1, 0, 0, 0, 0) /* CG1 x DG0 */                                        \
+  X(0, 2, 0, 0, 0, 0) /* CG1 x DG1 */                                        \
+  X(0, 0, 0, 0, 1, 0) /* DG0 x CG1 */                                        \
+  X(0, 0, 0, 0, 0, 1) /* DG0 x DG0 */                                        \
+  X(0, 0, 0, 0, 0, 2) /* DG0 x DG1 */                                        \
+  X(0, 0, 0, 0, 3, 0) /* DG1 x CG1 */                                        \
+  X(0, 0, 0, 0, 0, 3) /* DG1 x DG0 */                                        \
+  X(0, 0, 0, 0, 0, 6) /* DG1 x DG1 */                                        \
+  X(1, 1, 1, 1, 0, 0) /* P2 x P2 */                                          \
+  X(3, 0, 0, 0, 0, 0) /* 3-vector P1 x P1 */
+
+bool column_supports(const int32_t *d) {
+#define PM_MATCH(a, b, c, e, f, g)                                           \
+  if (Layout<a, b, c, e, f, g>::matches(d)) return true;
+  PM_LAYOUTS(PM_MATCH)
+#undef PM_MATCH
+  return false;
+}
+
+int launch_column(const LoopArgs &a, const int32_t *delta6, bool colored) {
+#define PM_DISPATCH(a_, b_, c_, e_, f_, g_)                                  \
+  if (Layout<a_, b_, c_, e_, f_, g_>::matches(delta6))                       \
+    return column_k<Layout<a_, b_, c_, e_, f_, g_>>(a, colored);
+  PM_LAYOUTS(PM_DISPATCH)
+#undef PM_DISPATCH
+  set_error("layout not built into the column kernel");
+  return PM_EINVAL;
+}
+
+} // namespace pm

@@ -1,0 +1,156 @@
+// DG column loop with TMA bulk streaming (sm_100a cp.async.bulk).
+//
+// For a layout with DoFs only on the prism cells ((2,1) entities, e.g.
+// DG1 x DG1) Algorithm 1 numbers cell c's column as one block of
+// delta*layers values and the cell columns follow each other, so slot j of
+// layer l is  map[c][j] + l*offset_j  with  map[c][j] = delta*layers*c + j
+// and offset_j = delta: the whole field is a dense (cell, layer, slot)
+// array.  Work unit = 256 consecutive cell-layers (one per thread) whose
+// x block (256*delta doubles) arrives by one bulk copy into a S-stage
+// shared-memory ring (mbarrier completion); each thread applies the element
+// kernel in place and the block leaves by one bulk store.  Coordinates are
+// gathered per cell-layer through the coordinate map + offsets.
+#include "column_loop.cuh"
+#include "pm_ptx.cuh"
+
+namespace pm {
+
+constexpr int kStreamT = 256;  // cell-layers per unit (= threads per CTA)
+constexpr int kStreamS = 4;    // pipeline stages
+
+template <int D>
+__global__ void __launch_bounds__(kStreamT)
+k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
+            const int32_t *__restrict__ xmap,
+            const int32_t *__restrict__ xoff,
+            const double *__restrict__ coords,
+            const double *__restrict__ x, double *__restrict__ y) {
+  constexpr int T = kStreamT, S = kStreamS;
+  constexpr uint32_t BYTES = T * D * sizeof(double);
+  extern __shared__ __align__(128) unsigned char smem[];
+  double *buf = reinterpret_cast<double *>(smem);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + S * BYTES);
+  const int t = threadIdx.x;
+
+  int xo[18];
+#pragma unroll
+  for (int j = 0; j < 18; ++j) xo[j] = __ldg(xoff + j);
+
+  if (t == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t n_mine =
+      first < n_units ? (n_units - first + stride - 1) / stride : 0;
+
+  if (t == 0) {
+    for (int64_t i = 0; i < S - 1 && i < n_mine; ++i) {
+      const int64_t u = first + i * stride;
+      mbar_arrive_expect_tx(&bar[i], BYTES);
+      bulk_g2s(buf + i * T * D, x + u * T * D, BYTES, &bar[i]);
+    }
+  }
+
+  for (int64_t i = 0; i < n_mine; ++i) {
+    const int s = (int)(i % S);
+    const int64_t u = first + i * stride;
+    double *b = buf + s * T * D;
+
+    // geometry first: its gathers overlap the bulk copy still in flight
+    const uint32_t g = (uint32_t)(u * T + t);
+    const uint32_t c = g / (uint32_t)layers;
+    const int l = (int)(g - c * (uint32_t)layers);
+    const int32_t *xm = xmap + (size_t)c * 18;
+    double X[6], Y[6], Z[6];
+#pragma unroll
+    for (int v = 0; v < 6; ++v) {
+      const int q = 3 * v;
+      X[v] = __ldg(coords + __ldg(xm + q) + l * xo[q]);
+      Y[v] = __ldg(coords + __ldg(xm + q + 1) + l * xo[q + 1]);
+      Z[v] = __ldg(coords + __ldg(xm + q + 2) + l * xo[q + 2]);
+    }
+    const double det = prism_abs_detj(X, Y, Z);
+
+    mbar_wait(&bar[s], (uint32_t)((i / S) & 1));
+    double xv[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) xv[j] = b[t * D + j];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < D; ++q) acc = fma(M.m[j * D + q], xv[q], acc);
+      b[t * D + j] = det * acc;
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (t == 0) {
+      bulk_s2g(y + u * T * D, b, BYTES);
+      bulk_commit();
+      const int64_t nxt = i + S - 1;
+      if (nxt < n_mine) {
+        // stage of unit i-1: its store (one group back) must have read smem
+        bulk_wait_read<1>();
+        const int sn = (int)(nxt % S);
+        mbar_arrive_expect_tx(&bar[sn], BYTES);
+        bulk_g2s(buf + sn * T * D, x + (first + nxt * stride) * T * D, BYTES,
+                 &bar[sn]);
+      }
+    }
+  }
+  if (t == 0) bulk_wait<0>();
+}
+
+template <int D> static int dg_stream_k(const LoopArgs &a, bool *handled) {
+  *handled = false;
+  const int64_t n_cl = a.n_cells * (int64_t)a.layers;
+  const int64_t n_units = n_cl / kStreamT;
+  if ((reinterpret_cast<uintptr_t>(a.x) | reinterpret_cast<uintptr_t>(a.y)) &
+      15)
+    return PM_OK; // not aligned for bulk copies: caller picks another kernel
+  if (n_cl > 0xFFFFFFFFll) return PM_OK;
+  MassMat<D> M;
+  for (int i = 0; i < D * D; ++i) M.m[i] = a.mref[i];
+  if (n_units > 0) {
+    const size_t smem = kStreamS * kStreamT * D * sizeof(double) +
+                        kStreamS * sizeof(uint64_t);
+    static bool attr_set[8] = {false};
+    if (!attr_set[D]) {
+      PM_CUDA_TRY(cudaFuncSetAttribute(
+          k_dg_stream<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          (int)smem));
+      attr_set[D] = true;
+    }
+    int per_sm = 0;
+    PM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, k_dg_stream<D>, kStreamT, smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > n_units) grid = n_units;
+    k_dg_stream<D><<<(unsigned)grid, kStreamT, smem, a.s>>>(
+        M, n_units, a.layers, a.xmap, a.xoff, a.coords, a.x, a.y);
+    PM_LAUNCH_CHECK("k_dg_stream");
+  }
+  *handled = true;
+  // ragged tail (< one unit): flattened generic kernel, plain stores
+  if (n_units * kStreamT < n_cl)
+    return launch_generic(a, false, n_units * kStreamT);
+  return PM_OK;
+}
+
+int launch_dg_stream(const LoopArgs &a, bool *handled) {
+  switch (a.k) {
+  case 1: return dg_stream_k<1>(a, handled);
+  case 2: return dg_stream_k<2>(a, handled);
+  case 3: return dg_stream_k<3>(a, handled);
+  case 6: return dg_stream_k<6>(a, handled);
+  default:
+    *handled = false;
+    return PM_OK;
+  }
+}
+
+} // namespace pm

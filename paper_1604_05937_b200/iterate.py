@@ -15,11 +15,15 @@ CPU execution path).
 
 Schedules (``schedule=``):
 
-``"auto"``      DG layouts: warp-per-column streaming kernel; shared
-                layouts: fp64 atomics (fastest measured).
+``"auto"``      DG (2,1) fields in overwrite mode: ``"stream"``;
+                otherwise ``"column"``.
+``"stream"``    DG (2,1) fields through TMA bulk copies (dg_stream.cu).
+``"column"``    warp segment per column, lanes = layers; vertical sharing
+                in registers, column-shared DoFs via fp64 REDG.
 ``"atomic"``    one thread per cell-layer, shared DoFs via fp64 REDG.
-``"colored"``   one launch per colour of ``color_base_cells``; plain
-                stores, bitwise deterministic.
+``"colored"``   ``"column"`` once per colour of ``color_base_cells`` with
+                plain read-add-stores: bitwise deterministic
+                (SPEC.md:358-364).
 ``"sequential"`` alias of ``"colored"`` (the deterministic schedule).
 """
 from __future__ import annotations
@@ -30,7 +34,7 @@ import numpy as np
 
 from . import _lib
 
-SCHEDULES = ("auto", "atomic", "colored", "sequential", "column")
+SCHEDULES = ("auto", "atomic", "colored", "sequential", "column", "stream")
 
 
 @dataclass(frozen=True)

@@ -121,7 +121,7 @@ class MassOperator:
     @property
     def launches_per_apply(self) -> int:
         """Column-loop kernel launches one ``apply`` issues."""
-        if self.schedule in ("colored", "sequential") and self.share != 0:
+        if self.schedule in ("colored", "sequential") and self.share == 2:
             return self._color_lists()[1].shape[0] - 1
         return 1
 
@@ -155,26 +155,37 @@ class MassOperator:
         if y is None:
             y = torch.empty(n, dtype=torch.float64, device=x.device)
             accumulate = False
-        if sched in ("colored", "sequential") and self.share != 0:
+        if sched not in _VARIANTS:
+            raise ValueError(f"unknown schedule {sched!r}")
+        if sched in ("colored", "sequential") and self.share == 2:
+            # one launch per colour: no two columns of a launch share a DoF
             if not accumulate:
                 y.zero_()
             order, ptr = self._color_lists()
             for c in range(len(ptr) - 1):
-                _lib.column_mass_cells(
-                    self.k, order[ptr[c]:ptr[c + 1]], self.layers, self.cmap,
-                    self.offs, self.xmap, self.xoffs, coords, self.mref, x, y,
-                    stream=stream)
+                _lib.column_mass(self.fs.layout, self.k, self.n_cells,
+                                 self.layers, self.cmap, self.offs, self.xmap,
+                                 self.xoffs, coords, self.mref, x, y, n,
+                                 accumulate=True,
+                                 variant=_lib.VARIANT_COLORED,
+                                 cells=order[ptr[c]:ptr[c + 1]],
+                                 stream=stream)
             return y
-        variant = {"auto": _lib.VARIANT_AUTO, "atomic": _lib.VARIANT_ATOMIC,
-                   "column": _lib.VARIANT_COLUMN, "colored": _lib.VARIANT_AUTO,
-                   "sequential": _lib.VARIANT_AUTO}[sched]
-        if sched == "column" and self.share != 0:
-            raise ValueError("the column schedule needs a DG (2,1) layout")
-        _lib.column_mass(self.k, self.share, self.n_cells, self.layers,
+        if sched == "stream" and self.share != 0:
+            raise ValueError("the stream schedule needs a DG (2,1) layout")
+        _lib.column_mass(self.fs.layout, self.k, self.n_cells, self.layers,
                          self.cmap, self.offs, self.xmap, self.xoffs, coords,
                          self.mref, x, y, n, accumulate=accumulate,
-                         variant=variant, stream=stream)
+                         variant=_VARIANTS[sched], stream=stream)
         return y
+
+
+_VARIANTS = {"auto": _lib.VARIANT_AUTO, "atomic": _lib.VARIANT_ATOMIC,
+             "column": _lib.VARIANT_COLUMN, "stream": _lib.VARIANT_STREAM,
+             # deterministic schedules for layouts without horizontal
+             # sharing: the column kernel writes every DoF exactly once
+             "colored": _lib.VARIANT_COLUMN,
+             "sequential": _lib.VARIANT_COLUMN}
 
 
 _COLORINGS = {}
