@@ -18,6 +18,8 @@
  *   pm_column_mass           <- SPEC.md:333-341 iterate_columns driving
  *                               SPEC.md:412-420 assemble_residual
  *                               (Algorithm 3)
+ *   pm_column_mass_patch     <- same, race-free owner-computes schedule
+ *                               replacing SPEC.md:343-364 colouring
  *   pm_column_probe          <- SPEC.md:338-340 counting / gather kernels
  *                               (verification.py:47-75 materialized maps)
  *   pm_halo_pack / _unpack   <- PAPER.md:770-775 (halo exchange between
@@ -46,7 +48,7 @@ enum {
 enum {
   PM_VARIANT_AUTO = 0,    /* DG (2,1) fields: STREAM, otherwise COLUMN      */
   PM_VARIANT_ATOMIC = 1,  /* thread per cell-layer, fp64 REDG on shared DoFs */
-  PM_VARIANT_PATCH = 2,   /* reserved: patch-owner gather                   */
+  PM_VARIANT_PATCH = 2,   /* patch-owner gather (pm_column_mass_patch)      */
   PM_VARIANT_COLUMN = 3,  /* warp segment per column, lanes = layers, REDG   */
   PM_VARIANT_COLORED = 4, /* COLUMN over one colour's cells, plain RMW      */
   PM_VARIANT_STREAM = 5   /* DG (2,1) fields through TMA bulk copies        */
@@ -98,6 +100,25 @@ int pm_column_mass(const int32_t *delta6, int32_t k, int64_t n_cells,
                    const double *mref, const double *x, double *y,
                    int64_t n_dofs, int32_t accumulate, int32_t variant,
                    const int32_t *cells, int64_t n_list, void *stream);
+
+/* Patch-owner schedule (PM_VARIANT_PATCH) for CG layouts whose DoFs live
+ * on vertex / edge columns: y = M x (overwrite), bitwise deterministic,
+ * no atomics.  The plan arrays (device) come from
+ * paper_1604_05937_b200/schedule.py: patch -> visited cells (grouped by
+ * colour: color_ptr[p*(n_colors+1)+c]), patch -> local entities (owned
+ * first; codes v or n_vertices+e), per visited cell the 16-bit local ids
+ * of its 3 vertices (+3 edges).  chunk = layers per chunk (8, 16, 32). */
+int pm_column_mass_patch(const int32_t *delta6, int32_t k, int64_t n_vertices,
+                         int64_t n_edges, int32_t layers,
+                         const int32_t *cell_map, const int32_t *coord_map,
+                         const double *coords, const double *mref,
+                         const double *x, double *y, int64_t n_patches,
+                         int32_t n_colors, int32_t chunk, int32_t max_local,
+                         int32_t max_owned, const int32_t *cell_ptr,
+                         const int32_t *cells, const int32_t *color_ptr,
+                         const int32_t *ent_ptr, const int32_t *owned,
+                         const int32_t *ents, const uint16_t *lents,
+                         void *stream);
 
 /* --- probes for the par-loop itself (exact integer checks) -------------
  * mode 0: out_i64[(c*layers+l)*k + j] = cell_map[c*k+j] + l*offsets[j]

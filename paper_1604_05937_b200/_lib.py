@@ -43,6 +43,12 @@ SIGNATURES = {
                                       _vp]),
     "pm_greedy_color_cells": (ctypes.c_int, [_i32p, _i64, _i64p, _i32p,
                                              _i32p, _i32p]),
+    "pm_column_mass_patch": (ctypes.c_int, [_i32p, _i32, _i64, _i64, _i32,
+                                            _vp, _vp, _vp,
+                                            ctypes.POINTER(_f64), _vp, _vp,
+                                            _i64, _i32, _i32, _i32, _i32,
+                                            _vp, _vp, _vp, _vp, _vp, _vp,
+                                            _vp, _vp]),
     "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
                                        _vp, _vp]),
     "pm_halo_pack": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
@@ -195,6 +201,22 @@ def column_mass(layout, k, n_cells, layers, cmap, offs, xmap, xoffs, coords,
         m.ctypes.data_as(ctypes.POINTER(_f64)), ptr(x), ptr(y), n_dofs,
         1 if accumulate else 0, variant, ptr(cells),
         0 if cells is None else cells.shape[0], stream_ptr(stream))
+    check(rc)
+
+
+def column_mass_patch(layout, k, base, layers, cmap, xmap, coords, mref, x,
+                      y, plan, dplan, chunk, stream=None):
+    """pm_column_mass_patch: y = M x with the patch-owner schedule."""
+    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    d = layout.delta6()
+    rc = host_lib().pm_column_mass_patch(
+        d.ctypes.data_as(_i32p), k, base.num_vertices, base.num_edges,
+        layers, ptr(cmap), ptr(xmap), ptr(coords),
+        m.ctypes.data_as(ctypes.POINTER(_f64)), ptr(x), ptr(y),
+        plan.n_patches, plan.n_colors, chunk, plan.max_local,
+        plan.max_owned, ptr(dplan["cell_ptr"]), ptr(dplan["cells"]),
+        ptr(dplan["color_ptr"]), ptr(dplan["ent_ptr"]), ptr(dplan["owned"]),
+        ptr(dplan["ents"]), ptr(dplan["lents"]), stream_ptr(stream))
     check(rc)
 
 

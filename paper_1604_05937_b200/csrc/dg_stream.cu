@@ -19,7 +19,7 @@ constexpr int kStreamT = 256;  // cell-layers per unit (= threads per CTA)
 constexpr int kStreamS = 4;    // pipeline stages
 
 template <int D>
-__global__ void __launch_bounds__(kStreamT)
+__global__ void __launch_bounds__(kStreamT, 3)
 k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
             const int32_t *__restrict__ xmap,
             const int32_t *__restrict__ xoff,
@@ -32,9 +32,11 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem + S * BYTES);
   const int t = threadIdx.x;
 
-  int xo[18];
-#pragma unroll
-  for (int j = 0; j < 18; ++j) xo[j] = __ldg(xoff + j);
+  // the coordinate space (COORDS_LAYOUT) moves every slot up by 3 per
+  // layer (Alg. 2); the device offsets array holds the same constants
+  (void)xoff;
+  constexpr int xo[18] = {3, 3, 3, 3, 3, 3, 3, 3, 3,
+                          3, 3, 3, 3, 3, 3, 3, 3, 3};
 
   if (t == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
@@ -54,23 +56,56 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
     }
   }
 
-  for (int64_t i = 0; i < n_mine; ++i) {
-    const int s = (int)(i % S);
-    const int64_t u = first + i * stride;
-    double *b = buf + s * T * D;
-
-    // geometry first: its gathers overlap the bulk copy still in flight
+  // Coordinates are software-pipelined one unit ahead: the bottom-level
+  // (x,y,z) of the three vertices for unit i+1 are in flight while unit i
+  // computes; the top level comes from the next lane (same column) or, on
+  // a column's last layer / the warp's last lane, from its own load.
+  const int lane = t & 31;
+  double cb[9], nb[9];
+  int64_t cur_c = 0;
+  int cur_l = 0;
+  auto gather = [&](int64_t u, double *dst, int64_t &cc, int &ll) {
     const uint32_t g = (uint32_t)(u * T + t);
     const uint32_t c = g / (uint32_t)layers;
     const int l = (int)(g - c * (uint32_t)layers);
     const int32_t *xm = xmap + (size_t)c * 18;
-    double X[6], Y[6], Z[6];
 #pragma unroll
-    for (int v = 0; v < 6; ++v) {
-      const int q = 3 * v;
-      X[v] = __ldg(coords + __ldg(xm + q) + l * xo[q]);
-      Y[v] = __ldg(coords + __ldg(xm + q + 1) + l * xo[q + 1]);
-      Z[v] = __ldg(coords + __ldg(xm + q + 2) + l * xo[q + 2]);
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        dst[3 * a + q] =
+            __ldg(coords + __ldg(xm + 6 * a + q) + l * xo[6 * a + q]);
+    cc = c;
+    ll = l;
+  };
+  if (n_mine > 0) gather(first, cb, cur_c, cur_l);
+
+  for (int64_t i = 0; i < n_mine; ++i) {
+    const int s = (int)(i % S);
+    const int64_t u = first + i * stride;
+    double *b = buf + s * T * D;
+    int64_t nxt_c = 0;
+    int nxt_l = 0;
+    if (i + 1 < n_mine) gather(u + stride, nb, nxt_c, nxt_l);
+
+    // top level of this cell-layer: the next lane's bottom level when it
+    // is the same column one layer up, otherwise an own load
+    const int64_t c_up = __shfl_down_sync(0xffffffffu, cur_c, 1);
+    const bool own_top = lane == 31 || cur_l == layers - 1 || c_up != cur_c;
+    double X[6], Y[6], Z[6];
+    const int32_t *xm = xmap + (size_t)cur_c * 18;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double top[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const double up = __shfl_down_sync(0xffffffffu, cb[3 * a + q], 1);
+        top[q] = own_top ? __ldg(coords + __ldg(xm + 6 * a + 3 + q) +
+                                 cur_l * xo[6 * a + 3 + q])
+                         : up;
+      }
+      X[2 * a] = cb[3 * a], Y[2 * a] = cb[3 * a + 1], Z[2 * a] = cb[3 * a + 2];
+      X[2 * a + 1] = top[0], Y[2 * a + 1] = top[1], Z[2 * a + 1] = top[2];
     }
     const double det = prism_abs_detj(X, Y, Z);
 
@@ -100,6 +135,10 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
                  &bar[sn]);
       }
     }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) cb[q] = nb[q];
+    cur_c = nxt_c;
+    cur_l = nxt_l;
   }
   if (t == 0) bulk_wait<0>();
 }

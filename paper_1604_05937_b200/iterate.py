@@ -15,8 +15,11 @@ CPU execution path).
 
 Schedules (``schedule=``):
 
-``"auto"``      DG (2,1) fields in overwrite mode: ``"stream"``;
-                otherwise ``"column"``.
+``"auto"``      DG (2,1) fields in overwrite mode: ``"stream"``; CG
+                fields on vertex/edge columns: ``"patch"``; otherwise
+                ``"column"``.
+``"patch"``     owner-computes over compact patches, shared-memory
+                accumulation, no atomics, deterministic (schedule.py).
 ``"stream"``    DG (2,1) fields through TMA bulk copies (dg_stream.cu).
 ``"column"``    warp segment per column, lanes = layers; vertical sharing
                 in registers, column-shared DoFs via fp64 REDG.
@@ -34,7 +37,8 @@ import numpy as np
 
 from . import _lib
 
-SCHEDULES = ("auto", "atomic", "colored", "sequential", "column", "stream")
+SCHEDULES = ("auto", "atomic", "colored", "sequential", "column", "stream",
+             "patch")
 
 
 @dataclass(frozen=True)

@@ -112,6 +112,7 @@ class MassOperator:
         self.k = fs.num_slots
         self.schedule = schedule
         self._coloring = None
+        self._patch = None
         self._dev = _lib.cuda_device()
         self.cmap = fs.device_cell_map()
         self.offs = fs.device_offsets()
@@ -123,6 +124,9 @@ class MassOperator:
         """Column-loop kernel launches one ``apply`` issues."""
         if self.schedule in ("colored", "sequential") and self.share == 2:
             return self._color_lists()[1].shape[0] - 1
+        if self.schedule in ("auto", "patch") and self.share == 2 and \
+                self.patch_ok:
+            return 1
         return 1
 
     @property
@@ -132,6 +136,22 @@ class MassOperator:
     @property
     def layers(self):
         return self.fs.mesh.layers
+
+    @property
+    def patch_ok(self) -> bool:
+        """DoFs only on vertex / edge columns (the patch schedule's case)."""
+        d = self.fs.layout.delta6()
+        return d[4] == 0 and d[5] == 0 and tuple(d) in _PATCH_LAYOUTS
+
+    def _patch_plan(self):
+        if self._patch is None:
+            from .schedule import plan_for
+            col = _color(self.fs.mesh)
+            plan, W, _ch, _need = plan_for(self.fs.mesh.base, self.fs.layout,
+                                           self.layers, col.color_of,
+                                           col.num_colors)
+            self._patch = (plan, plan.device(self._dev), W)
+        return self._patch
 
     def _color_lists(self):
         if self._coloring is None:
@@ -155,6 +175,29 @@ class MassOperator:
         if y is None:
             y = torch.empty(n, dtype=torch.float64, device=x.device)
             accumulate = False
+        if sched == "auto" and self.share == 2 and self.patch_ok:
+            sched = "patch"
+        if sched == "patch":
+            if not self.patch_ok:
+                raise ValueError(
+                    f"the patch schedule needs a vertex/edge-only layout, "
+                    f"got {self.fs.layout.name}")
+            plan, dplan, W = self._patch_plan()
+            if accumulate:
+                tmp = torch.empty_like(y)
+                _lib.column_mass_patch(self.fs.layout, self.k,
+                                       self.fs.mesh.base, self.layers,
+                                       self.cmap, self.xmap, coords,
+                                       self.mref, x, tmp, plan, dplan, W,
+                                       stream=stream)
+                y += tmp
+            else:
+                _lib.column_mass_patch(self.fs.layout, self.k,
+                                       self.fs.mesh.base, self.layers,
+                                       self.cmap, self.xmap, coords,
+                                       self.mref, x, y, plan, dplan, W,
+                                       stream=stream)
+            return y
         if sched not in _VARIANTS:
             raise ValueError(f"unknown schedule {sched!r}")
         if sched in ("colored", "sequential") and self.share == 2:
@@ -179,6 +222,10 @@ class MassOperator:
                          variant=_VARIANTS[sched], stream=stream)
         return y
 
+
+#: layouts compiled into the patch kernel (csrc/patch.cu)
+_PATCH_LAYOUTS = {(1, 0, 0, 0, 0, 0), (0, 1, 0, 0, 0, 0), (0, 2, 0, 0, 0, 0),
+                  (1, 1, 1, 1, 0, 0), (3, 0, 0, 0, 0, 0)}
 
 _VARIANTS = {"auto": _lib.VARIANT_AUTO, "atomic": _lib.VARIANT_ATOMIC,
              "column": _lib.VARIANT_COLUMN, "stream": _lib.VARIANT_STREAM,

@@ -126,7 +126,13 @@ def test_arity_and_mesh_mismatch_rejected(gmesh):
         iterate_columns([fs, xfs2], k, [None, None, None])
 
 
-SCHEDULES = ("auto", "atomic", "colored")
+SCHEDULES = ("auto", "atomic", "colored", "column", "patch")
+
+
+def _schedule_applies(lname, schedule):
+    if schedule == "patch":
+        return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "P2xP2", "VP1")
+    return True
 
 
 @pytest.mark.parametrize("mname", ("one", "two", "sq5", "sq4rnd"))
@@ -135,6 +141,8 @@ SCHEDULES = ("auto", "atomic", "colored")
 @pytest.mark.parametrize("schedule", SCHEDULES)
 def test_mass_action_matches_oracle(gmesh, mname, layers, lname, schedule):
     from paper_1604_05937_b200.kernels import mass_action
+    if not _schedule_applies(lname, schedule):
+        pytest.skip("schedule not defined for this layout")
     from paper_1604_05937_b200.quadrature import prism_quadrature
     base = gmesh(mname)
     fs = _space(base, layers, lname)
@@ -170,13 +178,38 @@ def test_iterate_columns_accumulates(gmesh, lname):
 
 
 @pytest.mark.parametrize("lname", ("CG1xCG1", "P2xP2", "VP1", "CG1xDG1"))
-def test_colored_schedule_is_deterministic(gmesh, lname):
+@pytest.mark.parametrize("schedule", ("colored", "patch"))
+def test_deterministic_schedules(gmesh, lname, schedule):
     from paper_1604_05937_b200.kernels import mass_action
     fs = _space(gmesh("sq5"), 4, lname)
     f = torch.rand(fs.total_dofs, dtype=torch.float64, device="cuda")
-    a = mass_action(fs, f, schedule="colored")
-    b = mass_action(fs, f, schedule="colored")
+    a = mass_action(fs, f, schedule=schedule)
+    b = mass_action(fs, f, schedule=schedule)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("lname", ("CG1xCG1", "P2xP2", "VP1"))
+@pytest.mark.parametrize("W", (8, 16, 32))
+@pytest.mark.parametrize("layers", (1, 7, 33))
+def test_patch_chunk_widths(lname, W, layers):
+    """Every chunk width and ragged chunk tails against the oracle."""
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator
+    from paper_1604_05937_b200.schedule import plan_for
+    w = configs.Workload("pw", 12, layers, lname, quad_degrees(lname),
+                         jitter=0.2)
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    op = MassOperator(fs, quad, schedule="patch")
+    from paper_1604_05937_b200.kernels import _color
+    col = _color(m)
+    plan, W2, _, _ = plan_for(m.base, fs.layout, layers, col.color_of,
+                              col.num_colors, W=W, smem_budget=24 * 1024)
+    op._patch = (plan, plan.device(op._dev), W2)
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    y = op.apply(torch.from_numpy(x).cuda(), coords).cpu().numpy()
+    ref = _oracle_for(w, fs).assemble(x)
+    assert _rel(y, ref) <= 1e-10
 
 
 def test_residual_field_api_and_conservation(gmesh):
@@ -256,7 +289,9 @@ def test_config3_full_size_properties():
     xa = torch.from_numpy(x).cuda()
     ya = MassOperator(fs, quad, schedule="atomic").apply(xa, coords)
     yc = MassOperator(fs, quad, schedule="colored").apply(xa, coords)
+    yp = MassOperator(fs, quad, schedule="patch").apply(xa, coords)
     assert _rel(ya.cpu().numpy(), yc.cpu().numpy()) <= 1e-10
+    assert _rel(yp.cpu().numpy(), yc.cpu().numpy()) <= 1e-10
     one = torch.ones_like(xa)
     s = MassOperator(fs, quad).apply(one, coords).sum().item()
     assert abs(s - 1.0) < 1e-10
