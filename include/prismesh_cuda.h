@@ -85,6 +85,9 @@ int pm_extrude_coordinates(const double *base_coords, int64_t n_vertices,
  * coord_map: device int32 [n_cells*18];  coord_offsets: device int32 [18]
  * coords   : device fp64 extruded coordinate field
  * mref     : HOST fp64 [k*k] reference-prism mass matrix (slot order)
+ * mtri, mline: HOST fp64 Kronecker factors of mref (nh x nh triangle,
+ *            nv x nv interval mass matrices of the layout's element; the
+ *            column / patch kernels apply mref by sum factorisation)
  * x, y     : device fp64 fields of length n_dofs (DoF numbers < 2^31)
  * accumulate: 0 -> y = M x (y is overwritten), 1 -> y += M x
  * variant  : PM_VARIANT_*
@@ -97,7 +100,8 @@ int pm_column_mass(const int32_t *delta6, int32_t k, int64_t n_cells,
                    int32_t layers, const int32_t *cell_map,
                    const int32_t *offsets, const int32_t *coord_map,
                    const int32_t *coord_offsets, const double *coords,
-                   const double *mref, const double *x, double *y,
+                   const double *mref, const double *mtri,
+                   const double *mline, const double *x, double *y,
                    int64_t n_dofs, int32_t accumulate, int32_t variant,
                    const int32_t *cells, int64_t n_list, void *stream);
 
@@ -112,6 +116,7 @@ int pm_column_mass_patch(const int32_t *delta6, int32_t k, int64_t n_vertices,
                          int64_t n_edges, int32_t layers,
                          const int32_t *cell_map, const int32_t *coord_map,
                          const double *coords, const double *mref,
+                         const double *mtri, const double *mline,
                          const double *x, double *y, int64_t n_patches,
                          int32_t n_colors, int32_t chunk, int32_t max_local,
                          int32_t max_owned, const int32_t *cell_ptr,

@@ -39,12 +39,16 @@ SIGNATURES = {
                                               _vp]),
     "pm_column_mass": (ctypes.c_int, [_i32p, _i32, _i64, _i32, _vp, _vp,
                                       _vp, _vp, _vp, ctypes.POINTER(_f64),
+                                      ctypes.POINTER(_f64),
+                                      ctypes.POINTER(_f64),
                                       _vp, _vp, _i64, _i32, _i32, _vp, _i64,
                                       _vp]),
     "pm_greedy_color_cells": (ctypes.c_int, [_i32p, _i64, _i64p, _i32p,
                                              _i32p, _i32p]),
     "pm_column_mass_patch": (ctypes.c_int, [_i32p, _i32, _i64, _i64, _i32,
                                             _vp, _vp, _vp,
+                                            ctypes.POINTER(_f64),
+                                            ctypes.POINTER(_f64),
                                             ctypes.POINTER(_f64), _vp, _vp,
                                             _i64, _i32, _i32, _i32, _i32,
                                             _vp, _vp, _vp, _vp, _vp, _vp,
@@ -187,32 +191,44 @@ def column_probe(mode, fs, out, stream=None):
                                      i64, f64, stream_ptr(stream)))
 
 
+def _f64ptr(a):
+    if a is None:
+        return None
+    return a.ctypes.data_as(ctypes.POINTER(_f64))
+
+
 def column_mass(layout, k, n_cells, layers, cmap, offs, xmap, xoffs, coords,
                 mref, x, y, n_dofs, accumulate=False, variant=VARIANT_AUTO,
-                cells=None, stream=None):
-    """pm_column_mass: y (+)= M x over the column loop (device tensors)."""
+                cells=None, stream=None, kron=None):
+    """pm_column_mass: y (+)= M x over the column loop (device tensors).
+    ``kron`` = (Mtri, Mline) factors of ``mref`` (host arrays)."""
     m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
     if m.shape[0] != k * k:
         raise ValueError(f"mref must be {k}x{k}")
+    mt, ml = (None, None) if kron is None else (
+        np.ascontiguousarray(kron[0], dtype=np.float64).ravel(),
+        np.ascontiguousarray(kron[1], dtype=np.float64).ravel())
     d = layout.delta6()
     rc = host_lib().pm_column_mass(
         d.ctypes.data_as(_i32p), k, n_cells, layers, ptr(cmap), ptr(offs),
-        ptr(xmap), ptr(xoffs), ptr(coords),
-        m.ctypes.data_as(ctypes.POINTER(_f64)), ptr(x), ptr(y), n_dofs,
+        ptr(xmap), ptr(xoffs), ptr(coords), _f64ptr(m), _f64ptr(mt),
+        _f64ptr(ml), ptr(x), ptr(y), n_dofs,
         1 if accumulate else 0, variant, ptr(cells),
         0 if cells is None else cells.shape[0], stream_ptr(stream))
     check(rc)
 
 
 def column_mass_patch(layout, k, base, layers, cmap, xmap, coords, mref, x,
-                      y, plan, dplan, chunk, stream=None):
+                      y, plan, dplan, chunk, stream=None, kron=None):
     """pm_column_mass_patch: y = M x with the patch-owner schedule."""
     m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
+    ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
     d = layout.delta6()
     rc = host_lib().pm_column_mass_patch(
         d.ctypes.data_as(_i32p), k, base.num_vertices, base.num_edges,
-        layers, ptr(cmap), ptr(xmap), ptr(coords),
-        m.ctypes.data_as(ctypes.POINTER(_f64)), ptr(x), ptr(y),
+        layers, ptr(cmap), ptr(xmap), ptr(coords), _f64ptr(m), _f64ptr(mt),
+        _f64ptr(ml), ptr(x), ptr(y),
         plan.n_patches, plan.n_colors, chunk, plan.max_local,
         plan.max_owned, ptr(dplan["cell_ptr"]), ptr(dplan["cells"]),
         ptr(dplan["color_ptr"]), ptr(dplan["ent_ptr"]), ptr(dplan["owned"]),

@@ -123,6 +123,7 @@ extern "C" int pm_column_mass(const int32_t *delta6, int32_t k,
                               const int32_t *coord_map,
                               const int32_t *coord_offsets,
                               const double *coords, const double *mref,
+                              const double *mtri, const double *mline,
                               const double *x, double *y, int64_t n_dofs,
                               int32_t accumulate, int32_t variant,
                               const int32_t *cells, int64_t n_list,
@@ -154,6 +155,8 @@ extern "C" int pm_column_mass(const int32_t *delta6, int32_t k,
   a.xoff = coord_offsets;
   a.coords = coords;
   a.mref = mref;
+  a.mtri = mtri;
+  a.mline = mline;
   a.x = x;
   a.y = y;
   a.accumulate = accumulate ? 1 : 0;

@@ -12,6 +12,13 @@ template <int K> struct MassMat {
   double m[K * K]; // reference-prism mass matrix, row-major, slot order
 };
 
+// Reference-prism mass matrix as the tensor product of its triangle and
+// interval factors: Mref[(c,h,v),(c,h',v')] = Mtri[h][h'] * Mline[v][v'].
+struct KronMat {
+  double t[36]; // Mtri, row-major (<= 6 x 6)
+  double l[9];  // Mline, row-major (<= 3 x 3)
+};
+
 // |det J| of the affine map reference prism -> physical prism cell-layer.
 // Vertex index v = 2a + b (a: triangle vertex, b: 0 bottom / 1 top level).
 // Same operation order as the oracle (oracle/prismesh_oracle.c).
@@ -34,6 +41,7 @@ struct LoopArgs {
   const int32_t *cells; // optional cell list (colour / order), device
   const int32_t *cmap, *coff, *xmap, *xoff;
   const double *coords, *mref, *x;
+  const double *mtri, *mline; // Kronecker factors (host), may be NULL
   double *y;
   int accumulate;
   SlotTable st;
@@ -41,6 +49,38 @@ struct LoopArgs {
   bool hshared;  // some DoF shared between columns
   cudaStream_t s;
 };
+
+// y = det * (Mtri (x) Mline) x by sum factorisation over a layout's
+// compile-time slot table T (NH x NV functions per component).
+template <class LY>
+__device__ __forceinline__ void kron_apply(const KronMat &M, const double *xv,
+                                           double det, double *yv) {
+  constexpr typename LY::Tab T = LY::make();
+  constexpr int NH = LY::NH, NV = LY::NV, NC = LY::NC;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double z[NH][NV];
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NV; ++w)
+          s = fma(M.l[v * NV + w], xv[T.slot[c][h][w]], s);
+        z[h][v] = s;
+      }
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double s = 0.0;
+#pragma unroll
+        for (int g = 0; g < NH; ++g) s = fma(M.t[h * NH + g], z[g][v], s);
+        yv[T.slot[c][h][v]] = det * s;
+      }
+  }
+}
 
 // Kernel launchers (one translation unit each).
 int launch_generic(const LoopArgs &a, bool atomic, int64_t cl_begin);

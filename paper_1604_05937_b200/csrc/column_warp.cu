@@ -17,7 +17,7 @@
 namespace pm {
 
 template <int K> struct ColumnArgs {
-  MassMat<K> M;
+  KronMat M;
 };
 
 enum { kStorePlain = 0, kStoreAtomic = 1, kStoreRmw = 2 };
@@ -131,15 +131,7 @@ k_column(const ColumnArgs<K> A, int64_t n_cells, int layers,
 
       // ---- element kernel
       double yv[K];
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        double acc = 0.0;
-#pragma unroll
-        for (int i = 0; i < K; ++i)
-          if (T.comp[i] == T.comp[j]) // structural zeros skipped
-            acc = fma(A.M.m[j * K + i], xv[i], acc);
-        yv[j] = det * acc;
-      }
+      kron_apply<LY>(A.M, xv, det, yv);
 
       // ---- vertical combine: top(l-1) joins bottom(l)
 #pragma unroll
@@ -174,7 +166,12 @@ template <class LY>
 static int column_k(const LoopArgs &a, bool colored) {
   constexpr int K = LY::K;
   ColumnArgs<K> A;
-  for (int i = 0; i < K * K; ++i) A.M.m[i] = a.mref[i];
+  if (!a.mtri || !a.mline) {
+    set_error("the column kernel needs the Kronecker factors mtri/mline");
+    return PM_EINVAL;
+  }
+  for (int i = 0; i < LY::NH * LY::NH; ++i) A.M.t[i] = a.mtri[i];
+  for (int i = 0; i < LY::NV * LY::NV; ++i) A.M.l[i] = a.mline[i];
   // segment width: smallest lane waste for this layer count
   int W = 32;
   {

@@ -16,7 +16,7 @@
 namespace pm {
 
 constexpr int kStreamT = 256;  // cell-layers per unit (= threads per CTA)
-constexpr int kStreamS = 4;    // pipeline stages
+constexpr int kStreamS = 6;    // pipeline stages
 
 template <int D>
 __global__ void __launch_bounds__(kStreamT, 3)

@@ -31,7 +31,7 @@ struct PatchDev {
 
 template <class LY, int W, int K = LY::K>
 __global__ void __launch_bounds__(256)
-k_patch(const MassMat<K> M, const PatchDev P, int64_t n_patches, int layers,
+k_patch(const KronMat M, const PatchDev P, int64_t n_patches, int layers,
         const int32_t *__restrict__ cmap, const int32_t *__restrict__ xmap,
         const double *__restrict__ coords, const double *__restrict__ x,
         double *__restrict__ y) {
@@ -119,14 +119,7 @@ k_patch(const MassMat<K> M, const PatchDev P, int64_t n_patches, int layers,
           }
           const double det = act ? prism_abs_detj(X, Y, Z) : 0.0;
           double yv[K];
-#pragma unroll
-          for (int j = 0; j < K; ++j) {
-            double s = 0.0;
-#pragma unroll
-            for (int i = 0; i < K; ++i)
-              if (T.comp[i] == T.comp[j]) s = fma(M.m[j * K + i], xv[i], s);
-            yv[j] = det * s;
-          }
+          kron_apply<LY>(M, xv, det, yv);
           // vertical combine inside the chunk; the chunk's top level goes
           // to accumulator level `nl` (carried by phase B)
 #pragma unroll
@@ -190,8 +183,13 @@ static int patch_k(const LoopArgs &a, const PatchDev &P, int64_t n_patches,
                    int W) {
   constexpr int K = LY::K;
   constexpr int CH = LY::CH0 > LY::CH1 ? LY::CH0 : LY::CH1;
-  MassMat<K> M;
-  for (int i = 0; i < K * K; ++i) M.m[i] = a.mref[i];
+  if (!a.mtri || !a.mline) {
+    set_error("the patch kernel needs the Kronecker factors mtri/mline");
+    return PM_EINVAL;
+  }
+  KronMat M;
+  for (int i = 0; i < LY::NH * LY::NH; ++i) M.t[i] = a.mtri[i];
+  for (int i = 0; i < LY::NV * LY::NV; ++i) M.l[i] = a.mline[i];
   const size_t smem =
       sizeof(double) * ((size_t)P.max_local * CH * (W + 1) +
                         (size_t)P.max_owned * CH);
@@ -254,8 +252,8 @@ int launch_patch(const LoopArgs &a, const int32_t *delta6,
 extern "C" int pm_column_mass_patch(
     const int32_t *delta6, int32_t k, int64_t n_vertices, int64_t n_edges,
     int32_t layers, const int32_t *cell_map, const int32_t *coord_map,
-    const double *coords, const double *mref, const double *x, double *y,
-    int64_t n_patches, int32_t n_colors, int32_t chunk, int32_t max_local,
+    const double *coords, const double *mref, const double *mtri,
+    const double *mline, const double *x, double *y, int64_t n_patches, int32_t n_colors, int32_t chunk, int32_t max_local,
     int32_t max_owned, const int32_t *cell_ptr, const int32_t *cells,
     const int32_t *color_ptr, const int32_t *ent_ptr, const int32_t *owned,
     const int32_t *ents, const uint16_t *lents, void *stream) {
@@ -280,6 +278,8 @@ extern "C" int pm_column_mass_patch(
   a.xmap = coord_map;
   a.coords = coords;
   a.mref = mref;
+  a.mtri = mtri;
+  a.mline = mline;
   a.x = x;
   a.y = y;
   a.s = (cudaStream_t)stream;

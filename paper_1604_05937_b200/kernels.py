@@ -25,8 +25,8 @@ import numpy as np
 from . import _lib
 from .fspace import COORDS_LAYOUT, FunctionSpace, number_dofs
 from .quadrature import (PrismElement, QuadratureRule, element_for_layout,
-                         prism_quadrature, reference_mass_matrix,
-                         sharing_class)
+                         kronecker_factors, prism_quadrature,
+                         reference_mass_matrix, sharing_class)
 
 __all__ = ["Field", "KernelProfile", "MassKernel", "MassOperator",
            "CountingKernel", "ListProbeKernel", "assemble_residual",
@@ -108,6 +108,12 @@ class MassOperator:
         self.element = element or element_for_layout(fs.layout)
         self.quadrature = quadrature or default_quadrature(self.element)
         self.mref = reference_mass_matrix(self.element, self.quadrature)
+        self.kron = kronecker_factors(self.element, self.quadrature)
+        # the compiled column / patch kernels assume the layout's default
+        # element (their slot -> basis map is a compile-time table)
+        default = element_for_layout(fs.layout) if element is not None \
+            else self.element
+        self.kron_ok = default == self.element
         self.share = sharing_class(fs.layout)
         self.k = fs.num_slots
         self.schedule = schedule
@@ -175,6 +181,8 @@ class MassOperator:
         if y is None:
             y = torch.empty(n, dtype=torch.float64, device=x.device)
             accumulate = False
+        if not self.kron_ok and sched != "stream":
+            sched = "atomic"   # dense Mref in the generic kernel
         if sched == "auto" and self.share == 2 and self.patch_ok:
             sched = "patch"
         if sched == "patch":
@@ -189,14 +197,14 @@ class MassOperator:
                                        self.fs.mesh.base, self.layers,
                                        self.cmap, self.xmap, coords,
                                        self.mref, x, tmp, plan, dplan, W,
-                                       stream=stream)
+                                       stream=stream, kron=self.kron)
                 y += tmp
             else:
                 _lib.column_mass_patch(self.fs.layout, self.k,
                                        self.fs.mesh.base, self.layers,
                                        self.cmap, self.xmap, coords,
                                        self.mref, x, y, plan, dplan, W,
-                                       stream=stream)
+                                       stream=stream, kron=self.kron)
             return y
         if sched not in _VARIANTS:
             raise ValueError(f"unknown schedule {sched!r}")
@@ -212,14 +220,15 @@ class MassOperator:
                                  accumulate=True,
                                  variant=_lib.VARIANT_COLORED,
                                  cells=order[ptr[c]:ptr[c + 1]],
-                                 stream=stream)
+                                 stream=stream, kron=self.kron)
             return y
         if sched == "stream" and self.share != 0:
             raise ValueError("the stream schedule needs a DG (2,1) layout")
         _lib.column_mass(self.fs.layout, self.k, self.n_cells, self.layers,
                          self.cmap, self.offs, self.xmap, self.xoffs, coords,
                          self.mref, x, y, n, accumulate=accumulate,
-                         variant=_VARIANTS[sched], stream=stream)
+                         variant=_VARIANTS[sched], stream=stream,
+                         kron=self.kron)
         return y
 
 

@@ -241,6 +241,18 @@ def reference_mass_matrix(element: PrismElement, rule: QuadratureRule):
     return np.ascontiguousarray(M)
 
 
+def kronecker_factors(element: PrismElement, rule: QuadratureRule):
+    """(Mtri, Mline) with Mref[j,j'] = delta(comp) Mtri[h,h'] Mline[v,v']:
+    the triangle / interval mass matrices under the rule's two factors
+    (exact product structure of the tensor-product rule)."""
+    tp, tw = triangle_rule(rule.tri_degree)
+    lp, lw = line_rule(rule.line_degree)
+    T = tri_basis(element.tri, tp[:, 0], tp[:, 1])
+    L = line_basis(element.line, lp)
+    return (np.ascontiguousarray((T * tw) @ T.T),
+            np.ascontiguousarray((L * lw) @ L.T))
+
+
 def sharing_class(layout) -> int:
     """0: no sharing (DG on (2,1)); 1: vertical only; 2: horizontal."""
     dims = {d for (d, _v) in layout.counts}

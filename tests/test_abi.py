@@ -45,16 +45,16 @@ def test_num_slots_and_errors():
         _lib.check(_lib.PM_EINVAL)
     # slot count that does not match the layout
     rc = lib.pm_column_mass(d.ctypes.data_as(i32p), 7, 10, 3, None, None,
-                            None, None, None, None, None, None, 0, 0, 0,
-                            None, 0, None)
+                            None, None, None, None, None, None, None, None,
+                            0, 0, 0, None, 0, None)
     assert rc == _lib.PM_EINVAL and "slot count" in _lib.last_error()
     # coloured variant without a cell list
     mref = np.eye(6)
     rc = lib.pm_column_mass(d.ctypes.data_as(i32p), 6, 10, 3, None, None,
                             None, None, None,
                             mref.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
-                            None, None, 0, 1, _lib.VARIANT_COLORED, None, 0,
-                            None)
+                            None, None, None, None, 0, 1,
+                            _lib.VARIANT_COLORED, None, 0, None)
     assert rc == _lib.PM_EINVAL
 
 

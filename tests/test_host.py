@@ -203,3 +203,15 @@ def test_perfbench_formulas():
         perfbench.balance_factor(0, 0, 0)
     with pytest.raises(ValueError):
         perfbench.vector_factor(2, 1)
+
+
+@pytest.mark.parametrize("lname", sorted(set(LAYOUT_COUNTS) - {"coords"}))
+def test_kronecker_factors_reproduce_mref(lname):
+    from paper_1604_05937_b200.quadrature import kronecker_factors
+    el = element_for_layout(DofLayout(lname, LAYOUT_COUNTS[lname]))
+    q = prism_quadrature(*quad_degrees(lname))
+    M = reference_mass_matrix(el, q)
+    Mt, Ml = kronecker_factors(el, q)
+    h, v, c = (np.array(a) for a in (el.slot_h, el.slot_v, el.slot_comp))
+    K = Mt[h][:, h] * Ml[v][:, v] * (c[:, None] == c[None, :])
+    np.testing.assert_allclose(K, M, rtol=0, atol=1e-16)
