@@ -189,7 +189,7 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_1604_05937_b200 import configs
-    w = configs.WORKLOADS[args.config]
+    w = configs.workload(args.config)
     fs, quad, x, _ = configs.build(w)
     arm = CpuArm(w, fs, x)
     arm.calibrate(max(1.0, 120.0 / max(1, args.steps + args.warmup)))
@@ -227,7 +227,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    w = configs.WORKLOADS[args.config]
+    w = configs.workload(args.config)
     fs, quad, x_np, _ = configs.build(w)
     m = fs.mesh
     coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
@@ -316,7 +316,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {
-                "workload": f"{w.name}: {w.note}, fp64, seed {w.seed}",
+                "workload": f"{w.name}: {w.note or w.layout}, fp64, seed {w.seed}",
                 "base_cells": m.base.num_cells, "layers": m.layers,
                 "layout": w.layout, "ordering": w.ordering,
                 "quadrature": list(w.quad),

@@ -101,3 +101,14 @@ def build(w: Workload):
     else:
         x = rng.uniform(-1.0, 1.0, fs.total_dofs)
     return fs, prism_quadrature(*w.quad), x, rng
+
+
+def workload(name: str) -> Workload:
+    """``C1``..``C5b`` or a config-4 sweep point ``C4-<layout>-<ordering>-L<n>``
+    (e.g. ``C4-CG1xCG1-rcm-L50``)."""
+    if name in WORKLOADS:
+        return WORKLOADS[name]
+    parts = name.split("-")
+    if len(parts) == 4 and parts[0] == "C4" and parts[3].startswith("L"):
+        return sweep_workload(parts[1], int(parts[3][1:]), parts[2])
+    raise ValueError(f"unknown workload {name!r}")

@@ -13,19 +13,21 @@
 #include "column_loop.cuh"
 #include "pm_ptx.cuh"
 
+#include <stdlib.h>
+
 namespace pm {
 
 constexpr int kStreamT = 256;  // cell-layers per unit (= threads per CTA)
-constexpr int kStreamS = 6;    // pipeline stages
 
-template <int D>
-__global__ void __launch_bounds__(kStreamT, 3)
+// S pipeline stages, MINB resident CTAs per SM (register budget)
+template <int D, int S, int MINB>
+__global__ void __launch_bounds__(kStreamT, MINB)
 k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
             const int32_t *__restrict__ xmap,
             const int32_t *__restrict__ xoff,
             const double *__restrict__ coords,
             const double *__restrict__ x, double *__restrict__ y) {
-  constexpr int T = kStreamT, S = kStreamS;
+  constexpr int T = kStreamT;
   constexpr uint32_t BYTES = T * D * sizeof(double);
   extern __shared__ __align__(128) unsigned char smem[];
   double *buf = reinterpret_cast<double *>(smem);
@@ -56,53 +58,69 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
     }
   }
 
-  // Coordinates are software-pipelined one unit ahead: the bottom-level
-  // (x,y,z) of the three vertices for unit i+1 are in flight while unit i
-  // computes; the top level comes from the next lane (same column) or, on
-  // a column's last layer / the warp's last lane, from its own load.
+  // Coordinates are software-pipelined: the coordinate-map entries of unit
+  // i+2 and the bottom-level (x,y,z) of the three vertices of unit i+1 are
+  // in flight while unit i computes, so neither the map -> coordinate
+  // dependency nor the gather latency is exposed.  The top level comes
+  // from the next lane (same column, one layer up) or, on a column's last
+  // layer / the warp's last lane, from an own (L1-resident) load.  In the
+  // coordinate space slot 6a+3b+q sits 3b+q after slot 6a (COORDS_LAYOUT).
   const int lane = t & 31;
-  double cb[9], nb[9];
-  int64_t cur_c = 0;
-  int cur_l = 0;
-  auto gather = [&](int64_t u, double *dst, int64_t &cc, int &ll) {
+  struct Where {
+    uint32_t c;
+    int l;
+  };
+  auto where = [&](int64_t u) {
     const uint32_t g = (uint32_t)(u * T + t);
     const uint32_t c = g / (uint32_t)layers;
-    const int l = (int)(g - c * (uint32_t)layers);
-    const int32_t *xm = xmap + (size_t)c * 18;
+    return Where{c, (int)(g - c * (uint32_t)layers)};
+  };
+  auto load_map = [&](const Where &w, int32_t *lx) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) lx[a] = __ldg(xmap + (size_t)w.c * 18 + 6 * a);
+  };
+  auto load_xyz = [&](const Where &w, const int32_t *lx, double *dst) {
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int q = 0; q < 3; ++q)
-        dst[3 * a + q] =
-            __ldg(coords + __ldg(xm + 6 * a + q) + l * xo[6 * a + q]);
-    cc = c;
-    ll = l;
+        dst[3 * a + q] = __ldg(coords + lx[a] + q + 3 * w.l);
   };
-  if (n_mine > 0) gather(first, cb, cur_c, cur_l);
+  Where w0{0, 0}, w1{0, 0}, w2{0, 0};
+  int32_t lx0[3] = {0, 0, 0}, lx1[3] = {0, 0, 0}, lx2[3] = {0, 0, 0};
+  double cb[9], nb[9];
+  if (n_mine > 0) {
+    w0 = where(first);
+    load_map(w0, lx0);
+    load_xyz(w0, lx0, cb);
+  }
+  if (n_mine > 1) {
+    w1 = where(first + stride);
+    load_map(w1, lx1);
+  }
+  (void)xo;
 
   for (int64_t i = 0; i < n_mine; ++i) {
     const int s = (int)(i % S);
     const int64_t u = first + i * stride;
     double *b = buf + s * T * D;
-    int64_t nxt_c = 0;
-    int nxt_l = 0;
-    if (i + 1 < n_mine) gather(u + stride, nb, nxt_c, nxt_l);
+    if (i + 1 < n_mine) load_xyz(w1, lx1, nb);
+    if (i + 2 < n_mine) {
+      w2 = where(u + 2 * stride);
+      load_map(w2, lx2);
+    }
 
-    // top level of this cell-layer: the next lane's bottom level when it
-    // is the same column one layer up, otherwise an own load
-    const int64_t c_up = __shfl_down_sync(0xffffffffu, cur_c, 1);
-    const bool own_top = lane == 31 || cur_l == layers - 1 || c_up != cur_c;
+    // top level of this cell-layer
+    const uint32_t c_up = __shfl_down_sync(0xffffffffu, w0.c, 1);
+    const bool own_top = lane == 31 || w0.l == layers - 1 || c_up != w0.c;
     double X[6], Y[6], Z[6];
-    const int32_t *xm = xmap + (size_t)cur_c * 18;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       double top[3];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const double up = __shfl_down_sync(0xffffffffu, cb[3 * a + q], 1);
-        top[q] = own_top ? __ldg(coords + __ldg(xm + 6 * a + 3 + q) +
-                                 cur_l * xo[6 * a + 3 + q])
-                         : up;
+        top[q] = own_top ? __ldg(coords + lx0[a] + 3 + q + 3 * w0.l) : up;
       }
       X[2 * a] = cb[3 * a], Y[2 * a] = cb[3 * a + 1], Z[2 * a] = cb[3 * a + 2];
       X[2 * a + 1] = top[0], Y[2 * a + 1] = top[1], Z[2 * a + 1] = top[2];
@@ -110,15 +128,33 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
     const double det = prism_abs_detj(X, Y, Z);
 
     mbar_wait(&bar[s], (uint32_t)((i / S) & 1));
-    double xv[D];
+    double xv[D], yv[D];
+    if constexpr (D % 2 == 0) { // 16-byte shared accesses: conflict-free
+      const double2 *b2 = reinterpret_cast<const double2 *>(b + t * D);
 #pragma unroll
-    for (int j = 0; j < D; ++j) xv[j] = b[t * D + j];
+      for (int j = 0; j < D / 2; ++j) {
+        const double2 v = b2[j];
+        xv[2 * j] = v.x;
+        xv[2 * j + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < D; ++j) xv[j] = b[t * D + j];
+    }
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       double acc = 0.0;
 #pragma unroll
       for (int q = 0; q < D; ++q) acc = fma(M.m[j * D + q], xv[q], acc);
-      b[t * D + j] = det * acc;
+      yv[j] = det * acc;
+    }
+    if constexpr (D % 2 == 0) {
+      double2 *b2 = reinterpret_cast<double2 *>(b + t * D);
+#pragma unroll
+      for (int j = 0; j < D / 2; ++j) b2[j] = make_double2(yv[2 * j], yv[2 * j + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < D; ++j) b[t * D + j] = yv[j];
     }
     fence_proxy_async_smem();
     __syncthreads();
@@ -137,10 +173,45 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
     }
 #pragma unroll
     for (int q = 0; q < 9; ++q) cb[q] = nb[q];
-    cur_c = nxt_c;
-    cur_l = nxt_l;
+    w0 = w1;
+    w1 = w2;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lx0[a] = lx1[a];
+      lx1[a] = lx2[a];
+    }
   }
   if (t == 0) bulk_wait<0>();
+}
+
+template <int D, int S, int MINB>
+static int dg_stream_launch(const LoopArgs &a, const MassMat<D> &M,
+                            int64_t n_units) {
+  const size_t smem = S * kStreamT * D * sizeof(double) + S * sizeof(uint64_t);
+  auto kern = k_dg_stream<D, S, MINB>;
+  PM_CUDA_TRY(cudaFuncSetAttribute(
+      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  PM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
+                                                            kStreamT, smem));
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  if (grid > n_units) grid = n_units;
+  kern<<<(unsigned)grid, kStreamT, smem, a.s>>>(M, n_units, a.layers, a.xmap,
+                                                a.xoff, a.coords, a.x, a.y);
+  PM_LAUNCH_CHECK("k_dg_stream");
+  return PM_OK;
+}
+
+// Stream pipeline shape (stages x CTAs/SM); PM_STREAM_CFG=1 selects the
+// deeper two-CTA ring (tuning knob, measured in profiles/).
+static int stream_cfg() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char *e = getenv("PM_STREAM_CFG");
+    cfg = e ? atoi(e) : 0;
+  }
+  return cfg;
 }
 
 template <int D> static int dg_stream_k(const LoopArgs &a, bool *handled) {
@@ -154,24 +225,9 @@ template <int D> static int dg_stream_k(const LoopArgs &a, bool *handled) {
   MassMat<D> M;
   for (int i = 0; i < D * D; ++i) M.m[i] = a.mref[i];
   if (n_units > 0) {
-    const size_t smem = kStreamS * kStreamT * D * sizeof(double) +
-                        kStreamS * sizeof(uint64_t);
-    static bool attr_set[8] = {false};
-    if (!attr_set[D]) {
-      PM_CUDA_TRY(cudaFuncSetAttribute(
-          k_dg_stream<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-          (int)smem));
-      attr_set[D] = true;
-    }
-    int per_sm = 0;
-    PM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k_dg_stream<D>, kStreamT, smem));
-    if (per_sm < 1) per_sm = 1;
-    int64_t grid = (int64_t)sm_count() * per_sm;
-    if (grid > n_units) grid = n_units;
-    k_dg_stream<D><<<(unsigned)grid, kStreamT, smem, a.s>>>(
-        M, n_units, a.layers, a.xmap, a.xoff, a.coords, a.x, a.y);
-    PM_LAUNCH_CHECK("k_dg_stream");
+    const int rc = stream_cfg() == 1 ? dg_stream_launch<D, 8, 2>(a, M, n_units)
+                                     : dg_stream_launch<D, 6, 3>(a, M, n_units);
+    if (rc) return rc;
   }
   *handled = true;
   // ragged tail (< one unit): flattened generic kernel, plain stores
