@@ -114,8 +114,12 @@ def stream_ptr(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def ptr(t):
-    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+def ptr(t, base=0):
+    """Device address of tensor ``t``; ``base`` (elements) shifts it so that
+    global indices land inside a window tensor that starts at ``base``."""
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr() - base * t.element_size())
 
 
 # ---------------------------------------------------------------------------
@@ -199,7 +203,8 @@ def _f64ptr(a):
 
 def column_mass(layout, k, n_cells, layers, cmap, offs, xmap, xoffs, coords,
                 mref, x, y, n_dofs, accumulate=False, variant=VARIANT_AUTO,
-                cells=None, stream=None, kron=None):
+                cells=None, stream=None, kron=None, x_base=0, y_base=0,
+                coords_base=0):
     """pm_column_mass: y (+)= M x over the column loop (device tensors).
     ``kron`` = (Mtri, Mline) factors of ``mref`` (host arrays)."""
     m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
@@ -211,8 +216,8 @@ def column_mass(layout, k, n_cells, layers, cmap, offs, xmap, xoffs, coords,
     d = layout.delta6()
     rc = host_lib().pm_column_mass(
         d.ctypes.data_as(_i32p), k, n_cells, layers, ptr(cmap), ptr(offs),
-        ptr(xmap), ptr(xoffs), ptr(coords), _f64ptr(m), _f64ptr(mt),
-        _f64ptr(ml), ptr(x), ptr(y), n_dofs,
+        ptr(xmap), ptr(xoffs), ptr(coords, coords_base), _f64ptr(m),
+        _f64ptr(mt), _f64ptr(ml), ptr(x, x_base), ptr(y, y_base), n_dofs,
         1 if accumulate else 0, variant, ptr(cells),
         0 if cells is None else cells.shape[0], stream_ptr(stream))
     check(rc)
@@ -250,14 +255,15 @@ def greedy_color_cells(cell_vertices, vc_offsets, vc_cells):
     return color, nc.value
 
 
-def halo_pack(y, cols, col, buf, stream=None):
-    check(host_lib().pm_halo_pack(ptr(y), ptr(cols), cols.shape[0], col,
+def halo_pack(y, cols, col, buf, base=0, stream=None):
+    check(host_lib().pm_halo_pack(ptr(y, base), ptr(cols), cols.shape[0], col,
                                   ptr(buf), stream_ptr(stream)))
 
 
-def halo_unpack_add(y, cols, col, buf, stream=None):
-    check(host_lib().pm_halo_unpack_add(ptr(y), ptr(cols), cols.shape[0],
-                                        col, ptr(buf), stream_ptr(stream)))
+def halo_unpack_add(y, cols, col, buf, base=0, stream=None):
+    check(host_lib().pm_halo_unpack_add(ptr(y, base), ptr(cols),
+                                        cols.shape[0], col, ptr(buf),
+                                        stream_ptr(stream)))
 
 
 def device_info():

@@ -1,0 +1,233 @@
+"""Base-mesh partitioning across GPUs (BASELINE config 5).
+
+The paper decomposes the *base* mesh between MPI ranks and notes that the
+column numbering is orthogonal to that decomposition (PAPER.md:463-465,
+770-775; the SPEC drops MPI).  Here one process drives one GPU:
+
+* rank p takes the p-th contiguous block of the (RCM-ordered) base cells
+  (``np.array_split``); columns are never split, the numbering stays the
+  global one, so every rank's maps are rows of the global maps;
+* a DoF-carrying base entity (vertex, edge) is owned by the lowest rank
+  whose block touches it;
+* each rank runs the column loop over its own cells into a window of the
+  global field that covers every entity its cells touch, then sends the
+  partial columns of the entities it touches but does not own to their
+  owners, which add them (one grouped send/recv per neighbour pair, NCCL
+  on GPUs, gloo in the CPU tests).
+
+After the exchange each rank holds the final values of its owned entity
+columns; nothing else is communicated (inputs are replicated at setup).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class Shard:
+    rank: int
+    world: int
+    cells: np.ndarray                 # int32 global cell ids (contiguous)
+    dim_entities: dict                # d -> touched entity ids (sorted)
+    owned: dict                       # d -> owned entity ids (sorted)
+    send: dict = field(default_factory=dict)   # peer -> {d: ids}
+    recv: dict = field(default_factory=dict)   # peer -> {d: ids}
+    window: tuple = (0, 0)            # [lo, hi) DoFs touched by the block
+    coord_window: tuple = (0, 0)      # [lo, hi) coordinate DoFs touched
+
+
+def _entities(base, d):
+    if d == 0:
+        return np.asarray(base.cell_vertices, dtype=np.int64)
+    if d == 1:
+        return np.asarray(base.cell_edges, dtype=np.int64)
+    raise ValueError("only vertex / edge entities are shared")
+
+
+def partition(fs, world: int):
+    """Per-rank Shard descriptions for space ``fs`` (host, deterministic)."""
+    base = fs.mesh.base
+    layout = fs.layout
+    dims = [d for d in (0, 1) if layout.dofs(d, 0) or layout.dofs(d, 1)]
+    if layout.dofs(2, 0) or layout.dofs(2, 1):
+        if dims:
+            raise ValueError("mixed cell + vertex/edge layouts not sharded")
+    n_cells = base.num_cells
+    blocks = np.array_split(np.arange(n_cells, dtype=np.int64), world)
+    block_of = np.empty(n_cells, dtype=np.int64)
+    for p, b in enumerate(blocks):
+        block_of[b] = p
+    owner = {}
+    for d in dims:
+        ents = _entities(base, d)
+        own = np.full(base.entity_count(d), world, dtype=np.int64)
+        np.minimum.at(own, ents.ravel(), np.repeat(block_of, ents.shape[1]))
+        owner[d] = own
+    layers = fs.mesh.layers
+    shards = []
+    for p, b in enumerate(blocks):
+        touched = {d: np.unique(_entities(base, d)[b].ravel()) for d in dims}
+        owned = {d: touched[d][owner[d][touched[d]] == p] for d in dims}
+        s = Shard(rank=p, world=world, cells=b.astype(np.int32),
+                  dim_entities=touched, owned=owned)
+        # window of global DoFs touched by the block
+        lo, hi = [], []
+        if dims:
+            for d in dims:
+                if touched[d].size:
+                    col = fs.column_sizes[d]
+                    start = fs.origin_starts[d]
+                    lo.append(start + col * int(touched[d][0]))
+                    hi.append(start + col * (int(touched[d][-1]) + 1))
+        elif b.size:
+            col = fs.column_sizes[2]
+            start = fs.origin_starts[2]
+            lo.append(start + col * int(b[0]))
+            hi.append(start + col * (int(b[-1]) + 1))
+        s.window = (min(lo), max(hi)) if lo else (0, 0)
+        if b.size:
+            vt = np.unique(np.asarray(base.cell_vertices)[b].ravel())
+            s.coord_window = (3 * (layers + 1) * int(vt[0]),
+                              3 * (layers + 1) * (int(vt[-1]) + 1))
+        shards.append(s)
+    # halo lists: entities touched by p, owned by q != p
+    for s in shards:
+        for d in dims:
+            t = s.dim_entities[d]
+            o = owner[d][t]
+            for q in np.unique(o[o != s.rank]):
+                ids = t[o == q]
+                s.send.setdefault(int(q), {})[d] = ids
+                shards[int(q)].recv.setdefault(s.rank, {})[d] = ids
+    return shards
+
+
+def ghost_origins(fs, ids_by_dim):
+    """DoF origins (int64) and column length per dim of an entity list."""
+    out = []
+    for d in sorted(ids_by_dim):
+        ids = np.asarray(ids_by_dim[d], dtype=np.int64)
+        col = fs.column_sizes[d]
+        out.append((d, fs.origin_starts[d] + col * ids, col))
+    return out
+
+
+class HaloExchange:
+    """Grouped send/recv of ghost partial columns, owner adds.
+
+    ``pack(y, origins, col) -> buf`` and ``unpack_add(y, origins, col,
+    buf)`` default to the CUDA kernels ``pm_halo_pack`` /
+    ``pm_halo_unpack_add``; ``y`` is the rank's window tensor and origins
+    are global DoF numbers (``base`` = window start).
+    """
+
+    def __init__(self, fs, shard: Shard, pack=None, unpack_add=None,
+                 device=None):
+        import torch
+        self.fs = fs
+        self.shard = shard
+        self.lo = shard.window[0]
+        dev = device or "cpu"
+        self.send = {q: [(d, torch.from_numpy(o).to(dev), c)
+                         for d, o, c in ghost_origins(fs, ids)]
+                     for q, ids in sorted(shard.send.items())}
+        self.recv = {q: [(d, torch.from_numpy(o).to(dev), c)
+                         for d, o, c in ghost_origins(fs, ids)]
+                     for q, ids in sorted(shard.recv.items())}
+        self._pack = pack or self._cuda_pack
+        self._unpack = unpack_add or self._cuda_unpack
+
+    def _cuda_pack(self, y, origins, col):
+        import torch
+        from . import _lib
+        buf = torch.empty(origins.shape[0] * col, dtype=y.dtype,
+                          device=y.device)
+        _lib.halo_pack(y, origins, col, buf, base=self.lo)
+        return buf
+
+    def _cuda_unpack(self, y, origins, col, buf):
+        from . import _lib
+        _lib.halo_unpack_add(y, origins, col, buf, base=self.lo)
+
+    def bytes_per_exchange(self):
+        n = 0
+        for lst in self.send.values():
+            n += sum(o.shape[0] * c for _d, o, c in lst) * 8
+        return n
+
+    def exchange(self, y, group=None):
+        """Send ghost partials to owners, add received partials (in place)."""
+        import torch
+        import torch.distributed as dist
+        ops, inbox = [], []
+        for q, lst in self.send.items():
+            for _d, o, c in lst:
+                ops.append(dist.P2POp(dist.isend, self._pack(y, o, c), q,
+                                      group=group))
+        for q, lst in self.recv.items():
+            for _d, o, c in lst:
+                buf = torch.empty(o.shape[0] * c, dtype=y.dtype,
+                                  device=y.device)
+                inbox.append((o, c, buf))
+                ops.append(dist.P2POp(dist.irecv, buf, q, group=group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for o, c, buf in inbox:
+            self._unpack(y, o, c, buf)
+        return y
+
+
+class ShardedMassOperator:
+    """The column loop over one rank's cell block + the halo exchange.
+
+    ``x_window`` / ``coords_window`` are the global fields restricted to
+    ``shard.window`` / ``shard.coord_window``; the result is the rank's
+    window of ``y`` with final values on its owned entity columns.
+    """
+
+    def __init__(self, fs, rank, world, quadrature=None, group=None):
+        import torch
+        from . import _lib
+        from .kernels import MassOperator
+        self.fs = fs
+        self.rank, self.world = rank, world
+        self.group = group
+        self.shard = partition(fs, world)[rank]
+        self.op = MassOperator(fs, quadrature, schedule="column")
+        dev = self.op._dev
+        self.d_cells = torch.from_numpy(self.shard.cells).to(dev)
+        self.halo = HaloExchange(fs, self.shard, device=dev)
+        self._lib = _lib
+
+    @property
+    def window(self):
+        return self.shard.window
+
+    def apply(self, x_window, coords_window, y_window=None, exchange=True):
+        import torch
+        lo, hi = self.shard.window
+        clo, _chi = self.shard.coord_window
+        if y_window is None:
+            y_window = torch.empty(hi - lo, dtype=torch.float64,
+                                   device=x_window.device)
+        y_window.zero_()
+        op = self.op
+        self._lib.column_mass(
+            op.fs.layout, op.k, op.n_cells, op.layers, op.cmap, op.offs,
+            op.xmap, op.xoffs, coords_window, op.mref, x_window, y_window,
+            hi - lo, accumulate=True, variant=self._lib.VARIANT_COLUMN,
+            cells=self.d_cells, kron=op.kron, x_base=lo, y_base=lo,
+            coords_base=clo)
+        if exchange and self.world > 1:
+            self.halo.exchange(y_window, group=self.group)
+        return y_window
+
+    def owned_slices(self):
+        """(window-relative start, length) of every owned entity column."""
+        out = []
+        for d, o, c in ghost_origins(self.fs, self.shard.owned):
+            out.append((d, o - self.shard.window[0], c))
+        return out

@@ -300,3 +300,56 @@ def test_config3_full_size_properties():
     lhs = torch.dot(z, op.apply(xa, coords)).item()
     rhs = torch.dot(xa, op.apply(z, coords)).item()
     assert abs(lhs - rhs) <= 1e-11 * abs(lhs)
+
+
+@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1", "P2xP2"))
+@pytest.mark.parametrize("world", (1, 2, 4))
+def test_sharded_windows_on_one_gpu(lname, world):
+    """Each rank's windowed column loop (no exchange), then the halo adds
+    emulated on the host: equals the full mass action (config-5 path)."""
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.shard import ShardedMassOperator, ghost_origins
+    w = configs.Workload("c5-small", 24, 6, lname, quad_degrees(lname))
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    ref = _oracle_for(w, fs).assemble(x)
+    xd = torch.from_numpy(x).cuda()
+    ops = [ShardedMassOperator(fs, r, world, quad) for r in range(world)]
+    wins = []
+    for op in ops:
+        lo, hi = op.window
+        clo, chi = op.shard.coord_window
+        wins.append(op.apply(xd[lo:hi].clone(), coords[clo:chi].clone(),
+                             exchange=False).cpu().numpy())
+    for op in ops:
+        s = op.shard
+        for q, ids in s.send.items():
+            for _d, o, c in ghost_origins(fs, ids):
+                for org in o:
+                    a = org - s.window[0]
+                    b = org - ops[q].window[0]
+                    wins[q][b:b + c] += wins[s.rank][a:a + c]
+    got = np.zeros_like(ref)
+    for op in ops:
+        for _d, o, c in ghost_origins(fs, op.shard.owned):
+            for org in o:
+                a = org - op.window[0]
+                got[org:org + c] = wins[op.rank][a:a + c]
+    assert _rel(got, ref) <= 1e-10
+
+
+def test_halo_kernels_match_host():
+    from paper_1604_05937_b200 import _lib
+    y = torch.rand(1000, dtype=torch.float64, device="cuda")
+    cols = torch.tensor([100, 300, 650], dtype=torch.int64, device="cuda")
+    buf = torch.empty(3 * 7, dtype=torch.float64, device="cuda")
+    _lib.halo_pack(y, cols, 7, buf, base=50)   # window starts at DoF 50
+    yh = y.cpu().numpy()
+    want = np.concatenate([yh[c - 50:c - 50 + 7] for c in (100, 300, 650)])
+    np.testing.assert_array_equal(buf.cpu().numpy(), want)
+    y2 = y.clone()
+    _lib.halo_unpack_add(y2, cols, 7, buf, base=50)
+    d = (y2 - y).cpu().numpy()
+    for c in (100, 300, 650):
+        np.testing.assert_array_equal(d[c - 50:c - 50 + 7], yh[c - 50:c - 50 + 7])
