@@ -20,6 +20,8 @@
  *                               (Algorithm 3)
  *   pm_column_mass_patch     <- same, race-free owner-computes schedule
  *                               replacing SPEC.md:343-364 colouring
+ *   pm_column_mass_strip     <- same, strip-patch schedule (vertex layouts)
+ *   pm_build_strips          <- host planner of that schedule
  *   pm_column_probe          <- SPEC.md:338-340 counting / gather kernels
  *                               (verification.py:47-75 materialized maps)
  *   pm_halo_pack / _unpack   <- PAPER.md:770-775 (halo exchange between
@@ -51,7 +53,8 @@ enum {
   PM_VARIANT_PATCH = 2,   /* patch-owner gather (pm_column_mass_patch)      */
   PM_VARIANT_COLUMN = 3,  /* warp segment per column, lanes = layers, REDG   */
   PM_VARIANT_COLORED = 4, /* COLUMN over one colour's cells, plain RMW      */
-  PM_VARIANT_STREAM = 5   /* DG (2,1) fields through TMA bulk copies        */
+  PM_VARIANT_STREAM = 5,  /* DG (2,1) fields through TMA bulk copies        */
+  PM_VARIANT_STRIP = 6    /* strip-patch owner gather (pm_column_mass_strip) */
 };
 
 const char *pm_last_error(void);
@@ -125,6 +128,26 @@ int pm_column_mass_patch(const int32_t *delta6, int32_t k, int64_t n_vertices,
                          const int32_t *ents, const uint16_t *lents,
                          void *stream);
 
+/* Strip-patch schedule (PM_VARIANT_STRIP) for layouts whose DoFs live on
+ * vertex columns (P1, 3-vector P1, CG1 x DGk): y = M x (overwrite),
+ * deterministic, no atomics.  Per patch the local vertex columns are staged
+ * in shared memory once per chunk and the cells are walked as strips (one
+ * new vertex per step); plan arrays from schedule.build_strip_plan /
+ * pm_build_strips. */
+int pm_column_mass_strip(const int32_t *delta6, int32_t k, int32_t layers,
+                         const double *coords, const double *mref,
+                         const double *mtri, const double *mline,
+                         const double *x, double *y, int64_t n_patches,
+                         int32_t chunk, int32_t threads, int32_t max_local,
+                         int32_t max_y, int32_t max_owned,
+                         const int32_t *ent_ptr, const int32_t *owned,
+                         const int32_t *ents, const int32_t *patch_strip_ptr,
+                         const int32_t *strip_step_ptr, const uint16_t *step_v,
+                         const uint8_t *step_slot, const uint8_t *step_flags,
+                         const int32_t *step_y, const int32_t *patch_y_count,
+                         const int32_t *own_base, const int32_t *own_y_ptr,
+                         const int32_t *own_y, void *stream);
+
 /* --- probes for the par-loop itself (exact integer checks) -------------
  * mode 0: out_i64[(c*layers+l)*k + j] = cell_map[c*k+j] + l*offsets[j]
  *         (the materialised per-(cell,layer) lists)
@@ -156,6 +179,20 @@ int pm_rcm_order(const int64_t *offsets, const int64_t *neighbours, int64_t n,
 int pm_greedy_color_cells(const int32_t *cell_vertices, int64_t n_cells,
                           const int64_t *vc_offsets, const int32_t *vc_cells,
                           int32_t *color_out, int32_t *n_colors);
+
+/* --- host setup: strips for the strip-patch schedule ----------------------
+ * Per patch (visited cells cell_ptr/cells, 16-bit local vertex ids lents,
+ * `owned` owned vertices first) walk the cells as edge-connected strips of
+ * at most max_len cells; see csrc/host_setup.cpp for the record format.
+ * totals = {strips, steps, owner-list entries}. */
+int pm_build_strips(int64_t n_patches, const int32_t *cell_ptr,
+                    const int32_t *cells, const int32_t *cell_edges,
+                    const uint16_t *lents, const int32_t *owned,
+                    const int32_t *ent_ptr, int32_t max_len,
+                    int32_t *patch_strip_ptr, int32_t *strip_step_ptr,
+                    uint16_t *step_v, uint8_t *step_slot, uint8_t *step_flags,
+                    int32_t *step_y, int32_t *patch_y_count,
+                    int32_t *own_y_ptr, int32_t *own_y, int64_t *totals);
 
 /* Device properties used to size grids (SM count, L2 bytes). */
 int pm_device_info(int32_t *sm_count, int64_t *l2_bytes);

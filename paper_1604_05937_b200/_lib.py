@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "_native", "libprismesh_cuda.so")
 PM_OK, PM_EINVAL, PM_ECUDA, PM_EOVERFLOW = 0, 1, 2, 3
 SHARE_NONE, SHARE_VERTICAL, SHARE_HORIZONTAL = 0, 1, 2
 (VARIANT_AUTO, VARIANT_ATOMIC, VARIANT_PATCH, VARIANT_COLUMN, VARIANT_COLORED,
- VARIANT_STREAM) = range(6)
+ VARIANT_STREAM, VARIANT_STRIP) = range(7)
 
 _lib = None
 
@@ -53,6 +53,14 @@ SIGNATURES = {
                                             _i64, _i32, _i32, _i32, _i32,
                                             _vp, _vp, _vp, _vp, _vp, _vp,
                                             _vp, _vp]),
+    "pm_column_mass_strip": (ctypes.c_int, [_i32p, _i32, _i32, _vp,
+                                            ctypes.POINTER(_f64),
+                                            ctypes.POINTER(_f64),
+                                            ctypes.POINTER(_f64), _vp, _vp,
+                                            _i64, _i32, _i32, _i32, _i32,
+                                            _i32] + [_vp] * 14),
+    "pm_build_strips": (ctypes.c_int, [_i64] + [_vp] * 6 + [_i32] +
+                        [_vp] * 10),
     "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
                                        _vp, _vp]),
     "pm_halo_pack": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
@@ -238,6 +246,27 @@ def column_mass_patch(layout, k, base, layers, cmap, xmap, coords, mref, x,
         plan.max_owned, ptr(dplan["cell_ptr"]), ptr(dplan["cells"]),
         ptr(dplan["color_ptr"]), ptr(dplan["ent_ptr"]), ptr(dplan["owned"]),
         ptr(dplan["ents"]), ptr(dplan["lents"]), stream_ptr(stream))
+    check(rc)
+
+
+def column_mass_strip(layout, k, layers, coords, mref, x, y, plan, dplan,
+                      kron, stream=None):
+    """pm_column_mass_strip: y = M x with the strip-patch schedule."""
+    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
+    ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
+    d = layout.delta6()
+    pp = plan.patch
+    rc = host_lib().pm_column_mass_strip(
+        d.ctypes.data_as(_i32p), k, layers, ptr(coords), _f64ptr(m),
+        _f64ptr(mt), _f64ptr(ml), ptr(x), ptr(y), pp.n_patches, plan.W,
+        plan.threads, pp.max_local, plan.max_y, pp.max_owned,
+        ptr(dplan["ent_ptr"]), ptr(dplan["owned"]), ptr(dplan["ents"]),
+        ptr(dplan["strip_ptr"]), ptr(dplan["step_ptr"]),
+        ptr(dplan["step_v"]), ptr(dplan["step_slot"]),
+        ptr(dplan["step_flags"]), ptr(dplan["step_y"]),
+        ptr(dplan["y_count"]), ptr(dplan["own_base"]),
+        ptr(dplan["own_y_ptr"]), ptr(dplan["own_y"]), stream_ptr(stream))
     check(rc)
 
 

@@ -106,3 +106,155 @@ extern "C" int pm_greedy_color_cells(const int32_t *cv, int64_t n_cells,
   if (n_colors) *n_colors = used_max;
   return PM_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Strip planner for the strip-patch column schedule (csrc/strip.cu).
+//
+// Per patch, the visited cells are walked as strips: consecutive cells share
+// an edge, so each step brings exactly one new vertex into a 3-vertex window
+// (the vertex opposite the shared edge leaves).  Greedy: start at the
+// unvisited cell with the fewest unvisited edge-neighbours (ties: lowest
+// visit index), always continue to the unvisited neighbour with the fewest
+// unvisited neighbours; strips are cut at `max_len` cells.
+//
+// Output: one record per step.  A strip starts with three "fill" steps
+// (window slots 0,1,2 <- the first cell's vertices); every following step
+// replaces one slot.  flags bit0 = apply the cell kernel after this step.
+// Each vertex residency (entry into a slot until it leaves / the strip ends)
+// gets a Y slot if the vertex is owned by the patch (local id < n_owned),
+// else -1; y slots are numbered per patch, and for every owned vertex the
+// list of its y slots is returned (CSR over owned vertices, per patch).
+// ---------------------------------------------------------------------------
+#include <algorithm>
+
+extern "C" int pm_build_strips(
+    int64_t n_patches, const int32_t *cell_ptr, const int32_t *cells,
+    const int32_t *cell_edges, const uint16_t *lents, const int32_t *owned,
+    const int32_t *ent_ptr, int32_t max_len,
+    // outputs (capacities: steps <= 3*n_visit, strips <= n_visit)
+    int32_t *patch_strip_ptr, int32_t *strip_step_ptr, uint16_t *step_v,
+    uint8_t *step_slot, uint8_t *step_flags, int32_t *step_y,
+    int32_t *patch_y_count, int32_t *own_y_ptr, int32_t *own_y,
+    int64_t *totals /* [n_strips, n_steps, n_own_y_entries] */) {
+  pm::clear_error();
+  if (n_patches < 0 || max_len < 1) {
+    pm::set_error("pm_build_strips: bad arguments");
+    return PM_EINVAL;
+  }
+  int64_t n_strips = 0, n_steps = 0, n_oy = 0, own_base = 0;
+  strip_step_ptr[0] = 0;
+  (void)ent_ptr;
+  std::vector<int32_t> nb;      // neighbours (visit-local) of each cell, 3 each
+  std::vector<int32_t> deg;
+  std::vector<uint8_t> used;
+  std::vector<std::vector<int32_t>> yl; // per owned vertex: its y slots
+  for (int64_t p = 0; p < n_patches; ++p) {
+    patch_strip_ptr[p] = (int32_t)n_strips;
+    const int32_t c0 = cell_ptr[p], c1 = cell_ptr[p + 1], n = c1 - c0;
+    // edge-adjacency inside the patch
+    std::vector<std::pair<int32_t, int32_t>> ek; // (edge, local cell)
+    ek.reserve(3 * n);
+    for (int32_t i = 0; i < n; ++i)
+      for (int k = 0; k < 3; ++k)
+        ek.push_back({cell_edges[3 * (int64_t)cells[c0 + i] + k], i});
+    std::sort(ek.begin(), ek.end());
+    nb.assign(3 * (size_t)n, -1);
+    for (size_t a = 0; a + 1 < ek.size(); ++a)
+      if (ek[a].first == ek[a + 1].first) {
+        const int32_t u = ek[a].second, w = ek[a + 1].second;
+        for (int k = 0; k < 3; ++k)
+          if (nb[3 * u + k] < 0) { nb[3 * u + k] = w; break; }
+        for (int k = 0; k < 3; ++k)
+          if (nb[3 * w + k] < 0) { nb[3 * w + k] = u; break; }
+      }
+    used.assign(n, 0);
+    deg.assign(n, 0);
+    for (int32_t i = 0; i < n; ++i)
+      for (int k = 0; k < 3; ++k) deg[i] += nb[3 * i + k] >= 0;
+    const int32_t n_own = owned[p];
+    yl.assign(n_own, {});
+    int32_t ycount = 0;
+    auto vid = [&](int32_t i, int k) { return (int32_t)lents[3 * (int64_t)(c0 + i) + k]; };
+    auto take = [&](int32_t i) {
+      used[i] = 1;
+      for (int k = 0; k < 3; ++k) {
+        const int32_t w = nb[3 * i + k];
+        if (w >= 0) --deg[w];
+      }
+    };
+    auto new_y = [&](int32_t v) -> int32_t {
+      if (v >= n_own) return -1;
+      yl[v].push_back(ycount);
+      return ycount++;
+    };
+    int32_t remaining = n;
+    while (remaining > 0) {
+      int32_t cur = -1;
+      for (int32_t i = 0; i < n; ++i)
+        if (!used[i] && (cur < 0 || deg[i] < deg[cur])) cur = i;
+      take(cur);
+      --remaining;
+      int32_t win[3];
+      for (int k = 0; k < 3; ++k) {
+        win[k] = vid(cur, k);
+        step_v[n_steps] = (uint16_t)win[k];
+        step_slot[n_steps] = (uint8_t)k;
+        step_flags[n_steps] = k == 2 ? 1 : 0;
+        step_y[n_steps] = new_y(win[k]);
+        ++n_steps;
+      }
+      int32_t len = 1;
+      while (len < max_len) {
+        int32_t nxt = -1;
+        for (int k = 0; k < 3; ++k) {
+          const int32_t w = nb[3 * cur + k];
+          if (w >= 0 && !used[w] && (nxt < 0 || deg[w] < deg[nxt])) nxt = w;
+        }
+        if (nxt < 0) break;
+        take(nxt);
+        --remaining;
+        // the window vertex not in `nxt` leaves; nxt's third vertex enters
+        int slot = -1;
+        int32_t vin = -1;
+        for (int k = 0; k < 3; ++k) {
+          const int32_t v = win[k];
+          bool in = false;
+          for (int q = 0; q < 3; ++q) in |= vid(nxt, q) == v;
+          if (!in) slot = k;
+        }
+        for (int q = 0; q < 3; ++q) {
+          const int32_t v = vid(nxt, q);
+          if (v != win[0] && v != win[1] && v != win[2]) vin = v;
+        }
+        if (slot < 0 || vin < 0) {
+          pm::set_error("pm_build_strips: neighbours do not share an edge");
+          return PM_EINVAL;
+        }
+        win[slot] = vin;
+        step_v[n_steps] = (uint16_t)vin;
+        step_slot[n_steps] = (uint8_t)slot;
+        step_flags[n_steps] = 1;
+        step_y[n_steps] = new_y(vin);
+        ++n_steps;
+        cur = nxt;
+        ++len;
+      }
+      ++n_strips;
+      strip_step_ptr[n_strips] = (int32_t)n_steps;
+    }
+    patch_y_count[p] = ycount;
+    // owner lists: owned vertices are local ids 0..n_own-1; row of owned
+    // vertex v of patch p is own_base + v (own_base = sum of earlier owned)
+    for (int32_t v = 0; v < n_own; ++v) {
+      own_y_ptr[own_base + v] = (int32_t)n_oy;
+      for (int32_t y : yl[v]) own_y[n_oy++] = y;
+    }
+    own_base += n_own;
+  }
+  own_y_ptr[own_base] = (int32_t)n_oy;
+  patch_strip_ptr[n_patches] = (int32_t)n_strips;
+  totals[0] = n_strips;
+  totals[1] = n_steps;
+  totals[2] = n_oy;
+  return PM_OK;
+}

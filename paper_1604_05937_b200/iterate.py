@@ -20,6 +20,9 @@ Schedules (``schedule=``):
                 ``"column"``.
 ``"patch"``     owner-computes over compact patches, shared-memory
                 accumulation, no atomics, deterministic (schedule.py).
+``"strip"``     vertex-column layouts: patches staged in shared memory,
+                cells walked as strips (one new vertex per cell), owner
+                gather of per-residency partials; deterministic.
 ``"stream"``    DG (2,1) fields through TMA bulk copies (dg_stream.cu).
 ``"column"``    warp segment per column, lanes = layers; vertical sharing
                 in registers, column-shared DoFs via fp64 REDG.
@@ -38,7 +41,7 @@ import numpy as np
 from . import _lib
 
 SCHEDULES = ("auto", "atomic", "colored", "sequential", "column", "stream",
-             "patch")
+             "patch", "strip")
 
 
 @dataclass(frozen=True)

@@ -119,6 +119,7 @@ class MassOperator:
         self.schedule = schedule
         self._coloring = None
         self._patch = None
+        self._strip = None
         self._dev = _lib.cuda_device()
         self.cmap = fs.device_cell_map()
         self.offs = fs.device_offsets()
@@ -148,6 +149,21 @@ class MassOperator:
         """DoFs only on vertex / edge columns (the patch schedule's case)."""
         d = self.fs.layout.delta6()
         return d[4] == 0 and d[5] == 0 and tuple(d) in _PATCH_LAYOUTS
+
+    @property
+    def strip_ok(self) -> bool:
+        d = tuple(self.fs.layout.delta6())
+        return d in _STRIP_LAYOUTS
+
+    def _strip_plan(self):
+        if self._strip is None:
+            from .schedule import build_strip_plan
+            col = _color(self.fs.mesh)
+            plan = build_strip_plan(self.fs.mesh.base, self.fs.layout,
+                                    self.layers, col.color_of,
+                                    col.num_colors)
+            self._strip = (plan, plan.device(self._dev))
+        return self._strip
 
     def _patch_plan(self):
         if self._patch is None:
@@ -185,6 +201,19 @@ class MassOperator:
             sched = "atomic"   # dense Mref in the generic kernel
         if sched == "auto" and self.share == 2 and self.patch_ok:
             sched = "patch"
+        if sched == "strip":
+            if not self.strip_ok:
+                raise ValueError(
+                    f"the strip schedule needs a vertex-column layout, got "
+                    f"{self.fs.layout.name}")
+            plan, dplan = self._strip_plan()
+            out = torch.empty_like(y) if accumulate else y
+            _lib.column_mass_strip(self.fs.layout, self.k, self.layers,
+                                   coords, self.mref, x, out, plan, dplan,
+                                   self.kron, stream=stream)
+            if accumulate:
+                y += out
+            return y
         if sched == "patch":
             if not self.patch_ok:
                 raise ValueError(
@@ -235,6 +264,10 @@ class MassOperator:
 #: layouts compiled into the patch kernel (csrc/patch.cu)
 _PATCH_LAYOUTS = {(1, 0, 0, 0, 0, 0), (0, 1, 0, 0, 0, 0), (0, 2, 0, 0, 0, 0),
                   (1, 1, 1, 1, 0, 0), (3, 0, 0, 0, 0, 0)}
+
+#: layouts compiled into the strip kernel (csrc/strip.cu)
+_STRIP_LAYOUTS = {(1, 0, 0, 0, 0, 0), (0, 1, 0, 0, 0, 0), (0, 2, 0, 0, 0, 0),
+                  (3, 0, 0, 0, 0, 0)}
 
 _VARIANTS = {"auto": _lib.VARIANT_AUTO, "atomic": _lib.VARIANT_ATOMIC,
              "column": _lib.VARIANT_COLUMN, "stream": _lib.VARIANT_STREAM,

@@ -169,3 +169,102 @@ def plan_for(base, layout, layers, colors, n_colors, smem_budget=100 * 1024,
             return plan, W, ch, need
         target = max(16, int(target * smem_budget / need * 0.95))
     return plan, W, ch, need
+
+
+# ---------------------------------------------------------------------------
+# strip-patch schedule (csrc/strip.cu): vertex-column layouts
+# ---------------------------------------------------------------------------
+@dataclass
+class StripPlan:
+    patch: PatchPlan
+    W: int
+    threads: int
+    strip_ptr: np.ndarray      # int32 [n_patches+1] into strip_step_ptr
+    step_ptr: np.ndarray       # int32 [n_strips+1] into steps
+    step_v: np.ndarray         # uint16 local vertex entering the window
+    step_slot: np.ndarray      # uint8 window slot it replaces
+    step_flags: np.ndarray     # uint8 bit0: apply the cell kernel
+    step_y: np.ndarray         # int32 Y slot of the new residency or -1
+    y_count: np.ndarray        # int32 [n_patches]
+    own_base: np.ndarray       # int32 [n_patches] prefix of owned counts
+    own_y_ptr: np.ndarray      # int32 [total_owned+1]
+    own_y: np.ndarray          # int32
+    max_y: int
+    smem: int
+
+    def device(self, dev):
+        import torch
+        d = self.patch.device(dev)
+        for k in ("strip_ptr", "step_ptr", "step_v", "step_slot",
+                  "step_flags", "step_y", "y_count", "own_base", "own_y_ptr",
+                  "own_y"):
+            d[k] = torch.from_numpy(np.ascontiguousarray(getattr(self, k))) \
+                .to(dev)
+        return d
+
+
+def strip_smem(max_local, max_y, max_owned, ch, lv, W):
+    return 8 * (max_local * (W * ch + lv + 3 * (W + 1)) +
+                max_y * ch * (W + 1) + max_owned * lv)
+
+
+def build_strip_plan(base, layout, layers, colors, n_colors,
+                     smem_budget=200 * 1024, W=None, n_sm=148,
+                     max_strip=None):
+    """Patch plan (vertex entities) + strips, sized to the smem budget."""
+    import ctypes
+    from . import _lib
+    d = layout.delta6()
+    if d[2] or d[3] or d[4] or d[5]:
+        raise ValueError("the strip schedule handles vertex-column layouts")
+    lv, ch = int(d[0]), int(d[0] + d[1])
+    threads = 256 if ch > 2 else 512
+    if W is None:
+        W = min((8, 16, 32), key=lambda w: (-(-layers // w) * w / layers
+                                             + 0.05 * (-(-layers // w)), -w))
+    n_cells = base.num_cells
+    cap = max(16, n_cells // (n_sm))
+    # bytes per visited cell: ~0.62 local vertices, ~1.1 Y residencies
+    per_cell = 8 * (0.62 * (W * ch + lv + 3 * (W + 1)) + 1.1 * ch * (W + 1))
+    target = max(16, min(int(smem_budget / per_cell), cap, 4096))
+    for _ in range(10):
+        plan = build_patch_plan(base, False, target, colors, n_colors)
+        n_visit = plan.cells.shape[0]
+        n_p = plan.n_patches
+        strip_ptr = np.zeros(n_p + 1, np.int32)
+        step_ptr = np.zeros(n_visit + 1, np.int32)
+        cap_steps = 3 * n_visit
+        step_v = np.zeros(cap_steps, np.uint16)
+        step_slot = np.zeros(cap_steps, np.uint8)
+        step_flags = np.zeros(cap_steps, np.uint8)
+        step_y = np.zeros(cap_steps, np.int32)
+        y_count = np.zeros(n_p, np.int32)
+        own_total = int(plan.owned.sum())
+        own_y_ptr = np.zeros(own_total + 1, np.int32)
+        own_y = np.zeros(cap_steps, np.int32)
+        totals = np.zeros(3, np.int64)
+        ce = np.ascontiguousarray(base.cell_edges, dtype=np.int32)
+        per_warp = max(4, int(np.ceil(target / (threads // 32) / 1.0)))
+        mlen = max_strip or max(8, min(64, per_warp))
+        P = lambda a, t: a.ctypes.data_as(ctypes.POINTER(t))
+        i32, u16, u8, i64 = (ctypes.c_int32, ctypes.c_uint16, ctypes.c_uint8,
+                             ctypes.c_int64)
+        _lib.check(_lib.host_lib().pm_build_strips(
+            n_p, P(plan.cell_ptr, i32), P(plan.cells, i32), P(ce, i32),
+            P(np.ascontiguousarray(plan.lents), u16), P(plan.owned, i32),
+            P(plan.ent_ptr, i32), mlen, P(strip_ptr, i32), P(step_ptr, i32),
+            P(step_v, u16), P(step_slot, u8), P(step_flags, u8),
+            P(step_y, i32), P(y_count, i32), P(own_y_ptr, i32),
+            P(own_y, i32), P(totals, i64)))
+        n_strips, n_steps, n_oy = (int(v) for v in totals)
+        own_base = np.zeros(n_p, np.int32)
+        np.cumsum(plan.owned[:-1], out=own_base[1:])
+        max_y = int(y_count.max()) if n_p else 0
+        need = strip_smem(plan.max_local, max_y, plan.max_owned, ch, lv, W)
+        if need <= smem_budget or target <= 16:
+            break
+        target = max(16, int(target * smem_budget / need * 0.95))
+    return StripPlan(plan, W, threads, strip_ptr, step_ptr[:n_strips + 1],
+                     step_v[:n_steps], step_slot[:n_steps],
+                     step_flags[:n_steps], step_y[:n_steps], y_count,
+                     own_base, own_y_ptr, own_y[:n_oy], max_y, need)

@@ -126,12 +126,14 @@ def test_arity_and_mesh_mismatch_rejected(gmesh):
         iterate_columns([fs, xfs2], k, [None, None, None])
 
 
-SCHEDULES = ("auto", "atomic", "colored", "column", "patch")
+SCHEDULES = ("auto", "atomic", "colored", "column", "patch", "strip")
 
 
 def _schedule_applies(lname, schedule):
     if schedule == "patch":
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "P2xP2", "VP1")
+    if schedule == "strip":
+        return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1")
     return True
 
 
@@ -178,9 +180,11 @@ def test_iterate_columns_accumulates(gmesh, lname):
 
 
 @pytest.mark.parametrize("lname", ("CG1xCG1", "P2xP2", "VP1", "CG1xDG1"))
-@pytest.mark.parametrize("schedule", ("colored", "patch"))
+@pytest.mark.parametrize("schedule", ("colored", "patch", "strip"))
 def test_deterministic_schedules(gmesh, lname, schedule):
     from paper_1604_05937_b200.kernels import mass_action
+    if not _schedule_applies(lname, schedule):
+        pytest.skip("schedule not defined for this layout")
     fs = _space(gmesh("sq5"), 4, lname)
     f = torch.rand(fs.total_dofs, dtype=torch.float64, device="cuda")
     a = mass_action(fs, f, schedule=schedule)
@@ -353,3 +357,27 @@ def test_halo_kernels_match_host():
     d = (y2 - y).cpu().numpy()
     for c in (100, 300, 650):
         np.testing.assert_array_equal(d[c - 50:c - 50 + 7], yh[c - 50:c - 50 + 7])
+
+
+@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1", "CG1xDG1", "CG1xDG0"))
+@pytest.mark.parametrize("W", (8, 16, 32))
+@pytest.mark.parametrize("layers", (1, 7, 33, 64))
+def test_strip_chunk_widths(lname, W, layers):
+    """Strip schedule: every chunk width, ragged tails, small patches."""
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator, _color
+    from paper_1604_05937_b200.schedule import build_strip_plan
+    w = configs.Workload("sw", 14, layers, lname, quad_degrees(lname),
+                         ordering="random", jitter=0.2)
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    op = MassOperator(fs, quad, schedule="strip")
+    col = _color(m)
+    plan = build_strip_plan(m.base, fs.layout, layers, col.color_of,
+                            col.num_colors, W=W, smem_budget=48 * 1024,
+                            max_strip=11)
+    op._strip = (plan, plan.device(op._dev))
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    y = op.apply(torch.from_numpy(x).cuda(), coords).cpu().numpy()
+    ref = _oracle_for(w, fs).assemble(x)
+    assert _rel(y, ref) <= 1e-10

@@ -1,0 +1,122 @@
+"""Host planner of the strip-patch schedule + a numpy emulation of its
+kernel's accounting (window, residencies, Y slots, owner gather)."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import LAYOUT_COUNTS, families, quad_degrees
+
+
+def _plan(n, layers, lname, ordering="rcm", jitter=0.0, budget=200 * 1024,
+          max_strip=None):
+    from paper_1604_05937_b200 import DofLayout, ExtrudedMesh, number_dofs
+    from paper_1604_05937_b200.configs import base_mesh
+    from paper_1604_05937_b200.iterate import color_base_cells
+    from paper_1604_05937_b200.schedule import build_strip_plan
+    base, _ = base_mesh(n, ordering, jitter)
+    fs = number_dofs(ExtrudedMesh(base, layers),
+                     DofLayout(lname, LAYOUT_COUNTS[lname]))
+    col = color_base_cells(base)
+    plan = build_strip_plan(base, fs.layout, layers, col.color_of,
+                            col.num_colors, smem_budget=budget,
+                            max_strip=max_strip)
+    return fs, plan
+
+
+@pytest.mark.parametrize("n,budget", ((6, 8 * 1024), (12, 40 * 1024),
+                                      (20, 200 * 1024)))
+def test_strip_plan_invariants(n, budget):
+    fs, plan = _plan(n, 4, "CG1xCG1", budget=budget, max_strip=7)
+    pp = plan.patch
+    cv = fs.mesh.base.cell_vertices
+    for p in range(pp.n_patches):
+        ents = pp.ents[pp.ent_ptr[p]:pp.ent_ptr[p + 1]]
+        visited = set(pp.cells[pp.cell_ptr[p]:pp.cell_ptr[p + 1]].tolist())
+        seen = []
+        ys = []
+        for s in range(plan.strip_ptr[p], plan.strip_ptr[p + 1]):
+            win = [None, None, None]
+            for k in range(plan.step_ptr[s], plan.step_ptr[s + 1]):
+                win[plan.step_slot[k]] = int(ents[plan.step_v[k]])
+                if plan.step_y[k] >= 0:
+                    ys.append(int(plan.step_y[k]))
+                    assert plan.step_v[k] < pp.owned[p]
+                if plan.step_flags[k] & 1:
+                    cell = np.flatnonzero(
+                        (np.sort(cv, axis=1) == sorted(win)).all(axis=1))
+                    assert cell.size == 1
+                    seen.append(int(cell[0]))
+        assert sorted(seen) == sorted(visited), "each visited cell once"
+        assert sorted(ys) == list(range(plan.y_count[p])), "y slots unique"
+
+
+@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1", "CG1xDG1", "CG1xDG0"))
+@pytest.mark.parametrize("ordering", ("rcm", "random"))
+def test_strip_emulation_matches_oracle(lname, ordering):
+    """Run the kernel's algorithm in numpy (all layers at once)."""
+    from paper_1604_05937_b200.quadrature import (element_for_layout,
+                                                  kronecker_factors,
+                                                  prism_quadrature)
+    layers = 3
+    fs, plan = _plan(10, layers, lname, ordering, jitter=0.2,
+                     budget=30 * 1024, max_strip=9)
+    pp = plan.patch
+    base = fs.mesh.base
+    el = element_for_layout(fs.layout)
+    q = prism_quadrature(*quad_degrees(lname))
+    Mt, Ml = kronecker_factors(el, q)
+    h, v, c = (np.array(a) for a in (el.slot_h, el.slot_v, el.slot_comp))
+    M = Mt[h][:, h] * Ml[v][:, v] * (c[:, None] == c[None, :])
+    slots = fs.slots
+    x = np.random.default_rng(3).random(fs.total_dofs)
+    from paper_1604_05937_b200 import COORDS_LAYOUT
+    coords = oracle.extrude(base.coords, layers, 1.0 / layers)
+    col0 = fs.column_sizes[0]
+    lv = fs.layout.dofs(0, 0)
+    y = np.zeros(fs.total_dofs)
+    for p in range(pp.n_patches):
+        ents = pp.ents[pp.ent_ptr[p]:pp.ent_ptr[p + 1]]
+        Y = {}
+        for s in range(plan.strip_ptr[p], plan.strip_ptr[p + 1]):
+            win = [None] * 3
+            ysl = [-1] * 3
+            acc = [None] * 3
+
+            def flush(a):
+                if win[a] is not None and ysl[a] >= 0:
+                    Y[ysl[a]] = acc[a]
+            for k in range(plan.step_ptr[s], plan.step_ptr[s + 1]):
+                a = plan.step_slot[k]
+                flush(a)
+                win[a] = int(ents[plan.step_v[k]])
+                ysl[a] = int(plan.step_y[k])
+                acc[a] = np.zeros(col0)
+                if plan.step_flags[k] & 1:
+                    for l in range(layers):
+                        P = np.array([[coords[3 * (win[b] * (layers + 1) + l + t) + qq]
+                                       for t in (0, 1) for qq in range(3)]
+                                      for b in range(3)])
+                        xm = (P[:, 0] + P[:, 3]) / 2
+                        ym = (P[:, 1] + P[:, 4]) / 2
+                        a2 = (xm[1] - xm[0]) * (ym[2] - ym[0]) - \
+                            (xm[2] - xm[0]) * (ym[1] - ym[0])
+                        hh = ((P[0, 5] - P[0, 2]) + (P[1, 5] - P[1, 2]) +
+                              (P[2, 5] - P[2, 2])) / 3
+                        det = abs(a2 * hh)
+                        idx = [win[sl.local] * col0 + sl.within(fs.layout) +
+                               l * (fs.layout.dofs(0, 0) + fs.layout.dofs(0, 1))
+                               for sl in slots]
+                        loc = det * (M @ x[idx])
+                        for j, sl in enumerate(slots):
+                            acc[sl.local][idx[j] - win[sl.local] * col0] += loc[j]
+            for a in range(3):
+                flush(a)
+        for i in range(pp.owned[p]):
+            g = int(ents[i])
+            row = plan.own_base[p] + i
+            for yy in plan.own_y[plan.own_y_ptr[row]:plan.own_y_ptr[row + 1]]:
+                y[g * col0:(g + 1) * col0] += Y[int(yy)]
+    tri, line, nc = families(lname)
+    ref = oracle.Problem(base, layers, LAYOUT_COUNTS[lname], tri, line, nc,
+                         *quad_degrees(lname)).assemble(x)
+    np.testing.assert_allclose(y, ref, rtol=0, atol=1e-14 * np.abs(ref).max())
