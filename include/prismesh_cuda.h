@@ -139,7 +139,8 @@ int pm_column_mass_strip(const int32_t *delta6, int32_t k, int32_t layers,
                          const double *mtri, const double *mline,
                          const double *x, double *y, int64_t n_patches,
                          int32_t chunk, int32_t threads, int32_t max_local,
-                         int32_t max_y, int32_t max_owned,
+                         int32_t max_y, int32_t max_owned, int32_t max_steps,
+                         int32_t max_strips, int32_t max_oy,
                          const int32_t *ent_ptr, const int32_t *owned,
                          const int32_t *ents, const int32_t *patch_strip_ptr,
                          const int32_t *strip_step_ptr, const uint16_t *step_v,

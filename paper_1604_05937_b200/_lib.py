@@ -58,7 +58,8 @@ SIGNATURES = {
                                             ctypes.POINTER(_f64),
                                             ctypes.POINTER(_f64), _vp, _vp,
                                             _i64, _i32, _i32, _i32, _i32,
-                                            _i32] + [_vp] * 14),
+                                            _i32, _i32, _i32, _i32] +
+                            [_vp] * 14),
     "pm_build_strips": (ctypes.c_int, [_i64] + [_vp] * 6 + [_i32] +
                         [_vp] * 10),
     "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
@@ -261,7 +262,7 @@ def column_mass_strip(layout, k, layers, coords, mref, x, y, plan, dplan,
         d.ctypes.data_as(_i32p), k, layers, ptr(coords), _f64ptr(m),
         _f64ptr(mt), _f64ptr(ml), ptr(x), ptr(y), pp.n_patches, plan.W,
         plan.threads, pp.max_local, plan.max_y, pp.max_owned,
-        ptr(dplan["ent_ptr"]), ptr(dplan["owned"]), ptr(dplan["ents"]),
+        plan.max_steps, plan.max_strips, plan.max_oy, ptr(dplan["ent_ptr"]), ptr(dplan["owned"]), ptr(dplan["ents"]),
         ptr(dplan["strip_ptr"]), ptr(dplan["step_ptr"]),
         ptr(dplan["step_v"]), ptr(dplan["step_slot"]),
         ptr(dplan["step_flags"]), ptr(dplan["step_y"]),

@@ -32,6 +32,7 @@ struct StripDev {
   const int32_t *step_y;
   const int32_t *patch_y_count, *own_base, *own_y_ptr, *own_y;
   int32_t max_local, max_y, max_owned;
+  int32_t max_steps, max_strips, max_oy; // per-patch maxima (smem sizing)
   int64_t column0; // Alg. 1 vertex column length
 };
 
@@ -59,6 +60,11 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
   double *sC = sF + (size_t)P.max_local * FS;        // [max_local][CS]
   double *sY = sC + (size_t)P.max_local * CS;        // [max_y][CH][YS]
   double *sCarry = sY + (size_t)P.max_y * CH * YS;   // [max_owned][LV]
+  // per-patch plan records, staged once per patch
+  int2 *sStep = reinterpret_cast<int2 *>(sCarry + (size_t)P.max_owned * LVA);
+  int *sSPtr = reinterpret_cast<int *>(sStep + P.max_steps);   // strips+1
+  int *sOPtr = sSPtr + P.max_strips + 1;                       // owned+1
+  int *sOY = sOPtr + P.max_owned + 1;                          // y entries
 
   const int lane = threadIdx.x & 31;
   const int sl = lane % W, seg = lane / W;
@@ -74,21 +80,38 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
     const int n_strips = __ldg(P.patch_strip_ptr + p + 1) - sb;
     const int obase = __ldg(P.own_base + p);
     for (int i = threadIdx.x; i < n_own * LV; i += blockDim.x) sCarry[i] = 0.0;
+    // plan records of this patch -> shared memory (one dependent global
+    // round trip per patch instead of one per strip step)
+    const int kb = __ldg(P.strip_step_ptr + sb);
+    const int n_steps = __ldg(P.strip_step_ptr + sb + n_strips) - kb;
+    for (int i = threadIdx.x; i < n_steps; i += blockDim.x) {
+      const int kk = kb + i;
+      sStep[i] = make_int2((int)__ldg(P.step_v + kk) |
+                               ((int)__ldg(P.step_slot + kk) << 16) |
+                               ((int)__ldg(P.step_flags + kk) << 24),
+                           __ldg(P.step_y + kk));
+    }
+    for (int i = threadIdx.x; i <= n_strips; i += blockDim.x)
+      sSPtr[i] = __ldg(P.strip_step_ptr + sb + i) - kb;
+    const int ob = __ldg(P.own_y_ptr + obase);
+    for (int i = threadIdx.x; i <= n_own; i += blockDim.x)
+      sOPtr[i] = __ldg(P.own_y_ptr + obase + i) - ob;
+    const int n_oy = __ldg(P.own_y_ptr + obase + n_own) - ob;
+    for (int i = threadIdx.x; i < n_oy; i += blockDim.x)
+      sOY[i] = __ldg(P.own_y + ob + i);
 
     for (int l0 = 0; l0 < layers; l0 += W) {
       const int nl = min(W, layers - l0);
       // ---------------- stage: local vertex columns of the chunk
       {
+        // warp per vertex column segment: contiguous, coalesced
         const int fl = nl * CH + LV, cl = 3 * (nl + 1);
-        for (int i = threadIdx.x; i < n_loc * fl; i += blockDim.x) {
-          const int v = i / fl, e = i - v * fl;
+        for (int v = warp; v < n_loc; v += n_warps) {
           const int64_t g = __ldg(P.ents + eb + v);
-          sF[v * FS + e] = __ldg(x + g * P.column0 + (int64_t)l0 * CH + e);
-        }
-        for (int i = threadIdx.x; i < n_loc * cl; i += blockDim.x) {
-          const int v = i / cl, e = i - v * cl;
-          const int64_t g = __ldg(P.ents + eb + v);
-          sC[v * CS + e] = __ldg(coords + g * cstride + 3 * (int64_t)l0 + e);
+          const double *fx = x + g * P.column0 + (int64_t)l0 * CH;
+          const double *fc = coords + g * cstride + 3 * (int64_t)l0;
+          for (int e = lane; e < fl; e += 32) sF[v * FS + e] = __ldg(fx + e);
+          for (int e = lane; e < cl; e += 32) sC[v * CS + e] = __ldg(fc + e);
         }
       }
       __syncthreads();
@@ -98,8 +121,8 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
       for (int s0 = warp * SEGS; s0 < n_strips; s0 += n_warps * SEGS) {
         const int si = s0 + seg;
         const bool has = si < n_strips;
-        const int k0 = has ? __ldg(P.strip_step_ptr + sb + si) : 0;
-        const int k1 = has ? __ldg(P.strip_step_ptr + sb + si + 1) : 0;
+        const int k0 = has ? sSPtr[si] : 0;
+        const int k1 = has ? sSPtr[si + 1] : 0;
         int len = k1 - k0, maxlen = len;
 #pragma unroll
         for (int o = W; o < 32; o <<= 1)
@@ -151,11 +174,11 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
         };
         for (int k = 0; k < maxlen; ++k) {
           const bool act = k < len;
-          const int kk = k0 + k;
-          const int v = act ? (int)__ldg(P.step_v + kk) : 0;
-          const int slot = act ? (int)__ldg(P.step_slot + kk) : 3;
-          const int flg = act ? (int)__ldg(P.step_flags + kk) : 0;
-          const int ynew = act ? __ldg(P.step_y + kk) : -1;
+          const int2 rec = act ? sStep[k0 + k] : make_int2(3 << 16, -1);
+          const int v = rec.x & 0xffff;
+          const int slot = (rec.x >> 16) & 0xff;
+          const int flg = (rec.x >> 24) & 0xff;
+          const int ynew = rec.y;
           // the leaving vertex's partial column goes to its Y slot
           flush(slot); // shuffles run on every lane; stores predicated
 #pragma unroll
@@ -215,11 +238,10 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
         const int s = s0 + seg;
         if (s >= n_streams) continue;
         const int i = s / CH, c = s - i * CH;
-        const int y0 = __ldg(P.own_y_ptr + obase + i);
-        const int y1 = __ldg(P.own_y_ptr + obase + i + 1);
+        const int y0 = sOPtr[i], y1 = sOPtr[i + 1];
         double v = 0.0, top = 0.0;
         for (int q = y0; q < y1; ++q) {
-          const double *row = sY + ((size_t)__ldg(P.own_y + q) * CH + c) * YS;
+          const double *row = sY + ((size_t)sOY[q] * CH + c) * YS;
           if (sl < nl) v += row[sl];
           if (c < LV && sl == 0) top += row[nl];
         }
@@ -250,10 +272,13 @@ static int strip_k(const LoopArgs &a, const StripDev &P, int64_t n_patches,
   KronMat M;
   for (int i = 0; i < LY::NH * LY::NH; ++i) M.t[i] = a.mtri[i];
   for (int i = 0; i < LY::NV * LY::NV; ++i) M.l[i] = a.mline[i];
+  constexpr int LVA = LV > 0 ? LV : 1;
   const size_t smem =
       sizeof(double) * ((size_t)P.max_local * (W * CH + LV + 3 * (W + 1)) +
                         (size_t)P.max_y * CH * (W + 1) +
-                        (size_t)P.max_owned * LV);
+                        (size_t)P.max_owned * LVA) +
+      sizeof(int2) * (size_t)P.max_steps +
+      sizeof(int) * ((size_t)P.max_strips + 1 + P.max_owned + 1 + P.max_oy);
   if (smem > 227 * 1024) {
     set_error("strip plan needs %zu bytes of shared memory", smem);
     return PM_EINVAL;
@@ -313,6 +338,7 @@ extern "C" int pm_column_mass_strip(
     const double *mref, const double *mtri, const double *mline,
     const double *x, double *y, int64_t n_patches, int32_t chunk,
     int32_t threads, int32_t max_local, int32_t max_y, int32_t max_owned,
+    int32_t max_steps, int32_t max_strips, int32_t max_oy,
     const int32_t *ent_ptr, const int32_t *owned, const int32_t *ents,
     const int32_t *patch_strip_ptr, const int32_t *strip_step_ptr,
     const uint16_t *step_v, const uint8_t *step_slot,
@@ -365,6 +391,9 @@ extern "C" int pm_column_mass_strip(
   P.max_local = max_local;
   P.max_y = max_y;
   P.max_owned = max_owned;
+  P.max_steps = max_steps;
+  P.max_strips = max_strips;
+  P.max_oy = max_oy;
   P.column0 = (int64_t)layers * (delta6[0] + delta6[1]) + delta6[0];
 #define PM_DISPATCH(a_, b_, c_, e_, f_, g_)                                  \
   if (pm::Layout<a_, b_, c_, e_, f_, g_>::matches(delta6))                   \

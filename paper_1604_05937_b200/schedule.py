@@ -191,6 +191,9 @@ class StripPlan:
     own_y: np.ndarray          # int32
     max_y: int
     smem: int
+    max_steps: int = 0
+    max_strips: int = 0
+    max_oy: int = 0
 
     def device(self, dev):
         import torch
@@ -203,9 +206,11 @@ class StripPlan:
         return d
 
 
-def strip_smem(max_local, max_y, max_owned, ch, lv, W):
-    return 8 * (max_local * (W * ch + lv + 3 * (W + 1)) +
-                max_y * ch * (W + 1) + max_owned * lv)
+def strip_smem(max_local, max_y, max_owned, ch, lv, W, max_steps=0,
+               max_strips=0, max_oy=0):
+    return (8 * (max_local * (W * ch + lv + 3 * (W + 1)) +
+                 max_y * ch * (W + 1) + max_owned * max(lv, 1)) +
+            8 * max_steps + 4 * (max_strips + 1 + max_owned + 1 + max_oy))
 
 
 def build_strip_plan(base, layout, layers, colors, n_colors,
@@ -260,11 +265,18 @@ def build_strip_plan(base, layout, layers, colors, n_colors,
         own_base = np.zeros(n_p, np.int32)
         np.cumsum(plan.owned[:-1], out=own_base[1:])
         max_y = int(y_count.max()) if n_p else 0
-        need = strip_smem(plan.max_local, max_y, plan.max_owned, ch, lv, W)
+        steps_pp = step_ptr[strip_ptr[1:]] - step_ptr[strip_ptr[:-1]]
+        max_steps = int(steps_pp.max()) if n_p else 0
+        max_strips = int(np.diff(strip_ptr).max()) if n_p else 0
+        oy_pp = own_y_ptr[own_base + plan.owned] - own_y_ptr[own_base]
+        max_oy = int(oy_pp.max()) if n_p else 0
+        need = strip_smem(plan.max_local, max_y, plan.max_owned, ch, lv, W,
+                          max_steps, max_strips, max_oy)
         if need <= smem_budget or target <= 16:
             break
         target = max(16, int(target * smem_budget / need * 0.95))
     return StripPlan(plan, W, threads, strip_ptr, step_ptr[:n_strips + 1],
                      step_v[:n_steps], step_slot[:n_steps],
                      step_flags[:n_steps], step_y[:n_steps], y_count,
-                     own_base, own_y_ptr, own_y[:n_oy], max_y, need)
+                     own_base, own_y_ptr, own_y[:n_oy], max_y, need,
+                     max_steps, max_strips, max_oy)
