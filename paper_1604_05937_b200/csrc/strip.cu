@@ -24,6 +24,17 @@
 
 namespace pm {
 
+__device__ __forceinline__ void cp_async8(double *dst, const double *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
 struct StripDev {
   const int32_t *ent_ptr, *owned, *ents;
   const int32_t *patch_strip_ptr, *strip_step_ptr;
@@ -36,13 +47,16 @@ struct StripDev {
   int64_t column0; // Alg. 1 vertex column length
 };
 
-// 512 threads for scalar layouts, 256 (more registers) for the 3-vector
-template <class LY> constexpr int strip_threads() {
-  return LY::CH0 > 2 ? 256 : 512;
+// 256 threads per CTA, two CTAs per SM (one stages while the other walks
+// its strips)
+template <class LY> constexpr int strip_threads() { return 256; }
+// the 3-vector window needs ~170 registers: one CTA per SM there
+template <class LY> constexpr int strip_min_blocks() {
+  return LY::CH0 > 2 ? 1 : 2;
 }
 
 template <class LY, int W, int K = LY::K>
-__global__ void __launch_bounds__(strip_threads<LY>())
+__global__ void __launch_bounds__(strip_threads<LY>(), strip_min_blocks<LY>())
 k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
         const double *__restrict__ coords, const double *__restrict__ x,
         double *__restrict__ y) {
@@ -104,15 +118,17 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
       const int nl = min(W, layers - l0);
       // ---------------- stage: local vertex columns of the chunk
       {
-        // warp per vertex column segment: contiguous, coalesced
+        // warp per vertex column segment (contiguous, coalesced), copied
+        // with cp.async so every copy of the chunk is in flight at once
         const int fl = nl * CH + LV, cl = 3 * (nl + 1);
         for (int v = warp; v < n_loc; v += n_warps) {
           const int64_t g = __ldg(P.ents + eb + v);
           const double *fx = x + g * P.column0 + (int64_t)l0 * CH;
           const double *fc = coords + g * cstride + 3 * (int64_t)l0;
-          for (int e = lane; e < fl; e += 32) sF[v * FS + e] = __ldg(fx + e);
-          for (int e = lane; e < cl; e += 32) sC[v * CS + e] = __ldg(fc + e);
+          for (int e = lane; e < fl; e += 32) cp_async8(sF + v * FS + e, fx + e);
+          for (int e = lane; e < cl; e += 32) cp_async8(sC + v * CS + e, fc + e);
         }
+        cp_async_wait_all();
       }
       __syncthreads();
 

@@ -214,7 +214,7 @@ def strip_smem(max_local, max_y, max_owned, ch, lv, W, max_steps=0,
 
 
 def build_strip_plan(base, layout, layers, colors, n_colors,
-                     smem_budget=200 * 1024, W=None, n_sm=148,
+                     smem_budget=110 * 1024, W=None, n_sm=148,
                      max_strip=None):
     """Patch plan (vertex entities) + strips, sized to the smem budget."""
     import ctypes
@@ -223,12 +223,14 @@ def build_strip_plan(base, layout, layers, colors, n_colors,
     if d[2] or d[3] or d[4] or d[5]:
         raise ValueError("the strip schedule handles vertex-column layouts")
     lv, ch = int(d[0]), int(d[0] + d[1])
-    threads = 256 if ch > 2 else 512
+    threads = 256
+    if ch > 2:                 # one CTA per SM (register-bound window)
+        smem_budget = max(smem_budget, 200 * 1024)
     if W is None:
         W = min((8, 16, 32), key=lambda w: (-(-layers // w) * w / layers
                                              + 0.05 * (-(-layers // w)), -w))
     n_cells = base.num_cells
-    cap = max(16, n_cells // (n_sm))
+    cap = max(16, n_cells // (2 * n_sm))
     # bytes per visited cell: ~0.62 local vertices, ~1.1 Y residencies
     per_cell = 8 * (0.62 * (W * ch + lv + 3 * (W + 1)) + 1.1 * ch * (W + 1))
     target = max(16, min(int(smem_budget / per_cell), cap, 4096))
