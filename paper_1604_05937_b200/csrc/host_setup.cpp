@@ -242,6 +242,34 @@ extern "C" int pm_build_strips(
       ++n_strips;
       strip_step_ptr[n_strips] = (int32_t)n_steps;
     }
+    // longest strips first (the kernel hands strips out dynamically)
+    {
+      const int64_t s_lo = patch_strip_ptr[p], s_hi = n_strips;
+      const int64_t k_lo = strip_step_ptr[s_lo], k_hi = strip_step_ptr[s_hi];
+      std::vector<int64_t> ord(s_hi - s_lo);
+      for (int64_t i = 0; i < (int64_t)ord.size(); ++i) ord[i] = s_lo + i;
+      std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+        return strip_step_ptr[a + 1] - strip_step_ptr[a] >
+               strip_step_ptr[b + 1] - strip_step_ptr[b];
+      });
+      std::vector<uint16_t> tv(step_v + k_lo, step_v + k_hi);
+      std::vector<uint8_t> ts(step_slot + k_lo, step_slot + k_hi);
+      std::vector<uint8_t> tf(step_flags + k_lo, step_flags + k_hi);
+      std::vector<int32_t> ty(step_y + k_lo, step_y + k_hi);
+      std::vector<int32_t> tp(strip_step_ptr + s_lo, strip_step_ptr + s_hi + 1);
+      int64_t k = k_lo;
+      for (int64_t i = 0; i < (int64_t)ord.size(); ++i) {
+        const int64_t a = tp[ord[i] - s_lo] - k_lo, b = tp[ord[i] - s_lo + 1] - k_lo;
+        strip_step_ptr[s_lo + i] = (int32_t)k;
+        for (int64_t q = a; q < b; ++q, ++k) {
+          step_v[k] = tv[q];
+          step_slot[k] = ts[q];
+          step_flags[k] = tf[q];
+          step_y[k] = ty[q];
+        }
+      }
+      strip_step_ptr[s_hi] = (int32_t)k;
+    }
     patch_y_count[p] = ycount;
     // owner lists: owned vertices are local ids 0..n_own-1; row of owned
     // vertex v of patch p is own_base + v (own_base = sum of earlier owned)

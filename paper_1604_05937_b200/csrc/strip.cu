@@ -79,6 +79,7 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
   int *sSPtr = reinterpret_cast<int *>(sStep + P.max_steps);   // strips+1
   int *sOPtr = sSPtr + P.max_strips + 1;                       // owned+1
   int *sOY = sOPtr + P.max_owned + 1;                          // y entries
+  __shared__ int sCounter[1];
 
   const int lane = threadIdx.x & 31;
   const int sl = lane % W, seg = lane / W;
@@ -130,11 +131,17 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
         }
         cp_async_wait_all();
       }
+      if (threadIdx.x == 0) sCounter[0] = 0;
       __syncthreads();
 
-      // ---------------- strips
+      // ---------------- strips: segments grab strips dynamically (the
+      // planner orders them longest first), which balances the warps
       const bool lane_ok = sl < nl;
-      for (int s0 = warp * SEGS; s0 < n_strips; s0 += n_warps * SEGS) {
+      for (;;) {
+        int s0 = 0;
+        if (lane == 0) s0 = atomicAdd(sCounter, SEGS);
+        s0 = __shfl_sync(FULL, s0, 0);
+        if (s0 >= n_strips) break;
         const int si = s0 + seg;
         const bool has = si < n_strips;
         const int k0 = has ? sSPtr[si] : 0;

@@ -251,8 +251,7 @@ def build_strip_plan(base, layout, layers, colors, n_colors,
         own_y = np.zeros(cap_steps, np.int32)
         totals = np.zeros(3, np.int64)
         ce = np.ascontiguousarray(base.cell_edges, dtype=np.int32)
-        per_warp = max(4, int(np.ceil(target / (threads // 32) / 1.0)))
-        mlen = max_strip or max(8, min(64, per_warp))
+        mlen = max_strip or 24
         P = lambda a, t: a.ctypes.data_as(ctypes.POINTER(t))
         i32, u16, u8, i64 = (ctypes.c_int32, ctypes.c_uint16, ctypes.c_uint8,
                              ctypes.c_int64)
