@@ -187,6 +187,33 @@ extern "C" int pm_build_strips(
       yl[v].push_back(ycount);
       return ycount++;
     };
+    // neighbour of visit-local cell i across the edge {u, w} (or -1)
+    auto across = [&](int32_t i, int32_t u, int32_t w) -> int32_t {
+      for (int k = 0; k < 3; ++k) {
+        const int32_t j = nb[3 * i + k];
+        if (j < 0) continue;
+        int hit = 0;
+        for (int q = 0; q < 3; ++q) hit += vid(j, q) == u || vid(j, q) == w;
+        if (hit == 2) return j;
+      }
+      return -1;
+    };
+    auto third = [&](int32_t i, int32_t u, int32_t w) -> int32_t {
+      for (int q = 0; q < 3; ++q)
+        if (vid(i, q) != u && vid(i, q) != w) return vid(i, q);
+      return -1;
+    };
+    auto push = [&](int32_t v, int slot, int flags) {
+      step_v[n_steps] = (uint16_t)v;
+      step_slot[n_steps] = (uint8_t)slot;
+      step_flags[n_steps] = (uint8_t)flags;
+      step_y[n_steps] = new_y(v);
+      ++n_steps;
+    };
+    // Sequential strips: the window is kept in age order and the next cell
+    // is always the one across the edge of the two youngest vertices, so
+    // the replaced window slot cycles 0,1,2,0,... (compile-time in the
+    // kernel after a 3-way unroll).
     int32_t remaining = n;
     while (remaining > 0) {
       int32_t cur = -1;
@@ -194,50 +221,49 @@ extern "C" int pm_build_strips(
         if (!used[i] && (cur < 0 || deg[i] < deg[cur])) cur = i;
       take(cur);
       --remaining;
-      int32_t win[3];
-      for (int k = 0; k < 3; ++k) {
-        win[k] = vid(cur, k);
-        step_v[n_steps] = (uint16_t)win[k];
-        step_slot[n_steps] = (uint8_t)k;
-        step_flags[n_steps] = k == 2 ? 1 : 0;
-        step_y[n_steps] = new_y(win[k]);
-        ++n_steps;
+      // choose the first step (and the zig-zag direction) greedily
+      int32_t w0 = vid(cur, 0), w1 = vid(cur, 1), w2 = vid(cur, 2);
+      int32_t best_next = -1, best_score = -1;
+      int32_t bw[3] = {w0, w1, w2};
+      for (int e = 0; e < 3; ++e) {
+        const int32_t a0 = vid(cur, e), a1 = vid(cur, (e + 1) % 3),
+                      a2 = vid(cur, (e + 2) % 3);
+        const int32_t j = across(cur, a1, a2);
+        if (j < 0 || used[j]) continue;
+        for (int dir = 0; dir < 2; ++dir) {
+          const int32_t u = dir ? a2 : a1, w = dir ? a1 : a2; // window a0,u,w
+          const int32_t nv = third(j, u, w);
+          const int32_t j2 = across(j, w, nv);
+          const int32_t score = (j2 >= 0 && !used[j2] && j2 != cur ? 2 : 1) * 64 -
+                                deg[j];
+          if (score > best_score) {
+            best_score = score;
+            best_next = j;
+            bw[0] = a0, bw[1] = u, bw[2] = w;
+          }
+        }
       }
-      int32_t len = 1;
-      while (len < max_len) {
-        int32_t nxt = -1;
-        for (int k = 0; k < 3; ++k) {
-          const int32_t w = nb[3 * cur + k];
-          if (w >= 0 && !used[w] && (nxt < 0 || deg[w] < deg[nxt])) nxt = w;
-        }
-        if (nxt < 0) break;
-        take(nxt);
-        --remaining;
-        // the window vertex not in `nxt` leaves; nxt's third vertex enters
-        int slot = -1;
-        int32_t vin = -1;
-        for (int k = 0; k < 3; ++k) {
-          const int32_t v = win[k];
-          bool in = false;
-          for (int q = 0; q < 3; ++q) in |= vid(nxt, q) == v;
-          if (!in) slot = k;
-        }
-        for (int q = 0; q < 3; ++q) {
-          const int32_t v = vid(nxt, q);
-          if (v != win[0] && v != win[1] && v != win[2]) vin = v;
-        }
-        if (slot < 0 || vin < 0) {
+      int32_t win[3] = {bw[0], bw[1], bw[2]};
+      for (int k = 0; k < 3; ++k) push(win[k], k, k == 2 ? 1 : 0);
+      int32_t len = 1, slot = 0; // next slot to replace (the oldest)
+      int32_t next = best_next;
+      while (next >= 0 && len < max_len) {
+        const int32_t y1 = win[(slot + 1) % 3], y2 = win[(slot + 2) % 3];
+        const int32_t nv = third(next, y1, y2);
+        if (nv < 0) {
           pm::set_error("pm_build_strips: neighbours do not share an edge");
           return PM_EINVAL;
         }
-        win[slot] = vin;
-        step_v[n_steps] = (uint16_t)vin;
-        step_slot[n_steps] = (uint8_t)slot;
-        step_flags[n_steps] = 1;
-        step_y[n_steps] = new_y(vin);
-        ++n_steps;
-        cur = nxt;
+        take(next);
+        --remaining;
+        win[slot] = nv;
+        push(nv, slot, 1);
+        cur = next;
+        slot = (slot + 1) % 3;
         ++len;
+        // the next cell lies across the edge of the two youngest vertices
+        const int32_t j = across(cur, win[(slot + 1) % 3], win[(slot + 2) % 3]);
+        next = (j >= 0 && !used[j]) ? j : -1;
       }
       ++n_strips;
       strip_step_ptr[n_strips] = (int32_t)n_steps;

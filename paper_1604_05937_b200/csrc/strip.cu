@@ -22,6 +22,8 @@
 // Deterministic (fixed slot order), no zeroing pass.
 #include "column_layout.cuh"
 
+#include <type_traits>
+
 namespace pm {
 
 __device__ __forceinline__ void cp_async8(double *dst, const double *src) {
@@ -163,95 +165,91 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
 #pragma unroll
           for (int q = 0; q < 3; ++q) cb[a][q] = 0.0, ct[a][q] = 0.0;
         }
-        // partial column of the window slot `a` (a = 3: none) -> its Y
-        // slot; lanes = levels, top contributions shifted up one lane
-        auto flush = [&](int a) {
-          double lb[CH], lt[LVA];
-          int ly = -1;
-#pragma unroll
-          for (int c = 0; c < CH; ++c) lb[c] = 0.0;
-#pragma unroll
-          for (int c = 0; c < LVA; ++c) lt[c] = 0.0;
-#pragma unroll
-          for (int b = 0; b < 3; ++b)
-            if (b == a) {
-              ly = ysl[b];
-#pragma unroll
-              for (int c = 0; c < CH; ++c) lb[c] = ab[b][c], ab[b][c] = 0.0;
-#pragma unroll
-              for (int c = 0; c < LVA; ++c) lt[c] = at[b][c], at[b][c] = 0.0;
-            }
+        // partial column of window slot A -> its Y slot (lanes = levels;
+        // top contributions shifted up one lane).  `doit`: the slot held a
+        // residency of this segment's strip.
+        auto flush = [&](auto A_, bool doit) {
+          constexpr int A = decltype(A_)::value;
+          const int ly = doit ? ysl[A] : -1;
 #pragma unroll
           for (int c = 0; c < CH; ++c) {
-            double v = lb[c];
-            if (c < LV) {
-              const double below = __shfl_up_sync(FULL, lt[c], 1, W);
+            double v = ab[A][c];
+            if (c < LV) { // every lane takes part in the shuffle
+              const double below = __shfl_up_sync(FULL, at[A][c], 1, W);
               if (sl > 0) v += below;
             }
             if (ly >= 0) {
               double *row = sY + ((size_t)ly * CH + c) * YS;
               if (lane_ok) row[sl] = v;
-              if (c < LV && sl == nl - 1) row[nl] = lt[c];
+              if (c < LV && sl == nl - 1) row[nl] = at[A][c];
             }
+          }
+          if (doit) { // the residency is closed: clear its accumulators
+#pragma unroll
+            for (int c = 0; c < CH; ++c) ab[A][c] = 0.0;
+#pragma unroll
+            for (int c = 0; c < LVA; ++c) at[A][c] = 0.0;
           }
         };
-        for (int k = 0; k < maxlen; ++k) {
+        // one strip step into the compile-time window slot A
+        auto step = [&](auto A_, int k) {
+          constexpr int A = decltype(A_)::value;
           const bool act = k < len;
-          const int2 rec = act ? sStep[k0 + k] : make_int2(3 << 16, -1);
+          flush(A_, act);
+          if (!act) return;
+          const int2 rec = sStep[k0 + k];
           const int v = rec.x & 0xffff;
-          const int slot = (rec.x >> 16) & 0xff;
-          const int flg = (rec.x >> 24) & 0xff;
-          const int ynew = rec.y;
-          // the leaving vertex's partial column goes to its Y slot
-          flush(slot); // shuffles run on every lane; stores predicated
+          ysl[A] = rec.y;
+          const double *f = sF + v * FS + sl * CH;
+          const double *cc = sC + v * CS + 3 * sl;
+#pragma unroll
+          for (int c = 0; c < CH; ++c) fb[A][c] = lane_ok ? f[c] : 0.0;
+#pragma unroll
+          for (int c = 0; c < LV; ++c) ft[A][c] = lane_ok ? f[CH + c] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            cb[A][q] = lane_ok ? cc[q] : 0.0;
+            ct[A][q] = lane_ok ? cc[3 + q] : 0.0;
+          }
+          if (k < 2) return; // window not full yet
+          // the cell-layer in window order (symmetric element)
+          double X[6], Y[6], Z[6];
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
-            if (slot == a) {
-              ysl[a] = ynew;
-#pragma unroll
-              for (int c = 0; c < CH; ++c)
-                fb[a][c] = lane_ok ? sF[v * FS + sl * CH + c] : 0.0;
-#pragma unroll
-              for (int c = 0; c < LV; ++c)
-                ft[a][c] = lane_ok ? sF[v * FS + (sl + 1) * CH + c] : 0.0;
-#pragma unroll
-              for (int q = 0; q < 3; ++q) {
-                cb[a][q] = lane_ok ? sC[v * CS + 3 * sl + q] : 0.0;
-                ct[a][q] = lane_ok ? sC[v * CS + 3 * (sl + 1) + q] : 0.0;
-              }
-            }
+            X[2 * a] = cb[a][0], Y[2 * a] = cb[a][1], Z[2 * a] = cb[a][2];
+            X[2 * a + 1] = ct[a][0], Y[2 * a + 1] = ct[a][1];
+            Z[2 * a + 1] = ct[a][2];
           }
-          if (flg & 1) {
-            // the cell-layer in window order (symmetric element: window
-            // slot a plays cell-local vertex a)
-            double X[6], Y[6], Z[6];
+          const double det = lane_ok ? prism_abs_detj(X, Y, Z) : 0.0;
+          double xv[K], yv[K];
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              X[2 * a] = cb[a][0], Y[2 * a] = cb[a][1], Z[2 * a] = cb[a][2];
-              X[2 * a + 1] = ct[a][0], Y[2 * a + 1] = ct[a][1];
-              Z[2 * a + 1] = ct[a][2];
-            }
-            const double det = lane_ok ? prism_abs_detj(X, Y, Z) : 0.0;
-            double xv[K], yv[K];
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-              const int a = T.pos[j];
-              xv[j] = T.level[j] == 2 ? ft[a][T.ch[j]] : fb[a][T.ch[j]];
-            }
-            kron_apply<LY>(M, xv, det, yv);
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-              const int a = T.pos[j];
-              if (T.level[j] == 2)
-                at[a][T.ch[j]] += yv[j];
-              else
-                ab[a][T.ch[j]] += yv[j];
-            }
+          for (int j = 0; j < K; ++j) {
+            const int a = T.pos[j];
+            xv[j] = T.level[j] == 2 ? ft[a][T.ch[j]] : fb[a][T.ch[j]];
           }
+          kron_apply<LY>(M, xv, det, yv);
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            const int a = T.pos[j];
+            if (T.level[j] == 2)
+              at[a][T.ch[j]] += yv[j];
+            else
+              ab[a][T.ch[j]] += yv[j];
+          }
+        };
+        using S0 = std::integral_constant<int, 0>;
+        using S1 = std::integral_constant<int, 1>;
+        using S2 = std::integral_constant<int, 2>;
+        // sequential strips: the replaced slot cycles 0, 1, 2, 0, ...
+        for (int k = 0; k < maxlen; k += 3) {
+          step(S0{}, k);
+          step(S1{}, k + 1);
+          step(S2{}, k + 2);
         }
         // strip end: the three remaining residencies
-#pragma unroll
-        for (int a = 0; a < 3; ++a) flush(has ? a : 3);
+        flush(S0{}, has);
+        flush(S1{}, has);
+        flush(S2{}, has);
       }
       __syncthreads();
 

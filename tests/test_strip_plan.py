@@ -36,7 +36,11 @@ def test_strip_plan_invariants(n, budget):
         ys = []
         for s in range(plan.strip_ptr[p], plan.strip_ptr[p + 1]):
             win = [None, None, None]
+            k0 = plan.step_ptr[s]
+            assert plan.step_ptr[s + 1] - k0 >= 3
             for k in range(plan.step_ptr[s], plan.step_ptr[s + 1]):
+                # sequential strips: the replaced slot cycles 0, 1, 2, ...
+                assert plan.step_slot[k] == (k - k0) % 3
                 win[plan.step_slot[k]] = int(ents[plan.step_v[k]])
                 if plan.step_y[k] >= 0:
                     ys.append(int(plan.step_y[k]))
