@@ -21,7 +21,9 @@ struct KronMat {
 
 // |det J| of the affine map reference prism -> physical prism cell-layer.
 // Vertex index v = 2a + b (a: triangle vertex, b: 0 bottom / 1 top level).
-// Same operation order as the oracle (oracle/prismesh_oracle.c).
+// Same operation order as the oracle (oracle/prismesh_oracle.c) except the
+// mean height is a multiplication by 1/3 instead of a division (no DDIV
+// sequence per cell-layer; differs from the oracle in the last bit only).
 __device__ __forceinline__ double prism_abs_detj(const double *X,
                                                  const double *Y,
                                                  const double *Z) {
@@ -29,7 +31,8 @@ __device__ __forceinline__ double prism_abs_detj(const double *X,
   const double xm1 = 0.5 * (X[2] + X[3]), ym1 = 0.5 * (Y[2] + Y[3]);
   const double xm2 = 0.5 * (X[4] + X[5]), ym2 = 0.5 * (Y[4] + Y[5]);
   const double a2 = (xm1 - xm0) * (ym2 - ym0) - (xm2 - xm0) * (ym1 - ym0);
-  const double h = ((Z[1] - Z[0]) + (Z[3] - Z[2]) + (Z[5] - Z[4])) / 3.0;
+  constexpr double kThird = 1.0 / 3.0;
+  const double h = ((Z[1] - Z[0]) + (Z[3] - Z[2]) + (Z[5] - Z[4])) * kThird;
   return fabs(a2 * h);
 }
 

@@ -202,14 +202,16 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
           ysl[A] = rec.y;
           const double *f = sF + v * FS + sl * CH;
           const double *cc = sC + v * CS + 3 * sl;
+          // lanes past the chunk read stale (finite or not) staged data:
+          // their results never reach an active lane or a store
 #pragma unroll
-          for (int c = 0; c < CH; ++c) fb[A][c] = lane_ok ? f[c] : 0.0;
+          for (int c = 0; c < CH; ++c) fb[A][c] = f[c];
 #pragma unroll
-          for (int c = 0; c < LV; ++c) ft[A][c] = lane_ok ? f[CH + c] : 0.0;
+          for (int c = 0; c < LV; ++c) ft[A][c] = f[CH + c];
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
-            cb[A][q] = lane_ok ? cc[q] : 0.0;
-            ct[A][q] = lane_ok ? cc[3 + q] : 0.0;
+            cb[A][q] = cc[q];
+            ct[A][q] = cc[3 + q];
           }
           if (k < 2) return; // window not full yet
           // the cell-layer in window order (symmetric element)
@@ -220,7 +222,7 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
             X[2 * a + 1] = ct[a][0], Y[2 * a + 1] = ct[a][1];
             Z[2 * a + 1] = ct[a][2];
           }
-          const double det = lane_ok ? prism_abs_detj(X, Y, Z) : 0.0;
+          const double det = prism_abs_detj(X, Y, Z);
           double xv[K], yv[K];
 #pragma unroll
           for (int j = 0; j < K; ++j) {
