@@ -81,6 +81,7 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
   int *sSPtr = reinterpret_cast<int *>(sStep + P.max_steps);   // strips+1
   int *sOPtr = sSPtr + P.max_strips + 1;                       // owned+1
   int *sOY = sOPtr + P.max_owned + 1;                          // y entries
+  int *sEnt = sOY + P.max_oy;                                  // local ents
   __shared__ int sCounter[1];
 
   const int lane = threadIdx.x & 31;
@@ -116,6 +117,9 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
     const int n_oy = __ldg(P.own_y_ptr + obase + n_own) - ob;
     for (int i = threadIdx.x; i < n_oy; i += blockDim.x)
       sOY[i] = __ldg(P.own_y + ob + i);
+    for (int i = threadIdx.x; i < n_loc; i += blockDim.x)
+      sEnt[i] = __ldg(P.ents + eb + i);
+    __syncthreads();
 
     for (int l0 = 0; l0 < layers; l0 += W) {
       const int nl = min(W, layers - l0);
@@ -125,11 +129,19 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
         // with cp.async so every copy of the chunk is in flight at once
         const int fl = nl * CH + LV, cl = 3 * (nl + 1);
         for (int v = warp; v < n_loc; v += n_warps) {
-          const int64_t g = __ldg(P.ents + eb + v);
+          const int64_t g = sEnt[v];
           const double *fx = x + g * P.column0 + (int64_t)l0 * CH;
           const double *fc = coords + g * cstride + 3 * (int64_t)l0;
-          for (int e = lane; e < fl; e += 32) cp_async8(sF + v * FS + e, fx + e);
-          for (int e = lane; e < cl; e += 32) cp_async8(sC + v * CS + e, fc + e);
+#pragma unroll
+          for (int r = 0; r < (FS + 31) / 32; ++r) {
+            const int e = lane + 32 * r;
+            if (e < fl) cp_async8(sF + v * FS + e, fx + e);
+          }
+#pragma unroll
+          for (int r = 0; r < (CS + 31) / 32; ++r) {
+            const int e = lane + 32 * r;
+            if (e < cl) cp_async8(sC + v * CS + e, fc + e);
+          }
         }
         cp_async_wait_all();
       }
@@ -268,7 +280,7 @@ k_strip(const KronMat M, const StripDev P, int64_t n_patches, int layers,
           if (sl < nl) v += row[sl];
           if (c < LV && sl == 0) top += row[nl];
         }
-        const int64_t origin = (int64_t)__ldg(P.ents + eb + i) * P.column0;
+        const int64_t origin = (int64_t)sEnt[i] * P.column0;
         if (c < LV) {
           if (sl == 0) {
             v += sCarry[i * LV + c];
@@ -301,7 +313,8 @@ static int strip_k(const LoopArgs &a, const StripDev &P, int64_t n_patches,
                         (size_t)P.max_y * CH * (W + 1) +
                         (size_t)P.max_owned * LVA) +
       sizeof(int2) * (size_t)P.max_steps +
-      sizeof(int) * ((size_t)P.max_strips + 1 + P.max_owned + 1 + P.max_oy);
+      sizeof(int) * ((size_t)P.max_strips + 1 + P.max_owned + 1 + P.max_oy +
+                     P.max_local);
   if (smem > 227 * 1024) {
     set_error("strip plan needs %zu bytes of shared memory", smem);
     return PM_EINVAL;

@@ -210,7 +210,8 @@ def strip_smem(max_local, max_y, max_owned, ch, lv, W, max_steps=0,
                max_strips=0, max_oy=0):
     return (8 * (max_local * (W * ch + lv + 3 * (W + 1)) +
                  max_y * ch * (W + 1) + max_owned * max(lv, 1)) +
-            8 * max_steps + 4 * (max_strips + 1 + max_owned + 1 + max_oy))
+            8 * max_steps + 4 * (max_strips + 1 + max_owned + 1 + max_oy +
+                                 max_local))
 
 
 def build_strip_plan(base, layout, layers, colors, n_colors,
