@@ -14,6 +14,8 @@
 // columns of a launch share a DoF -- with plain read-add-stores.
 #include "column_layout.cuh"
 
+#include <stdlib.h>
+
 namespace pm {
 
 template <int K> struct ColumnArgs {
@@ -173,8 +175,16 @@ static int column_k(const LoopArgs &a, bool colored) {
   for (int i = 0; i < LY::NH * LY::NH; ++i) A.M.t[i] = a.mtri[i];
   for (int i = 0; i < LY::NV * LY::NV; ++i) A.M.l[i] = a.mline[i];
   // segment width: smallest lane waste for this layer count
+  // (PM_COLUMN_W=8|16|32 overrides, a tuning knob)
   int W = 32;
-  {
+  static int forced = -1;
+  if (forced < 0) {
+    const char *e = getenv("PM_COLUMN_W");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 8 || forced == 16 || forced == 32) {
+    W = forced;
+  } else {
     double best = 1e30;
     for (int w : {32, 16, 8}) {
       const int chunks = (a.layers + w - 1) / w;
