@@ -22,6 +22,8 @@
  *                               replacing SPEC.md:343-364 colouring
  *   pm_column_mass_strip     <- same, strip-patch schedule (vertex layouts)
  *   pm_build_strips          <- host planner of that schedule
+ *   pm_column_mass_strip_red <- same, global strips + REDG
+ *   pm_build_global_strips   <- host planner of that schedule
  *   pm_column_probe          <- SPEC.md:338-340 counting / gather kernels
  *                               (verification.py:47-75 materialized maps)
  *   pm_halo_pack / _unpack   <- PAPER.md:770-775 (halo exchange between
@@ -54,7 +56,8 @@ enum {
   PM_VARIANT_COLUMN = 3,  /* warp segment per column, lanes = layers, REDG   */
   PM_VARIANT_COLORED = 4, /* COLUMN over one colour's cells, plain RMW      */
   PM_VARIANT_STREAM = 5,  /* DG (2,1) fields through TMA bulk copies        */
-  PM_VARIANT_STRIP = 6    /* strip-patch owner gather (pm_column_mass_strip) */
+  PM_VARIANT_STRIP = 6,   /* strip-patch owner gather (pm_column_mass_strip) */
+  PM_VARIANT_STRIPRED = 7 /* global strips + REDG (pm_column_mass_strip_red) */
 };
 
 const char *pm_last_error(void);
@@ -149,6 +152,18 @@ int pm_column_mass_strip(const int32_t *delta6, int32_t k, int32_t layers,
                          const int32_t *own_base, const int32_t *own_y_ptr,
                          const int32_t *own_y, void *stream);
 
+/* Global-strip schedule (PM_VARIANT_STRIPRED) for vertex-column layouts:
+ * sequential strips over the whole mesh (pm_build_global_strips), one
+ * register window per W-lane segment, one coalesced fp64 REDG per
+ * departing vertex.  accumulate = 0 zeroes y first. */
+int pm_column_mass_strip_red(const int32_t *delta6, int32_t k, int32_t layers,
+                             const double *coords, const double *mref,
+                             const double *mtri, const double *mline,
+                             const double *x, double *y, int64_t n_dofs,
+                             int32_t accumulate, int64_t n_strips,
+                             int32_t chunk, const int32_t *strip_ptr,
+                             const int32_t *steps, void *stream);
+
 /* --- probes for the par-loop itself (exact integer checks) -------------
  * mode 0: out_i64[(c*layers+l)*k + j] = cell_map[c*k+j] + l*offsets[j]
  *         (the materialised per-(cell,layer) lists)
@@ -194,6 +209,16 @@ int pm_build_strips(int64_t n_patches, const int32_t *cell_ptr,
                     uint16_t *step_v, uint8_t *step_slot, uint8_t *step_flags,
                     int32_t *step_y, int32_t *patch_y_count,
                     int32_t *own_y_ptr, int32_t *own_y, int64_t *totals);
+
+/* --- host setup: global sequential strips -------------------------------
+ * strip_ptr[n_strips+1] into steps (3 fill vertices, then one new vertex per
+ * cell); capacities: strips <= n_cells, steps <= 3*n_cells.  totals =
+ * {strips, steps}. */
+int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
+                           const int32_t *cell_vertices,
+                           const int32_t *cell_edges, int32_t max_len,
+                           int32_t *strip_ptr, int32_t *steps,
+                           int64_t *totals);
 
 /* Device properties used to size grids (SM count, L2 bytes). */
 int pm_device_info(int32_t *sm_count, int64_t *l2_bytes);

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "_native", "libprismesh_cuda.so")
 PM_OK, PM_EINVAL, PM_ECUDA, PM_EOVERFLOW = 0, 1, 2, 3
 SHARE_NONE, SHARE_VERTICAL, SHARE_HORIZONTAL = 0, 1, 2
 (VARIANT_AUTO, VARIANT_ATOMIC, VARIANT_PATCH, VARIANT_COLUMN, VARIANT_COLORED,
- VARIANT_STREAM, VARIANT_STRIP) = range(7)
+ VARIANT_STREAM, VARIANT_STRIP, VARIANT_STRIPRED) = range(8)
 
 _lib = None
 
@@ -62,6 +62,14 @@ SIGNATURES = {
                             [_vp] * 14),
     "pm_build_strips": (ctypes.c_int, [_i64] + [_vp] * 6 + [_i32] +
                         [_vp] * 10),
+    "pm_column_mass_strip_red": (ctypes.c_int, [_i32p, _i32, _i32, _vp,
+                                                ctypes.POINTER(_f64),
+                                                ctypes.POINTER(_f64),
+                                                ctypes.POINTER(_f64), _vp,
+                                                _vp, _i64, _i32, _i64, _i32,
+                                                _vp, _vp, _vp]),
+    "pm_build_global_strips": (ctypes.c_int, [_i64, _i64, _vp, _vp, _i32,
+                                              _vp, _vp, _vp]),
     "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
                                        _vp, _vp]),
     "pm_halo_pack": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
@@ -268,6 +276,36 @@ def column_mass_strip(layout, k, layers, coords, mref, x, y, plan, dplan,
         ptr(dplan["step_flags"]), ptr(dplan["step_y"]),
         ptr(dplan["y_count"]), ptr(dplan["own_base"]),
         ptr(dplan["own_y_ptr"]), ptr(dplan["own_y"]), stream_ptr(stream))
+    check(rc)
+
+
+def build_global_strips(base, max_len=64):
+    """(strip_ptr int32, steps int32) over the whole mesh (host C++)."""
+    cv = np.ascontiguousarray(base.cell_vertices, dtype=np.int32)
+    ce = np.ascontiguousarray(base.cell_edges, dtype=np.int32)
+    n = cv.shape[0]
+    sp = np.zeros(n + 1, dtype=np.int32)
+    st = np.zeros(3 * n + 3, dtype=np.int32)
+    tot = np.zeros(2, dtype=np.int64)
+    check(host_lib().pm_build_global_strips(
+        n, base.num_edges, cv.ctypes.data_as(_i32p), ce.ctypes.data_as(_i32p),
+        max_len, sp.ctypes.data_as(_i32p), st.ctypes.data_as(_i32p),
+        tot.ctypes.data_as(_i64p)))
+    return sp[:tot[0] + 1].copy(), st[:tot[1]].copy()
+
+
+def column_mass_strip_red(layout, k, layers, coords, mref, x, y, n_dofs,
+                          strips, kron, chunk, accumulate=False, stream=None):
+    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
+    ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
+    d = layout.delta6()
+    sp, st = strips
+    rc = host_lib().pm_column_mass_strip_red(
+        d.ctypes.data_as(_i32p), k, layers, ptr(coords), _f64ptr(m),
+        _f64ptr(mt), _f64ptr(ml), ptr(x), ptr(y), n_dofs,
+        1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp), ptr(st),
+        stream_ptr(stream))
     check(rc)
 
 

@@ -312,3 +312,99 @@ extern "C" int pm_build_strips(
   totals[2] = n_oy;
   return PM_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Global sequential strips for the strip-REDG schedule (csrc/strip_red.cu):
+// like pm_build_strips but over the whole mesh, starting each strip at the
+// first unused cell in index order (RCM order keeps concurrent strips
+// local), steps = global vertex ids (3 fills, then one per cell).
+// ---------------------------------------------------------------------------
+extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
+                                      const int32_t *cell_vertices,
+                                      const int32_t *cell_edges,
+                                      int32_t max_len, int32_t *strip_ptr,
+                                      int32_t *steps, int64_t *totals) {
+  pm::clear_error();
+  if (n_cells < 0 || n_edges < 0 || max_len < 1) {
+    pm::set_error("pm_build_global_strips: bad arguments");
+    return PM_EINVAL;
+  }
+  std::vector<int32_t> ec(2 * (size_t)n_edges, -1);
+  for (int64_t c = 0; c < n_cells; ++c)
+    for (int k = 0; k < 3; ++k) {
+      const int64_t e = cell_edges[3 * c + k];
+      if (ec[2 * e] < 0)
+        ec[2 * e] = (int32_t)c;
+      else
+        ec[2 * e + 1] = (int32_t)c;
+    }
+  std::vector<uint8_t> used(n_cells, 0);
+  auto vid = [&](int64_t c, int k) { return cell_vertices[3 * c + k]; };
+  auto across = [&](int64_t c, int32_t u, int32_t w) -> int64_t {
+    for (int k = 0; k < 3; ++k) {
+      const int32_t a = vid(c, (k + 1) % 3), b = vid(c, (k + 2) % 3);
+      if ((a == u && b == w) || (a == w && b == u)) {
+        const int64_t e = cell_edges[3 * c + k];
+        const int32_t o = ec[2 * e] == c ? ec[2 * e + 1] : ec[2 * e];
+        return o;
+      }
+    }
+    return -1;
+  };
+  auto third = [&](int64_t c, int32_t u, int32_t w) -> int32_t {
+    for (int q = 0; q < 3; ++q)
+      if (vid(c, q) != u && vid(c, q) != w) return vid(c, q);
+    return -1;
+  };
+  int64_t n_strips = 0, n_steps = 0, scan = 0;
+  strip_ptr[0] = 0;
+  while (true) {
+    while (scan < n_cells && used[scan]) ++scan;
+    if (scan >= n_cells) break;
+    int64_t cur = scan;
+    used[cur] = 1;
+    int32_t win[3] = {vid(cur, 0), vid(cur, 1), vid(cur, 2)};
+    int64_t next = -1;
+    int best = -1;
+    for (int e = 0; e < 3; ++e) {
+      const int32_t a0 = vid(cur, e), a1 = vid(cur, (e + 1) % 3),
+                    a2 = vid(cur, (e + 2) % 3);
+      const int64_t j = across(cur, a1, a2);
+      if (j < 0 || used[j]) continue;
+      for (int dir = 0; dir < 2; ++dir) {
+        const int32_t u = dir ? a2 : a1, w = dir ? a1 : a2;
+        const int32_t nv = third(j, u, w);
+        const int64_t j2 = across(j, w, nv);
+        // prefer a continuation; then the lower-index neighbour
+        const int score = (j2 >= 0 && !used[j2] && j2 != cur) ? 2 : 1;
+        if (score > best) {
+          best = score;
+          next = j;
+          win[0] = a0, win[1] = u, win[2] = w;
+        }
+      }
+    }
+    for (int k = 0; k < 3; ++k) steps[n_steps++] = win[k];
+    int32_t len = 1, slot = 0;
+    while (next >= 0 && len < max_len) {
+      const int32_t nv = third(next, win[(slot + 1) % 3], win[(slot + 2) % 3]);
+      if (nv < 0) {
+        pm::set_error("pm_build_global_strips: broken strip");
+        return PM_EINVAL;
+      }
+      used[next] = 1;
+      win[slot] = nv;
+      steps[n_steps++] = nv;
+      cur = next;
+      slot = (slot + 1) % 3;
+      ++len;
+      const int64_t j = across(cur, win[(slot + 1) % 3], win[(slot + 2) % 3]);
+      next = (j >= 0 && !used[j]) ? j : -1;
+    }
+    ++n_strips;
+    strip_ptr[n_strips] = (int32_t)n_steps;
+  }
+  totals[0] = n_strips;
+  totals[1] = n_steps;
+  return PM_OK;
+}

@@ -1,0 +1,264 @@
+// Global-strip schedule for vertex-column CG layouts (PM_VARIANT_STRIPRED):
+// P1, 3-vector P1, CG1 x DG0, CG1 x DG1.
+//
+// The base cells are walked as sequential strips (consecutive cells share
+// the edge of the two youngest window vertices, schedule.build_global_
+// strips), so every step brings exactly one new vertex into a 3-vertex
+// register window and the replaced window slot cycles 0,1,2 (compile-time
+// after a 3-way unroll).  A W-lane segment owns a strip, lane = layer of the
+// current W-layer chunk:
+//   * the new vertex's field and (x,y,z) at the lane's level are loaded
+//     straight from global memory, prefetched one step ahead (the strip's
+//     vertex ids are fetched W at a time and handed out by shfl);
+//   * the level above comes from the next lane (shfl.down);
+//   * the cell-layer contribution (sum-factorised Mtri (x) Mline) goes into
+//     per-window-vertex accumulators in registers;
+//   * when a vertex leaves the window its partial column is added to y with
+//     one coalesced fp64 REDG per channel (top contributions shifted one
+//     lane up; the chunk's top level by the last lane).
+// One vertex load and one partial flush per cell instead of three gathers
+// and three scatters per cell-layer.  Needs y zeroed first (overwrite mode).
+#include "column_layout.cuh"
+
+#include <type_traits>
+
+namespace pm {
+
+template <class LY, int W, int K = LY::K>
+__global__ void __launch_bounds__(256)
+k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
+            const int32_t *__restrict__ steps, int64_t n_strips, int layers,
+            const double *__restrict__ coords, const double *__restrict__ x,
+            double *__restrict__ y) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int SEGS = 32 / W;
+  constexpr typename LY::Tab T = LY::make();
+  constexpr int LV = LY::LV0;
+  constexpr int CH = LY::CH0;
+  constexpr int LVA = LV > 0 ? LV : 1;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % W, seg = lane / W;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t col = (int64_t)layers * CH + LV; // vertex column length
+  const int64_t ccol = 3 * (int64_t)(layers + 1);
+
+  for (int64_t s0 = warp * SEGS; s0 < n_strips; s0 += n_warps * SEGS) {
+    const int64_t si = s0 + seg;
+    const bool has = si < n_strips;
+    const int k0 = has ? __ldg(strip_ptr + si) : 0;
+    const int len = has ? __ldg(strip_ptr + si + 1) - k0 : 0;
+    int maxlen = len;
+#pragma unroll
+    for (int o = W; o < 32; o <<= 1)
+      maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
+
+    for (int l0 = 0; l0 < layers; l0 += W) {
+      const int nl = min(W, layers - l0);
+      const int l = l0 + sl;
+      const bool lane_ok = sl < nl;
+      double fb[3][CH], ft[3][LVA], cb[3][3], ct[3][3];
+      double ab[3][CH], at[3][LVA];
+      int64_t vo[3] = {0, 0, 0}; // field column origin of the window slot
+      bool live[3] = {false, false, false};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) fb[a][c] = 0.0, ab[a][c] = 0.0;
+#pragma unroll
+        for (int c = 0; c < LVA; ++c) ft[a][c] = 0.0, at[a][c] = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) cb[a][q] = 0.0, ct[a][q] = 0.0;
+      }
+      // vertex ids of the strip, W at a time (lane sl holds step base+sl)
+      int vbuf = (has && sl < len) ? __ldg(steps + k0 + sl) : 0;
+      int vbase = 0;
+      // prefetched lane-level values of the next vertex
+      double nf[CH], nc[3];
+      auto fetch = [&](int k, double *f, double *c3) {
+        // vertex of step k: from the id buffer (refilled every W steps)
+        if (k - vbase >= W) { // warp-uniform (vbase is per segment but all
+                              // segments advance in lockstep)
+          vbase += W;
+          vbuf = (has && vbase + sl < len) ? __ldg(steps + k0 + vbase + sl)
+                                           : 0;
+        }
+        const int v = __shfl_sync(FULL, vbuf, (k - vbase) & (W - 1), W);
+        const bool ok = k < len && lane_ok;
+        const double *fp = x + (int64_t)v * col + (int64_t)l * CH;
+        const double *cp = coords + (int64_t)v * ccol + 3 * (int64_t)l;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) f[q] = ok ? __ldg(fp + q) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) c3[q] = ok ? __ldg(cp + q) : 0.0;
+        return v;
+      };
+      int vnext = fetch(0, nf, nc);
+
+      auto flush = [&](auto A_) {
+        constexpr int A = decltype(A_)::value;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          double v = ab[A][c];
+          if (c < LV) {
+            const double below = __shfl_up_sync(FULL, at[A][c], 1, W);
+            if (sl > 0) v += below;
+          }
+          if (live[A] && lane_ok) {
+            double *yp = y + vo[A] + (int64_t)l * CH + c;
+            atomicAdd(yp, v);
+            if (c < LV && sl == nl - 1) atomicAdd(yp + CH, at[A][c]);
+          }
+          ab[A][c] = 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < LVA; ++c) at[A][c] = 0.0;
+      };
+
+      auto step = [&](auto A_, int k) {
+        constexpr int A = decltype(A_)::value;
+        flush(A_);
+        const bool act = k < len;
+        // the prefetched vertex enters slot A
+        const int64_t vcol = (int64_t)vnext;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) fb[A][c] = nf[c];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) cb[A][q] = nc[q];
+        // level above: next lane (same vertex column), last lane loads
+#pragma unroll
+        for (int c = 0; c < LV; ++c) {
+          const double up = __shfl_down_sync(FULL, nf[c], 1, W);
+          ft[A][c] = (sl == nl - 1 && act)
+                         ? __ldg(x + vcol * col + (int64_t)(l + 1) * CH + c)
+                         : up;
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double up = __shfl_down_sync(FULL, nc[q], 1, W);
+          ct[A][q] = (sl == nl - 1 && act)
+                         ? __ldg(coords + vcol * ccol + 3 * (int64_t)(l + 1) + q)
+                         : up;
+        }
+        vo[A] = vcol * col;
+        live[A] = act;
+        // prefetch the next step's vertex while this cell computes
+        vnext = fetch(k + 1, nf, nc);
+        if (k < 2) return; // window not full yet
+        double X[6], Y[6], Z[6];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          X[2 * a] = cb[a][0], Y[2 * a] = cb[a][1], Z[2 * a] = cb[a][2];
+          X[2 * a + 1] = ct[a][0], Y[2 * a + 1] = ct[a][1];
+          Z[2 * a + 1] = ct[a][2];
+        }
+        const double det = (act && lane_ok) ? prism_abs_detj(X, Y, Z) : 0.0;
+        double xv[K], yv[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int a = T.pos[j];
+          xv[j] = T.level[j] == 2 ? ft[a][T.ch[j]] : fb[a][T.ch[j]];
+        }
+        kron_apply<LY>(M, xv, det, yv);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int a = T.pos[j];
+          if (T.level[j] == 2)
+            at[a][T.ch[j]] += yv[j];
+          else
+            ab[a][T.ch[j]] += yv[j];
+        }
+      };
+      using S0 = std::integral_constant<int, 0>;
+      using S1 = std::integral_constant<int, 1>;
+      using S2 = std::integral_constant<int, 2>;
+      for (int k = 0; k < maxlen; k += 3) {
+        step(S0{}, k);
+        step(S1{}, k + 1);
+        step(S2{}, k + 2);
+      }
+      flush(S0{});
+      flush(S1{});
+      flush(S2{});
+    }
+  }
+}
+
+template <class LY>
+static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
+                       const int32_t *steps, int64_t n_strips, int W) {
+  if (!a.mtri || !a.mline) {
+    set_error("the strip kernel needs the Kronecker factors mtri/mline");
+    return PM_EINVAL;
+  }
+  KronMat M;
+  for (int i = 0; i < LY::NH * LY::NH; ++i) M.t[i] = a.mtri[i];
+  for (int i = 0; i < LY::NV * LY::NV; ++i) M.l[i] = a.mline[i];
+  const int segs = 32 / W;
+  const int64_t warps = (n_strips + segs - 1) / segs;
+  const unsigned grid = grid_for(warps * 32, 256, 8);
+#define PM_SR(WW)                                                            \
+  k_strip_red<LY, WW><<<grid, 256, 0, a.s>>>(M, strip_ptr, steps, n_strips,  \
+                                             a.layers, a.coords, a.x, a.y)
+  if (W == 32)
+    PM_SR(32);
+  else if (W == 16)
+    PM_SR(16);
+  else if (W == 8)
+    PM_SR(8);
+  else {
+    set_error("strip chunk width must be 8, 16 or 32 (got %d)", W);
+    return PM_EINVAL;
+  }
+#undef PM_SR
+  PM_LAUNCH_CHECK("k_strip_red");
+  return PM_OK;
+}
+
+#define PM_STRIPRED_LAYOUTS(X)                                               \
+  X(1, 0, 0, 0, 0, 0)                                                        \
+  X(0, 1, 0, 0, 0, 0)                                                        \
+  X(0, 2, 0, 0, 0, 0)                                                        \
+  X(3, 0, 0, 0, 0, 0)
+
+} // namespace pm
+
+extern "C" int pm_column_mass_strip_red(
+    const int32_t *delta6, int32_t k, int32_t layers, const double *coords,
+    const double *mref, const double *mtri, const double *mline,
+    const double *x, double *y, int64_t n_dofs, int32_t accumulate,
+    int64_t n_strips, int32_t chunk, const int32_t *strip_ptr,
+    const int32_t *steps, void *stream) {
+  pm::clear_error();
+  pm::LoopArgs a;
+  int rc = pm::make_slot_table(delta6, &a.st);
+  if (rc) return rc;
+  if (k != a.st.k || layers < 1 || n_strips < 0 || !mref || n_dofs < 0) {
+    pm::set_error("bad arguments to pm_column_mass_strip_red");
+    return PM_EINVAL;
+  }
+  a.k = k;
+  a.layers = layers;
+  a.coords = coords;
+  a.mref = mref;
+  a.mtri = mtri;
+  a.mline = mline;
+  a.x = x;
+  a.y = y;
+  a.s = (cudaStream_t)stream;
+  if (!accumulate && n_dofs > 0)
+    PM_CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)n_dofs * sizeof(double), a.s));
+  if (n_strips == 0) return PM_OK;
+  if (!coords || !x || !y || !strip_ptr || !steps) {
+    pm::set_error("NULL device pointer");
+    return PM_EINVAL;
+  }
+#define PM_DISPATCH(a_, b_, c_, e_, f_, g_)                                  \
+  if (pm::Layout<a_, b_, c_, e_, f_, g_>::matches(delta6))                   \
+    return pm::strip_red_k<pm::Layout<a_, b_, c_, e_, f_, g_>>(              \
+        a, strip_ptr, steps, n_strips, chunk);
+  PM_STRIPRED_LAYOUTS(PM_DISPATCH)
+#undef PM_DISPATCH
+  pm::set_error("layout not supported by the strip schedule");
+  return PM_EINVAL;
+}

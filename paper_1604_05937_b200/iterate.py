@@ -20,6 +20,8 @@ Schedules (``schedule=``):
                 ``"column"``.
 ``"patch"``     owner-computes over compact patches, shared-memory
                 accumulation, no atomics, deterministic (schedule.py).
+``"stripred"``  vertex-column layouts: global sequential strips, one
+                vertex load and one fp64 REDG flush per cell.
 ``"strip"``     vertex-column layouts: patches staged in shared memory,
                 cells walked as strips (one new vertex per cell), owner
                 gather of per-residency partials; deterministic.
@@ -41,7 +43,7 @@ import numpy as np
 from . import _lib
 
 SCHEDULES = ("auto", "atomic", "colored", "sequential", "column", "stream",
-             "patch", "strip")
+             "patch", "strip", "stripred")
 
 
 @dataclass(frozen=True)

@@ -120,6 +120,7 @@ class MassOperator:
         self._coloring = None
         self._patch = None
         self._strip = None
+        self._gstrips = None
         self._dev = _lib.cuda_device()
         self.cmap = fs.device_cell_map()
         self.offs = fs.device_offsets()
@@ -154,6 +155,17 @@ class MassOperator:
     def strip_ok(self) -> bool:
         d = tuple(self.fs.layout.delta6())
         return d in _STRIP_LAYOUTS
+
+    def _global_strips(self):
+        if self._gstrips is None:
+            import torch
+            sp, st = _lib.build_global_strips(self.fs.mesh.base, max_len=64)
+            L = self.layers
+            W = min((8, 16, 32), key=lambda w: (-(-L // w) * w / L
+                                                 + 0.05 * (-(-L // w)), -w))
+            self._gstrips = ((torch.from_numpy(sp).to(self._dev),
+                              torch.from_numpy(st).to(self._dev)), W)
+        return self._gstrips
 
     def _strip_plan(self):
         if self._strip is None:
@@ -201,6 +213,17 @@ class MassOperator:
             sched = "atomic"   # dense Mref in the generic kernel
         if sched == "auto" and self.share == 2 and self.patch_ok:
             sched = "patch"
+        if sched == "stripred":
+            if not self.strip_ok:
+                raise ValueError(
+                    f"the strip schedule needs a vertex-column layout, got "
+                    f"{self.fs.layout.name}")
+            strips, W = self._global_strips()
+            _lib.column_mass_strip_red(self.fs.layout, self.k, self.layers,
+                                       coords, self.mref, x, y, n, strips,
+                                       self.kron, W, accumulate=accumulate,
+                                       stream=stream)
+            return y
         if sched == "strip":
             if not self.strip_ok:
                 raise ValueError(

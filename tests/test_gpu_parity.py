@@ -126,13 +126,14 @@ def test_arity_and_mesh_mismatch_rejected(gmesh):
         iterate_columns([fs, xfs2], k, [None, None, None])
 
 
-SCHEDULES = ("auto", "atomic", "colored", "column", "patch", "strip")
+SCHEDULES = ("auto", "atomic", "colored", "column", "patch", "strip",
+             "stripred")
 
 
 def _schedule_applies(lname, schedule):
     if schedule == "patch":
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "P2xP2", "VP1")
-    if schedule == "strip":
+    if schedule in ("strip", "stripred"):
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1")
     return True
 
@@ -381,3 +382,22 @@ def test_strip_chunk_widths(lname, W, layers):
     y = op.apply(torch.from_numpy(x).cuda(), coords).cpu().numpy()
     ref = _oracle_for(w, fs).assemble(x)
     assert _rel(y, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1", "CG1xDG1", "CG1xDG0"))
+@pytest.mark.parametrize("layers", (1, 5, 16, 33, 64))
+def test_stripred_layers(lname, layers):
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator
+    w = configs.Workload("srl", 14, layers, lname, quad_degrees(lname),
+                         ordering="random", jitter=0.2)
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    op = MassOperator(fs, quad, schedule="stripred")
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    xd = torch.from_numpy(x).cuda()
+    y = op.apply(xd, coords).cpu().numpy()
+    ref = _oracle_for(w, fs).assemble(x)
+    assert _rel(y, ref) <= 1e-10
+    y2 = op.apply(xd, coords, torch.from_numpy(y).cuda(), accumulate=True)
+    assert _rel(y2.cpu().numpy(), 2 * ref) <= 1e-10

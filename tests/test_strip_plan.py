@@ -124,3 +124,24 @@ def test_strip_emulation_matches_oracle(lname, ordering):
     ref = oracle.Problem(base, layers, LAYOUT_COUNTS[lname], tri, line, nc,
                          *quad_degrees(lname)).assemble(x)
     np.testing.assert_allclose(y, ref, rtol=0, atol=1e-14 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("n,ordering,max_len", ((6, "rcm", 64), (12, "random", 7),
+                                                (20, "rcm", 5)))
+def test_global_strips_invariants(n, ordering, max_len):
+    from paper_1604_05937_b200 import _lib
+    from paper_1604_05937_b200.configs import base_mesh
+    base, _ = base_mesh(n, ordering, 0.2)
+    sp, st = _lib.build_global_strips(base, max_len)
+    cv = np.sort(base.cell_vertices, axis=1)
+    key = {tuple(r): i for i, r in enumerate(cv.tolist())}
+    seen = []
+    for s in range(len(sp) - 1):
+        steps = st[sp[s]:sp[s + 1]].tolist()
+        assert 3 <= len(steps) <= max_len + 2
+        win = steps[:3]
+        seen.append(key[tuple(sorted(win))])
+        for k, v in enumerate(steps[3:]):
+            win[k % 3] = v            # the oldest slot is replaced
+            seen.append(key[tuple(sorted(win))])
+    assert sorted(seen) == list(range(base.num_cells))
