@@ -43,18 +43,23 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
   const int64_t col = (int64_t)layers * CH + LV; // vertex column length
   const int64_t ccol = 3 * (int64_t)(layers + 1);
 
-  for (int64_t s0 = warp * SEGS; s0 < n_strips; s0 += n_warps * SEGS) {
-    const int64_t si = s0 + seg;
-    const bool has = si < n_strips;
+  // work item = (strip, layer chunk), chunk-major so that neighbouring
+  // strips (sharing vertex columns) run at the same time
+  const int n_chunks = (layers + W - 1) / W;
+  const int64_t n_items = n_strips * n_chunks;
+  for (int64_t i0 = warp * SEGS; i0 < n_items; i0 += n_warps * SEGS) {
+    const int64_t item = i0 + seg;
+    const bool has = item < n_items;
+    const int64_t si = has ? item % n_strips : 0;
+    const int l0 = has ? (int)(item / n_strips) * W : 0;
     const int k0 = has ? __ldg(strip_ptr + si) : 0;
     const int len = has ? __ldg(strip_ptr + si + 1) - k0 : 0;
     int maxlen = len;
 #pragma unroll
     for (int o = W; o < 32; o <<= 1)
       maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
-
-    for (int l0 = 0; l0 < layers; l0 += W) {
-      const int nl = min(W, layers - l0);
+    {
+      const int nl = has ? min(W, layers - l0) : 0;
       const int l = l0 + sl;
       const bool lane_ok = sl < nl;
       double fb[3][CH], ft[3][LVA], cb[3][3], ct[3][3];
@@ -195,7 +200,8 @@ static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
   for (int i = 0; i < LY::NH * LY::NH; ++i) M.t[i] = a.mtri[i];
   for (int i = 0; i < LY::NV * LY::NV; ++i) M.l[i] = a.mline[i];
   const int segs = 32 / W;
-  const int64_t warps = (n_strips + segs - 1) / segs;
+  const int64_t items = n_strips * ((a.layers + W - 1) / W);
+  const int64_t warps = (items + segs - 1) / segs;
   const unsigned grid = grid_for(warps * 32, 256, 8);
 #define PM_SR(WW)                                                            \
   k_strip_red<LY, WW><<<grid, 256, 0, a.s>>>(M, strip_ptr, steps, n_strips,  \

@@ -159,7 +159,7 @@ class MassOperator:
     def _global_strips(self):
         if self._gstrips is None:
             import torch
-            sp, st = _lib.build_global_strips(self.fs.mesh.base, max_len=64)
+            sp, st = _lib.build_global_strips(self.fs.mesh.base, max_len=32)
             L = self.layers
             W = min((8, 16, 32), key=lambda w: (-(-L // w) * w / L
                                                  + 0.05 * (-(-L // w)), -w))
