@@ -291,7 +291,18 @@ def build_global_strips(base, max_len=64):
         n, base.num_edges, cv.ctypes.data_as(_i32p), ce.ctypes.data_as(_i32p),
         max_len, sp.ctypes.data_as(_i32p), st.ctypes.data_as(_i32p),
         tot.ctypes.data_as(_i64p)))
-    return sp[:tot[0] + 1].copy(), st[:tot[1]].copy()
+    sp, st = sp[:tot[0] + 1].copy(), st[:tot[1]].copy()
+    # order strips by their mean vertex id: strips running concurrently on
+    # the GPU then share vertex columns (L2 reuse)
+    lens = np.diff(sp)
+    sums = np.add.reduceat(st.astype(np.int64), sp[:-1]) if lens.size else \
+        np.zeros(0)
+    order = np.argsort(sums / np.maximum(lens, 1), kind="stable")
+    new_sp = np.zeros_like(sp)
+    np.cumsum(lens[order], out=new_sp[1:])
+    idx = np.concatenate([np.arange(sp[i], sp[i + 1]) for i in order]) \
+        if order.size else np.zeros(0, dtype=np.int64)
+    return new_sp, st[idx].astype(np.int32)
 
 
 def column_mass_strip_red(layout, k, layers, coords, mref, x, y, n_dofs,
