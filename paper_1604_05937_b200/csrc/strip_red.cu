@@ -78,12 +78,12 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       // vertex ids of the strip, W at a time (lane sl holds step base+sl)
       int vbuf = (has && sl < len) ? __ldg(steps + k0 + sl) : 0;
       int vbase = 0;
-      // prefetch ring, three steps deep: slot r holds the lane-level field
-      // and coordinates of the vertex of the next step k with k % 3 == r
-      double rf[3][CH], rc[3][3];
-      int rv[3];
+      // prefetched lane-level values of the next vertex
+      double nf[CH], nc[3];
       auto fetch = [&](int k, double *f, double *c3) {
-        if (k - vbase >= W) { // all segments advance in lockstep
+        // vertex of step k: from the id buffer (refilled every W steps)
+        if (k - vbase >= W) { // warp-uniform (vbase is per segment but all
+                              // segments advance in lockstep)
           vbase += W;
           vbuf = (has && vbase + sl < len) ? __ldg(steps + k0 + vbase + sl)
                                            : 0;
@@ -98,9 +98,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         for (int q = 0; q < 3; ++q) c3[q] = ok ? __ldg(cp + q) : 0.0;
         return v;
       };
-      rv[0] = fetch(0, rf[0], rc[0]);
-      rv[1] = fetch(1, rf[1], rc[1]);
-      rv[2] = fetch(2, rf[2], rc[2]);
+      int vnext = fetch(0, nf, nc);
 
       auto flush = [&](auto A_) {
         constexpr int A = decltype(A_)::value;
@@ -126,31 +124,31 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         constexpr int A = decltype(A_)::value;
         flush(A_);
         const bool act = k < len;
-        // the prefetched vertex (ring slot A) enters window slot A
-        const int64_t vcol = (int64_t)rv[A];
+        // the prefetched vertex enters slot A
+        const int64_t vcol = (int64_t)vnext;
 #pragma unroll
-        for (int c = 0; c < CH; ++c) fb[A][c] = rf[A][c];
+        for (int c = 0; c < CH; ++c) fb[A][c] = nf[c];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) cb[A][q] = rc[A][q];
+        for (int q = 0; q < 3; ++q) cb[A][q] = nc[q];
         // level above: next lane (same vertex column), last lane loads
 #pragma unroll
         for (int c = 0; c < LV; ++c) {
-          const double up = __shfl_down_sync(FULL, rf[A][c], 1, W);
+          const double up = __shfl_down_sync(FULL, nf[c], 1, W);
           ft[A][c] = (sl == nl - 1 && act)
                          ? __ldg(x + vcol * col + (int64_t)(l + 1) * CH + c)
                          : up;
         }
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-          const double up = __shfl_down_sync(FULL, rc[A][q], 1, W);
+          const double up = __shfl_down_sync(FULL, nc[q], 1, W);
           ct[A][q] = (sl == nl - 1 && act)
                          ? __ldg(coords + vcol * ccol + 3 * (int64_t)(l + 1) + q)
                          : up;
         }
         vo[A] = vcol * col;
         live[A] = act;
-        // refill ring slot A with the vertex three steps ahead
-        rv[A] = fetch(k + 3, rf[A], rc[A]);
+        // prefetch the next step's vertex while this cell computes
+        vnext = fetch(k + 1, nf, nc);
         if (k < 2) return; // window not full yet
         double X[6], Y[6], Z[6];
 #pragma unroll
