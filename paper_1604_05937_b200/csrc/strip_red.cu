@@ -24,8 +24,30 @@
 
 namespace pm {
 
+__device__ __forceinline__ void sr_cp8(double *dst, const double *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void sr_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N> __device__ __forceinline__ void sr_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// values per ring row: field (CH) + coordinates (3)
+template <class LY> constexpr int sr_row() { return LY::CH0 + 3; }
+constexpr int kSrDepth = 3; // steps in flight per segment
+
+// 3-vector windows need more registers: one CTA per SM there
+template <class LY> constexpr int sr_min_blocks() {
+  return LY::CH0 > 2 ? 1 : 2;
+}
+
 template <class LY, int W, int K = LY::K>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, sr_min_blocks<LY>())
 k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
             const int32_t *__restrict__ steps, int64_t n_strips, int layers,
             const double *__restrict__ coords, const double *__restrict__ x,
@@ -78,27 +100,46 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       // vertex ids of the strip, W at a time (lane sl holds step base+sl)
       int vbuf = (has && sl < len) ? __ldg(steps + k0 + sl) : 0;
       int vbase = 0;
-      // prefetched lane-level values of the next vertex
-      double nf[CH], nc[3];
-      auto fetch = [&](int k, double *f, double *c3) {
-        // vertex of step k: from the id buffer (refilled every W steps)
-        if (k - vbase >= W) { // warp-uniform (vbase is per segment but all
-                              // segments advance in lockstep)
+      // per-warp shared-memory prefetch ring, kSrDepth steps deep: lane sl
+      // copies (cp.async) the field + coordinates of its own level into row
+      // sl; the chunk's last lane also copies the level above into row W.
+      // Every lane reads only what it copied itself.
+      constexpr int RW = sr_row<LY>();
+      extern __shared__ double sr_ring[];
+      double *ring = sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS *
+                                   (W + 1) * RW;
+      auto row = [&](int slot, int r) {
+        return ring + ((size_t)(slot * SEGS + seg) * (W + 1) + r) * RW;
+      };
+      int rv[kSrDepth];
+      auto fetch = [&](int k, int slot) {
+        if (k - vbase >= W) { // all segments advance in lockstep
           vbase += W;
           vbuf = (has && vbase + sl < len) ? __ldg(steps + k0 + vbase + sl)
                                            : 0;
         }
         const int v = __shfl_sync(FULL, vbuf, (k - vbase) & (W - 1), W);
-        const bool ok = k < len && lane_ok;
-        const double *fp = x + (int64_t)v * col + (int64_t)l * CH;
-        const double *cp = coords + (int64_t)v * ccol + 3 * (int64_t)l;
+        if (k < len && lane_ok) {
+          const double *fp = x + (int64_t)v * col + (int64_t)l * CH;
+          const double *cp = coords + (int64_t)v * ccol + 3 * (int64_t)l;
+          double *r = row(slot, sl);
 #pragma unroll
-        for (int q = 0; q < CH; ++q) f[q] = ok ? __ldg(fp + q) : 0.0;
+          for (int q = 0; q < CH; ++q) sr_cp8(r + q, fp + q);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) c3[q] = ok ? __ldg(cp + q) : 0.0;
+          for (int q = 0; q < 3; ++q) sr_cp8(r + CH + q, cp + q);
+          if (sl == nl - 1) { // the level above the chunk's last layer
+            double *t = row(slot, W);
+#pragma unroll
+            for (int q = 0; q < LV; ++q) sr_cp8(t + q, fp + CH + q);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) sr_cp8(t + CH + q, cp + 3 + q);
+          }
+        }
+        sr_commit(); // one group per step (possibly empty)
         return v;
       };
-      int vnext = fetch(0, nf, nc);
+#pragma unroll
+      for (int d = 0; d < kSrDepth; ++d) rv[d] = fetch(d, d);
 
       auto flush = [&](auto A_) {
         constexpr int A = decltype(A_)::value;
@@ -124,31 +165,31 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         constexpr int A = decltype(A_)::value;
         flush(A_);
         const bool act = k < len;
-        // the prefetched vertex enters slot A
-        const int64_t vcol = (int64_t)vnext;
+        // the vertex of ring slot A (step k) enters window slot A
+        sr_wait<kSrDepth - 1>(); // step k's copies (this lane's) landed
+        const int64_t vcol = (int64_t)rv[A];
+        const double *r = row(A, sl);
+        const double *t = row(A, W);
+        const bool top_own = sl == nl - 1;
 #pragma unroll
-        for (int c = 0; c < CH; ++c) fb[A][c] = nf[c];
+        for (int c = 0; c < CH; ++c) fb[A][c] = r[c];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) cb[A][q] = nc[q];
-        // level above: next lane (same vertex column), last lane loads
+        for (int q = 0; q < 3; ++q) cb[A][q] = r[CH + q];
+        // level above: the next lane's row (shfl), the last lane's own copy
 #pragma unroll
         for (int c = 0; c < LV; ++c) {
-          const double up = __shfl_down_sync(FULL, nf[c], 1, W);
-          ft[A][c] = (sl == nl - 1 && act)
-                         ? __ldg(x + vcol * col + (int64_t)(l + 1) * CH + c)
-                         : up;
+          const double up = __shfl_down_sync(FULL, fb[A][c], 1, W);
+          ft[A][c] = top_own ? t[c] : up;
         }
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-          const double up = __shfl_down_sync(FULL, nc[q], 1, W);
-          ct[A][q] = (sl == nl - 1 && act)
-                         ? __ldg(coords + vcol * ccol + 3 * (int64_t)(l + 1) + q)
-                         : up;
+          const double up = __shfl_down_sync(FULL, cb[A][q], 1, W);
+          ct[A][q] = top_own ? t[CH + q] : up;
         }
         vo[A] = vcol * col;
         live[A] = act;
-        // prefetch the next step's vertex while this cell computes
-        vnext = fetch(k + 1, nf, nc);
+        // refill ring slot A with the step kSrDepth ahead
+        rv[A] = fetch(k + kSrDepth, A);
         if (k < 2) return; // window not full yet
         double X[6], Y[6], Z[6];
 #pragma unroll
@@ -204,8 +245,15 @@ static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
   const int64_t warps = (items + segs - 1) / segs;
   const unsigned grid = grid_for(warps * 32, 256, 8);
 #define PM_SR(WW)                                                            \
-  k_strip_red<LY, WW><<<grid, 256, 0, a.s>>>(M, strip_ptr, steps, n_strips,  \
-                                             a.layers, a.coords, a.x, a.y)
+  do {                                                                       \
+    const size_t smem = sizeof(double) * 8 * kSrDepth * (32 / WW) *          \
+                        (WW + 1) * sr_row<LY>();                             \
+    PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
+        k_strip_red<LY, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+        (int)smem));                                                         \
+    k_strip_red<LY, WW><<<grid, 256, smem, a.s>>>(                           \
+        M, strip_ptr, steps, n_strips, a.layers, a.coords, a.x, a.y);        \
+  } while (0)
   if (W == 32)
     PM_SR(32);
   else if (W == 16)
