@@ -37,8 +37,12 @@ template <int N> __device__ __forceinline__ void sr_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// values per ring row: field (CH) + coordinates (3)
-template <class LY> constexpr int sr_row() { return LY::CH0 + 3; }
+// ring entry per segment: the vertex's chunk of the field column
+// (W*CH + LV values) and of the coordinate column (3*(W+1) values)
+template <class LY, int W> constexpr int sr_fs() { return W * LY::CH0 + LY::LV0; }
+template <class LY, int W> constexpr int sr_entry() {
+  return sr_fs<LY, W>() + 3 * (W + 1);
+}
 constexpr int kSrDepth = 3; // steps in flight per segment
 
 // 3-vector windows need more registers: one CTA per SM there
@@ -100,17 +104,18 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       // vertex ids of the strip, W at a time (lane sl holds step base+sl)
       int vbuf = (has && sl < len) ? __ldg(steps + k0 + sl) : 0;
       int vbase = 0;
-      // per-warp shared-memory prefetch ring, kSrDepth steps deep: lane sl
-      // copies (cp.async) the field + coordinates of its own level into row
-      // sl; the chunk's last lane also copies the level above into row W.
-      // Every lane reads only what it copied itself.
-      constexpr int RW = sr_row<LY>();
+      // per-warp shared-memory prefetch ring, kSrDepth steps deep: the
+      // segment copies its vertex's chunk of the field and coordinate
+      // columns contiguously (coalesced cp.async); lanes then read their
+      // own level (and the level above) out of shared memory.
+      constexpr int FS = sr_fs<LY, W>();
+      constexpr int ES = sr_entry<LY, W>();
       extern __shared__ double sr_ring[];
-      double *ring = sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS *
-                                   (W + 1) * RW;
-      auto row = [&](int slot, int r) {
-        return ring + ((size_t)(slot * SEGS + seg) * (W + 1) + r) * RW;
+      double *ring = sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
+      auto entry = [&](int slot) {
+        return ring + (size_t)(slot * SEGS + seg) * ES;
       };
+      const int fl = nl * CH + LV, cl = 3 * (nl + 1);
       int rv[kSrDepth];
       auto fetch = [&](int k, int slot) {
         if (k - vbase >= W) { // all segments advance in lockstep
@@ -119,20 +124,19 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
                                            : 0;
         }
         const int v = __shfl_sync(FULL, vbuf, (k - vbase) & (W - 1), W);
-        if (k < len && lane_ok) {
-          const double *fp = x + (int64_t)v * col + (int64_t)l * CH;
-          const double *cp = coords + (int64_t)v * ccol + 3 * (int64_t)l;
-          double *r = row(slot, sl);
+        if (k < len) {
+          const double *fp = x + (int64_t)v * col + (int64_t)l0 * CH;
+          const double *cp = coords + (int64_t)v * ccol + 3 * (int64_t)l0;
+          double *e = entry(slot);
 #pragma unroll
-          for (int q = 0; q < CH; ++q) sr_cp8(r + q, fp + q);
+          for (int r = 0; r < (FS + W - 1) / W; ++r) {
+            const int i = sl + W * r;
+            if (i < fl) sr_cp8(e + i, fp + i);
+          }
 #pragma unroll
-          for (int q = 0; q < 3; ++q) sr_cp8(r + CH + q, cp + q);
-          if (sl == nl - 1) { // the level above the chunk's last layer
-            double *t = row(slot, W);
-#pragma unroll
-            for (int q = 0; q < LV; ++q) sr_cp8(t + q, fp + CH + q);
-#pragma unroll
-            for (int q = 0; q < 3; ++q) sr_cp8(t + CH + q, cp + 3 + q);
+          for (int r = 0; r < (3 * (W + 1) + W - 1) / W; ++r) {
+            const int i = sl + W * r;
+            if (i < cl) sr_cp8(e + FS + i, cp + i);
           }
         }
         sr_commit(); // one group per step (possibly empty)
@@ -166,26 +170,20 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         flush(A_);
         const bool act = k < len;
         // the vertex of ring slot A (step k) enters window slot A
-        sr_wait<kSrDepth - 1>(); // step k's copies (this lane's) landed
+        sr_wait<kSrDepth - 1>(); // this lane's copies of step k landed
+        __syncwarp();            // ... and the other lanes' ones
         const int64_t vcol = (int64_t)rv[A];
-        const double *r = row(A, sl);
-        const double *t = row(A, W);
-        const bool top_own = sl == nl - 1;
+        const double *e = entry(A);
 #pragma unroll
-        for (int c = 0; c < CH; ++c) fb[A][c] = r[c];
+        for (int c = 0; c < CH; ++c) fb[A][c] = e[sl * CH + c];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) cb[A][q] = r[CH + q];
-        // level above: the next lane's row (shfl), the last lane's own copy
-#pragma unroll
-        for (int c = 0; c < LV; ++c) {
-          const double up = __shfl_down_sync(FULL, fb[A][c], 1, W);
-          ft[A][c] = top_own ? t[c] : up;
-        }
+        for (int c = 0; c < LV; ++c) ft[A][c] = e[(sl + 1) * CH + c];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-          const double up = __shfl_down_sync(FULL, cb[A][q], 1, W);
-          ct[A][q] = top_own ? t[CH + q] : up;
+          cb[A][q] = e[FS + 3 * sl + q];
+          ct[A][q] = e[FS + 3 * (sl + 1) + q];
         }
+        __syncwarp(); // reads done before the slot is refilled
         vo[A] = vcol * col;
         live[A] = act;
         // refill ring slot A with the step kSrDepth ahead
@@ -247,7 +245,7 @@ static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
 #define PM_SR(WW)                                                            \
   do {                                                                       \
     const size_t smem = sizeof(double) * 8 * kSrDepth * (32 / WW) *          \
-                        (WW + 1) * sr_row<LY>();                             \
+                        sr_entry<LY, WW>();                                  \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
         k_strip_red<LY, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
         (int)smem));                                                         \
