@@ -69,15 +69,16 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
   const int64_t col = (int64_t)layers * CH + LV; // vertex column length
   const int64_t ccol = 3 * (int64_t)(layers + 1);
 
-  // work item = (strip, layer chunk), chunk-major so that neighbouring
-  // strips (sharing vertex columns) run at the same time
+  // work item = (strip, layer chunk), chunk fastest: the chunks of a strip
+  // run side by side, so the sectors two chunks of a vertex column share
+  // are fetched once (neighbouring strips are still close in time)
   const int n_chunks = (layers + W - 1) / W;
   const int64_t n_items = n_strips * n_chunks;
   for (int64_t i0 = warp * SEGS; i0 < n_items; i0 += n_warps * SEGS) {
     const int64_t item = i0 + seg;
     const bool has = item < n_items;
-    const int64_t si = has ? item % n_strips : 0;
-    const int l0 = has ? (int)(item / n_strips) * W : 0;
+    const int64_t si = has ? item / n_chunks : 0;
+    const int l0 = has ? (int)(item % n_chunks) * W : 0;
     const int k0 = has ? __ldg(strip_ptr + si) : 0;
     const int len = has ? __ldg(strip_ptr + si + 1) - k0 : 0;
     int maxlen = len;
