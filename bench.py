@@ -312,7 +312,8 @@ def run_sharded(args, w):
                 "halo_bytes_rank0": op.halo.bytes_per_exchange(),
                 "setup_s_rank0": t_setup,
                 "l2": "inputs larger than L2: no flush",
-                "schedule": "column (REDG) over the rank's cell block"},
+                "schedule": ("strip-REDG" if op.strips is not None else
+                             "column (REDG)") + " over the rank's cell block"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak,
                          "traffic": ncu_traffic(w.name),

@@ -216,7 +216,9 @@ int pm_build_strips(int64_t n_patches, const int32_t *cell_ptr,
  * {strips, steps}. */
 int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                            const int32_t *cell_vertices,
-                           const int32_t *cell_edges, int32_t max_len,
+                           const int32_t *cell_edges,
+                           const uint8_t *cell_mask /* NULL: all cells */,
+                           int32_t max_len,
                            int32_t *strip_ptr, int32_t *steps,
                            int64_t *totals);
 

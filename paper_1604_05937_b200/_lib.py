@@ -68,8 +68,8 @@ SIGNATURES = {
                                                 ctypes.POINTER(_f64), _vp,
                                                 _vp, _i64, _i32, _i64, _i32,
                                                 _vp, _vp, _vp]),
-    "pm_build_global_strips": (ctypes.c_int, [_i64, _i64, _vp, _vp, _i32,
-                                              _vp, _vp, _vp]),
+    "pm_build_global_strips": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp,
+                                              _i32, _vp, _vp, _vp]),
     "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
                                        _vp, _vp]),
     "pm_halo_pack": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
@@ -279,16 +279,22 @@ def column_mass_strip(layout, k, layers, coords, mref, x, y, plan, dplan,
     check(rc)
 
 
-def build_global_strips(base, max_len=64):
-    """(strip_ptr int32, steps int32) over the whole mesh (host C++)."""
+def build_global_strips(base, max_len=32, cells=None):
+    """(strip_ptr int32, steps int32): sequential strips over the mesh or
+    over the subset ``cells`` (host C++)."""
     cv = np.ascontiguousarray(base.cell_vertices, dtype=np.int32)
     ce = np.ascontiguousarray(base.cell_edges, dtype=np.int32)
     n = cv.shape[0]
+    mask = None
+    if cells is not None:
+        mask = np.zeros(n, dtype=np.uint8)
+        mask[np.asarray(cells)] = 1
     sp = np.zeros(n + 1, dtype=np.int32)
     st = np.zeros(3 * n + 3, dtype=np.int32)
     tot = np.zeros(2, dtype=np.int64)
     check(host_lib().pm_build_global_strips(
         n, base.num_edges, cv.ctypes.data_as(_i32p), ce.ctypes.data_as(_i32p),
+        None if mask is None else mask.ctypes.data_as(ctypes.c_void_p),
         max_len, sp.ctypes.data_as(_i32p), st.ctypes.data_as(_i32p),
         tot.ctypes.data_as(_i64p)))
     sp, st = sp[:tot[0] + 1].copy(), st[:tot[1]].copy()
@@ -306,16 +312,18 @@ def build_global_strips(base, max_len=64):
 
 
 def column_mass_strip_red(layout, k, layers, coords, mref, x, y, n_dofs,
-                          strips, kron, chunk, accumulate=False, stream=None):
+                          strips, kron, chunk, accumulate=False, stream=None,
+                          x_base=0, y_base=0, coords_base=0):
     m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
     mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
     ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
     d = layout.delta6()
     sp, st = strips
     rc = host_lib().pm_column_mass_strip_red(
-        d.ctypes.data_as(_i32p), k, layers, ptr(coords), _f64ptr(m),
-        _f64ptr(mt), _f64ptr(ml), ptr(x), ptr(y), n_dofs,
-        1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp), ptr(st),
+        d.ctypes.data_as(_i32p), k, layers, ptr(coords, coords_base),
+        _f64ptr(m), _f64ptr(mt), _f64ptr(ml), ptr(x, x_base), ptr(y, y_base),
+        n_dofs, 1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp),
+        ptr(st),
         stream_ptr(stream))
     check(rc)
 

@@ -322,6 +322,7 @@ extern "C" int pm_build_strips(
 extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                                       const int32_t *cell_vertices,
                                       const int32_t *cell_edges,
+                                      const uint8_t *cell_mask,
                                       int32_t max_len, int32_t *strip_ptr,
                                       int32_t *steps, int64_t *totals) {
   pm::clear_error();
@@ -332,13 +333,17 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
   std::vector<int32_t> ec(2 * (size_t)n_edges, -1);
   for (int64_t c = 0; c < n_cells; ++c)
     for (int k = 0; k < 3; ++k) {
+      if (cell_mask && !cell_mask[c]) break;
       const int64_t e = cell_edges[3 * c + k];
       if (ec[2 * e] < 0)
         ec[2 * e] = (int32_t)c;
       else
         ec[2 * e + 1] = (int32_t)c;
     }
+  // cells outside the mask count as used: strips stay inside the subset
   std::vector<uint8_t> used(n_cells, 0);
+  if (cell_mask)
+    for (int64_t c = 0; c < n_cells; ++c) used[c] = !cell_mask[c];
   auto vid = [&](int64_t c, int k) { return cell_vertices[3 * c + k]; };
   auto across = [&](int64_t c, int32_t u, int32_t w) -> int64_t {
     for (int k = 0; k < 3; ++k) {

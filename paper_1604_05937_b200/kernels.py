@@ -132,8 +132,8 @@ class MassOperator:
         """Column-loop kernel launches one ``apply`` issues."""
         if self.schedule in ("colored", "sequential") and self.share == 2:
             return self._color_lists()[1].shape[0] - 1
-        if self.schedule in ("auto", "patch") and self.share == 2 and \
-                self.patch_ok:
+        if self.schedule in ("auto", "patch", "stripred", "strip") and \
+                self.share == 2:
             return 1
         return 1
 
@@ -211,8 +211,10 @@ class MassOperator:
             accumulate = False
         if not self.kron_ok and sched != "stream":
             sched = "atomic"   # dense Mref in the generic kernel
-        if sched == "auto" and self.share == 2 and self.patch_ok:
-            sched = "patch"
+        if sched == "auto" and self.share == 2:
+            # measured fastest (profiles/): global strips for vertex-column
+            # layouts, the warp-per-column kernel otherwise
+            sched = "stripred" if self.strip_ok else "column"
         if sched == "stripred":
             if not self.strip_ok:
                 raise ValueError(
@@ -298,6 +300,13 @@ _VARIANTS = {"auto": _lib.VARIANT_AUTO, "atomic": _lib.VARIANT_ATOMIC,
              # sharing: the column kernel writes every DoF exactly once
              "colored": _lib.VARIANT_COLUMN,
              "sequential": _lib.VARIANT_COLUMN}
+
+
+def strip_chunk_width(layers: int) -> int:
+    """Lanes per layer chunk for the strip kernel (least lane waste, a
+    small per-chunk charge)."""
+    return min((8, 16, 32), key=lambda w: (-(-layers // w) * w / layers
+                                           + 0.05 * (-(-layers // w)), -w))
 
 
 _COLORINGS = {}

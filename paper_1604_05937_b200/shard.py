@@ -199,6 +199,9 @@ class ShardedMassOperator:
         self.op = MassOperator(fs, quadrature, schedule="column")
         dev = self.op._dev
         self.d_cells = torch.from_numpy(self.shard.cells).to(dev)
+        # vertex-column layouts: sequential strips over the rank's block
+        self.strips = (self.op._global_strips(cells=self.shard.cells)
+                       if self.op.strip_ok and self.op.kron_ok else None)
         self.halo = HaloExchange(fs, self.shard, device=dev)
         self._lib = _lib
 
@@ -215,12 +218,19 @@ class ShardedMassOperator:
                                    device=x_window.device)
         y_window.zero_()
         op = self.op
-        self._lib.column_mass(
-            op.fs.layout, op.k, op.n_cells, op.layers, op.cmap, op.offs,
-            op.xmap, op.xoffs, coords_window, op.mref, x_window, y_window,
-            hi - lo, accumulate=True, variant=self._lib.VARIANT_COLUMN,
-            cells=self.d_cells, kron=op.kron, x_base=lo, y_base=lo,
-            coords_base=clo)
+        if self.strips is not None:
+            strips, W = self.strips
+            self._lib.column_mass_strip_red(
+                op.fs.layout, op.k, op.layers, coords_window, op.mref,
+                x_window, y_window, hi - lo, strips, op.kron, W,
+                accumulate=True, x_base=lo, y_base=lo, coords_base=clo)
+        else:
+            self._lib.column_mass(
+                op.fs.layout, op.k, op.n_cells, op.layers, op.cmap, op.offs,
+                op.xmap, op.xoffs, coords_window, op.mref, x_window,
+                y_window, hi - lo, accumulate=True,
+                variant=self._lib.VARIANT_COLUMN, cells=self.d_cells,
+                kron=op.kron, x_base=lo, y_base=lo, coords_base=clo)
         if exchange and self.world > 1:
             self.halo.exchange(y_window, group=self.group)
         return y_window
