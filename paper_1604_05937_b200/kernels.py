@@ -156,15 +156,18 @@ class MassOperator:
         d = tuple(self.fs.layout.delta6())
         return d in _STRIP_LAYOUTS
 
-    def _global_strips(self):
-        if self._gstrips is None:
+    def _global_strips(self, cells=None):
+        """Sequential strips over the mesh (cached) or over ``cells``."""
+        if self._gstrips is None or cells is not None:
             import torch
-            sp, st = _lib.build_global_strips(self.fs.mesh.base, max_len=32)
-            L = self.layers
-            W = min((8, 16, 32), key=lambda w: (-(-L // w) * w / L
-                                                 + 0.05 * (-(-L // w)), -w))
-            self._gstrips = ((torch.from_numpy(sp).to(self._dev),
-                              torch.from_numpy(st).to(self._dev)), W)
+            sp, st = _lib.build_global_strips(self.fs.mesh.base, max_len=32,
+                                              cells=cells)
+            g = ((torch.from_numpy(sp).to(self._dev),
+                  torch.from_numpy(st).to(self._dev)),
+                 strip_chunk_width(self.layers))
+            if cells is not None:
+                return g
+            self._gstrips = g
         return self._gstrips
 
     def _strip_plan(self):
