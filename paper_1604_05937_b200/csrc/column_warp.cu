@@ -188,7 +188,8 @@ static int column_k(const LoopArgs &a, bool colored) {
     double best = 1e30;
     for (int w : {32, 16, 8}) {
       const int chunks = (a.layers + w - 1) / w;
-      const double waste = (double)(chunks * w) / a.layers + 0.02 * chunks;
+      // measured (profiles/r01): small segments win -- more cells per warp
+      const double waste = (double)(chunks * w) / a.layers + 0.005 * chunks;
       if (waste < best - 1e-9) {
         best = waste;
         W = w;

@@ -160,8 +160,10 @@ class MassOperator:
         """Sequential strips over the mesh (cached) or over ``cells``."""
         if self._gstrips is None or cells is not None:
             import torch
-            sp, st = _lib.build_global_strips(self.fs.mesh.base, max_len=32,
-                                              cells=cells)
+            n = self.n_cells if cells is None else len(cells)
+            sp, st = _lib.build_global_strips(
+                self.fs.mesh.base, max_len=strip_max_len(n, self.layers),
+                cells=cells)
             g = ((torch.from_numpy(sp).to(self._dev),
                   torch.from_numpy(st).to(self._dev)),
                  strip_chunk_width(self.layers))
@@ -307,9 +309,20 @@ _VARIANTS = {"auto": _lib.VARIANT_AUTO, "atomic": _lib.VARIANT_ATOMIC,
 
 def strip_chunk_width(layers: int) -> int:
     """Lanes per layer chunk for the strip kernel (least lane waste, a
-    small per-chunk charge)."""
+    small per-chunk charge); PM_STRIP_W overrides (tuning knob)."""
+    import os
+    forced = int(os.environ.get("PM_STRIP_W", "0"))
+    if forced in (8, 16, 32):
+        return forced
     return min((8, 16, 32), key=lambda w: (-(-layers // w) * w / layers
                                            + 0.05 * (-(-layers // w)), -w))
+
+
+def strip_max_len(n_cells: int, layers: int) -> int:
+    """Strip length cap: long strips amortise the 3-vertex fill, but small
+    meshes need enough (strip, chunk) items to fill 148 SMs."""
+    chunks = -(-layers // strip_chunk_width(layers))
+    return int(max(4, min(32, n_cells * chunks // 24000)))
 
 
 _COLORINGS = {}
