@@ -118,13 +118,12 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       };
       const int fl = nl * CH + LV, cl = 3 * (nl + 1);
       int rv[kSrDepth];
-      // branch-free: every shuffle below runs with the whole warp converged
       auto fetch = [&](int k, int slot) {
-        const bool refill = k - vbase >= W; // uniform across the warp
-        vbase += refill ? W : 0;
-        const bool ld = refill && has && vbase + sl < len;
-        const int fresh = ld ? __ldg(steps + k0 + vbase + sl) : 0;
-        vbuf = refill ? fresh : vbuf;
+        if (k - vbase >= W) { // all segments advance in lockstep
+          vbase += W;
+          vbuf = (has && vbase + sl < len) ? __ldg(steps + k0 + vbase + sl)
+                                           : 0;
+        }
         const int v = __shfl_sync(FULL, vbuf, (k - vbase) & (W - 1), W);
         if (k < len) {
           const double *fp = x + (int64_t)v * col + (int64_t)l0 * CH;
@@ -190,9 +189,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         live[A] = act;
         // refill ring slot A with the step kSrDepth ahead
         rv[A] = fetch(k + kSrDepth, A);
-        // the cell (window full from the third step on); computed by every
-        // lane, accumulated only where it is real
-        const bool use = act && lane_ok && k >= 2;
+        if (k < 2) return; // window not full yet
         double X[6], Y[6], Z[6];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
@@ -200,7 +197,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
           X[2 * a + 1] = ct[a][0], Y[2 * a + 1] = ct[a][1];
           Z[2 * a + 1] = ct[a][2];
         }
-        const double det = use ? prism_abs_detj(X, Y, Z) : 0.0;
+        const double det = (act && lane_ok) ? prism_abs_detj(X, Y, Z) : 0.0;
         double xv[K], yv[K];
 #pragma unroll
         for (int j = 0; j < K; ++j) {
