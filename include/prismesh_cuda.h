@@ -162,7 +162,9 @@ int pm_column_mass_strip_red(const int32_t *delta6, int32_t k, int32_t layers,
                              const double *x, double *y, int64_t n_dofs,
                              int32_t accumulate, int64_t n_strips,
                              int32_t chunk, const int32_t *strip_ptr,
-                             const int32_t *steps, void *stream);
+                             const int32_t *steps,
+                             const int32_t *steps_e /* P2: 2 edges/step */,
+                             int64_t n_vertices, void *stream);
 
 /* --- probes for the par-loop itself (exact integer checks) -------------
  * mode 0: out_i64[(c*layers+l)*k + j] = cell_map[c*k+j] + l*offsets[j]
@@ -218,8 +220,9 @@ int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                            const int32_t *cell_vertices,
                            const int32_t *cell_edges,
                            const uint8_t *cell_mask /* NULL: all cells */,
-                           int32_t max_len,
-                           int32_t *strip_ptr, int32_t *steps,
+                           int32_t max_len, int32_t *strip_ptr,
+                           int32_t *steps,
+                           int32_t *steps_e /* NULL, or 2 edges per step */,
                            int64_t *totals);
 
 /* Device properties used to size grids (SM count, L2 bytes). */

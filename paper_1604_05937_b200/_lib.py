@@ -67,9 +67,9 @@ SIGNATURES = {
                                                 ctypes.POINTER(_f64),
                                                 ctypes.POINTER(_f64), _vp,
                                                 _vp, _i64, _i32, _i64, _i32,
-                                                _vp, _vp, _vp]),
+                                                _vp, _vp, _vp, _i64, _vp]),
     "pm_build_global_strips": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp,
-                                              _i32, _vp, _vp, _vp]),
+                                              _i32, _vp, _vp, _vp, _vp]),
     "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
                                        _vp, _vp]),
     "pm_halo_pack": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
@@ -279,9 +279,10 @@ def column_mass_strip(layout, k, layers, coords, mref, x, y, plan, dplan,
     check(rc)
 
 
-def build_global_strips(base, max_len=32, cells=None):
-    """(strip_ptr int32, steps int32): sequential strips over the mesh or
-    over the subset ``cells`` (host C++)."""
+def build_global_strips(base, max_len=32, cells=None, edges=False):
+    """(strip_ptr int32, steps int32[, steps_e int32 (n_steps, 2)]):
+    sequential strips over the mesh or over the subset ``cells`` (host
+    C++); with ``edges`` also the two window edges each step brings in."""
     cv = np.ascontiguousarray(base.cell_vertices, dtype=np.int32)
     ce = np.ascontiguousarray(base.cell_edges, dtype=np.int32)
     n = cv.shape[0]
@@ -291,13 +292,17 @@ def build_global_strips(base, max_len=32, cells=None):
         mask[np.asarray(cells)] = 1
     sp = np.zeros(n + 1, dtype=np.int32)
     st = np.zeros(3 * n + 3, dtype=np.int32)
+    se = np.zeros((3 * n + 3, 2), dtype=np.int32) if edges else None
     tot = np.zeros(2, dtype=np.int64)
     check(host_lib().pm_build_global_strips(
         n, base.num_edges, cv.ctypes.data_as(_i32p), ce.ctypes.data_as(_i32p),
         None if mask is None else mask.ctypes.data_as(ctypes.c_void_p),
         max_len, sp.ctypes.data_as(_i32p), st.ctypes.data_as(_i32p),
+        None if se is None else se.ctypes.data_as(_i32p),
         tot.ctypes.data_as(_i64p)))
     sp, st = sp[:tot[0] + 1].copy(), st[:tot[1]].copy()
+    if se is not None:
+        se = se[:tot[1]].copy()
     # order strips by their mean vertex id: strips running concurrently on
     # the GPU then share vertex columns (L2 reuse)
     lens = np.diff(sp)
@@ -308,23 +313,26 @@ def build_global_strips(base, max_len=32, cells=None):
     np.cumsum(lens[order], out=new_sp[1:])
     idx = np.concatenate([np.arange(sp[i], sp[i + 1]) for i in order]) \
         if order.size else np.zeros(0, dtype=np.int64)
+    if se is not None:
+        return new_sp, st[idx].astype(np.int32), \
+            np.ascontiguousarray(se[idx], dtype=np.int32)
     return new_sp, st[idx].astype(np.int32)
 
 
 def column_mass_strip_red(layout, k, layers, coords, mref, x, y, n_dofs,
                           strips, kron, chunk, accumulate=False, stream=None,
-                          x_base=0, y_base=0, coords_base=0):
+                          x_base=0, y_base=0, coords_base=0, n_vertices=0):
     m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
     mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
     ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
     d = layout.delta6()
-    sp, st = strips
+    sp, st = strips[0], strips[1]
+    se = strips[2] if len(strips) > 2 else None
     rc = host_lib().pm_column_mass_strip_red(
         d.ctypes.data_as(_i32p), k, layers, ptr(coords, coords_base),
         _f64ptr(m), _f64ptr(mt), _f64ptr(ml), ptr(x, x_base), ptr(y, y_base),
         n_dofs, 1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp),
-        ptr(st),
-        stream_ptr(stream))
+        ptr(st), ptr(se), n_vertices, stream_ptr(stream))
     check(rc)
 
 

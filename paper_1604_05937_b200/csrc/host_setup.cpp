@@ -324,7 +324,8 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                                       const int32_t *cell_edges,
                                       const uint8_t *cell_mask,
                                       int32_t max_len, int32_t *strip_ptr,
-                                      int32_t *steps, int64_t *totals) {
+                                      int32_t *steps, int32_t *steps_e,
+                                      int64_t *totals) {
   pm::clear_error();
   if (n_cells < 0 || n_edges < 0 || max_len < 1) {
     pm::set_error("pm_build_global_strips: bad arguments");
@@ -361,6 +362,12 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
       if (vid(c, q) != u && vid(c, q) != w) return vid(c, q);
     return -1;
   };
+  // edge of cell c opposite its vertex v (joins the other two)
+  auto opp = [&](int64_t c, int32_t v) -> int32_t {
+    for (int q = 0; q < 3; ++q)
+      if (vid(c, q) == v) return cell_edges[3 * c + q];
+    return -1;
+  };
   int64_t n_strips = 0, n_steps = 0, scan = 0;
   strip_ptr[0] = 0;
   while (true) {
@@ -389,7 +396,14 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
         }
       }
     }
-    for (int k = 0; k < 3; ++k) steps[n_steps++] = win[k];
+    for (int k = 0; k < 3; ++k) {
+      // fill: vertex slot k and the edge opposite it (edge slot k)
+      if (steps_e) {
+        steps_e[2 * n_steps] = opp(cur, win[k]);
+        steps_e[2 * n_steps + 1] = -1;
+      }
+      steps[n_steps++] = win[k];
+    }
     int32_t len = 1, slot = 0;
     while (next >= 0 && len < max_len) {
       const int32_t nv = third(next, win[(slot + 1) % 3], win[(slot + 2) % 3]);
@@ -398,6 +412,12 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
         return PM_EINVAL;
       }
       used[next] = 1;
+      if (steps_e) {
+        // new edge slots (slot+1)%3 and (slot+2)%3: opposite the kept
+        // vertices in the new cell (edge slot `slot` keeps the shared edge)
+        steps_e[2 * n_steps] = opp(next, win[(slot + 1) % 3]);
+        steps_e[2 * n_steps + 1] = opp(next, win[(slot + 2) % 3]);
+      }
       win[slot] = nv;
       steps[n_steps++] = nv;
       cur = next;

@@ -268,6 +268,315 @@ static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
   return PM_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Vertex + edge layouts (P2 x P2): the window also holds the three edges,
+// edge slot a opposite window vertex a.  A step replacing vertex slot s
+// keeps edge slot s (the shared edge) and brings in the two new edges for
+// slots s+1, s+2, so each cell costs one vertex + two edge column loads and
+// three partial flushes (against six gathers / six scatters per cell-layer
+// for the column kernel).
+// ---------------------------------------------------------------------------
+template <class LY, int W> constexpr int sre_fs0() { return W * LY::CH0 + LY::LV0; }
+template <class LY, int W> constexpr int sre_fs1() { return W * LY::CH1 + LY::LV1; }
+template <class LY, int W> constexpr int sre_entry() {
+  return sre_fs0<LY, W>() + 3 * (W + 1) + 2 * sre_fs1<LY, W>();
+}
+
+template <class LY, int W, int K = LY::K>
+__global__ void __launch_bounds__(256, 1)
+k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
+              const int32_t *__restrict__ steps,
+              const int32_t *__restrict__ steps_e, int64_t n_strips,
+              int layers, int64_t e_start, const double *__restrict__ coords,
+              const double *__restrict__ x, double *__restrict__ y) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int SEGS = 32 / W;
+  constexpr typename LY::Tab T = LY::make();
+  constexpr int LV0 = LY::LV0, CH0 = LY::CH0, LV1 = LY::LV1, CH1 = LY::CH1;
+  constexpr int FS0 = sre_fs0<LY, W>(), FS1 = sre_fs1<LY, W>();
+  constexpr int ES = sre_entry<LY, W>();
+  constexpr int OC = FS0, OE1 = FS0 + 3 * (W + 1), OE2 = OE1 + FS1;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % W, seg = lane / W;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t col0 = (int64_t)layers * CH0 + LV0;
+  const int64_t col1 = (int64_t)layers * CH1 + LV1;
+  const int64_t ccol = 3 * (int64_t)(layers + 1);
+  extern __shared__ double sr_ring[];
+  double *ring =
+      sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
+
+  const int n_chunks = (layers + W - 1) / W;
+  const int64_t n_items = n_strips * n_chunks;
+  for (int64_t i0 = warp * SEGS; i0 < n_items; i0 += n_warps * SEGS) {
+    const int64_t item = i0 + seg;
+    const bool has = item < n_items;
+    const int64_t si = has ? item / n_chunks : 0;
+    const int l0 = has ? (int)(item % n_chunks) * W : 0;
+    const int k0 = has ? __ldg(strip_ptr + si) : 0;
+    const int len = has ? __ldg(strip_ptr + si + 1) - k0 : 0;
+    int maxlen = len;
+#pragma unroll
+    for (int o = W; o < 32; o <<= 1)
+      maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
+    const int nl = has ? min(W, layers - l0) : 0;
+    const int l = l0 + sl;
+    const bool lane_ok = sl < nl;
+    const int fl0 = nl * CH0 + LV0, fl1 = nl * CH1 + LV1, cl = 3 * (nl + 1);
+
+    // window: vertices (field, coordinates) and edges (field)
+    double vb[3][CH0], vt[3][LV0], cb[3][3], ct[3][3], eb[3][CH1], et[3][LV1];
+    double vab[3][CH0], vat[3][LV0], eab[3][CH1], eat[3][LV1];
+    int64_t vo[3] = {0, 0, 0}, eo[3] = {0, 0, 0};
+    bool vlive[3] = {false, false, false}, elive[3] = {false, false, false};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+      for (int c = 0; c < CH0; ++c) vb[a][c] = 0.0, vab[a][c] = 0.0;
+#pragma unroll
+      for (int c = 0; c < LV0; ++c) vt[a][c] = 0.0, vat[a][c] = 0.0;
+#pragma unroll
+      for (int c = 0; c < CH1; ++c) eb[a][c] = 0.0, eab[a][c] = 0.0;
+#pragma unroll
+      for (int c = 0; c < LV1; ++c) et[a][c] = 0.0, eat[a][c] = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) cb[a][q] = 0.0, ct[a][q] = 0.0;
+    }
+    // ids of the strip's steps, W at a time
+    int vbuf = (has && sl < len) ? __ldg(steps + k0 + sl) : 0;
+    int e1buf = (has && sl < len) ? __ldg(steps_e + 2 * (k0 + sl)) : 0;
+    int e2buf = (has && sl < len) ? __ldg(steps_e + 2 * (k0 + sl) + 1) : 0;
+    int vbase = 0;
+    auto entry = [&](int slot) {
+      return ring + (size_t)(slot * SEGS + seg) * ES;
+    };
+    int rv[kSrDepth], re1[kSrDepth], re2[kSrDepth];
+    auto seg_copy = [&](double *dst, const double *src, int n, int cap) {
+#pragma unroll
+      for (int r = 0; r < (cap + W - 1) / W; ++r) {
+        const int i = sl + W * r;
+        if (i < n) sr_cp8(dst + i, src + i);
+      }
+    };
+    auto fetch = [&](int k, int slot) {
+      if (k - vbase >= W) { // all segments advance in lockstep
+        vbase += W;
+        const bool ok = has && vbase + sl < len;
+        vbuf = ok ? __ldg(steps + k0 + vbase + sl) : 0;
+        e1buf = ok ? __ldg(steps_e + 2 * (k0 + vbase + sl)) : 0;
+        e2buf = ok ? __ldg(steps_e + 2 * (k0 + vbase + sl) + 1) : 0;
+      }
+      const int idx = (k - vbase) & (W - 1);
+      const int v = __shfl_sync(FULL, vbuf, idx, W);
+      const int e1 = __shfl_sync(FULL, e1buf, idx, W);
+      const int e2 = __shfl_sync(FULL, e2buf, idx, W);
+      if (k < len) {
+        double *en = entry(slot);
+        seg_copy(en, x + (int64_t)v * col0 + (int64_t)l0 * CH0, fl0, FS0);
+        seg_copy(en + OC, coords + (int64_t)v * ccol + 3 * (int64_t)l0, cl,
+                 3 * (W + 1));
+        seg_copy(en + OE1, x + e_start + (int64_t)e1 * col1 +
+                               (int64_t)l0 * CH1, fl1, FS1);
+        if (k >= 3)
+          seg_copy(en + OE2, x + e_start + (int64_t)e2 * col1 +
+                                 (int64_t)l0 * CH1, fl1, FS1);
+      }
+      sr_commit();
+      rv[slot] = v, re1[slot] = e1, re2[slot] = e2;
+    };
+#pragma unroll
+    for (int d = 0; d < kSrDepth; ++d) fetch(d, d);
+
+    // flush a vertex / edge residency (top contributions one lane up)
+    auto flush_v = [&](auto A_) {
+      constexpr int A = decltype(A_)::value;
+#pragma unroll
+      for (int c = 0; c < CH0; ++c) {
+        double v = vab[A][c];
+        if (c < LV0) {
+          const double below = __shfl_up_sync(FULL, vat[A][c], 1, W);
+          if (sl > 0) v += below;
+        }
+        if (vlive[A] && lane_ok) {
+          double *yp = y + vo[A] + (int64_t)l * CH0 + c;
+          atomicAdd(yp, v);
+          if (c < LV0 && sl == nl - 1) atomicAdd(yp + CH0, vat[A][c]);
+        }
+        vab[A][c] = 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < LV0; ++c) vat[A][c] = 0.0;
+    };
+    auto flush_e = [&](auto A_) {
+      constexpr int A = decltype(A_)::value;
+#pragma unroll
+      for (int c = 0; c < CH1; ++c) {
+        double v = eab[A][c];
+        if (c < LV1) {
+          const double below = __shfl_up_sync(FULL, eat[A][c], 1, W);
+          if (sl > 0) v += below;
+        }
+        if (elive[A] && lane_ok) {
+          double *yp = y + eo[A] + (int64_t)l * CH1 + c;
+          atomicAdd(yp, v);
+          if (c < LV1 && sl == nl - 1) atomicAdd(yp + CH1, eat[A][c]);
+        }
+        eab[A][c] = 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < LV1; ++c) eat[A][c] = 0.0;
+    };
+    auto load_e = [&](auto A_, const double *src, int64_t origin, bool act) {
+      constexpr int A = decltype(A_)::value;
+#pragma unroll
+      for (int c = 0; c < CH1; ++c) eb[A][c] = src[sl * CH1 + c];
+#pragma unroll
+      for (int c = 0; c < LV1; ++c) et[A][c] = src[(sl + 1) * CH1 + c];
+      eo[A] = origin;
+      elive[A] = act;
+    };
+    // one strip step into vertex slot A; FILL: edge slot A, else the edge
+    // slots A+1, A+2
+    auto step = [&](auto A_, auto FILL_, int k) {
+      constexpr int A = decltype(A_)::value;
+      constexpr bool FILL = decltype(FILL_)::value;
+      constexpr int B1 = (A + 1) % 3, B2 = (A + 2) % 3;
+      using I1 = std::integral_constant<int, B1>;
+      using I2 = std::integral_constant<int, B2>;
+      flush_v(A_);
+      if (FILL) {
+        flush_e(A_);
+      } else {
+        flush_e(I1{});
+        flush_e(I2{});
+      }
+      const bool act = k < len;
+      sr_wait<kSrDepth - 1>();
+      __syncwarp();
+      const double *en = entry(A);
+#pragma unroll
+      for (int c = 0; c < CH0; ++c) vb[A][c] = en[sl * CH0 + c];
+#pragma unroll
+      for (int c = 0; c < LV0; ++c) vt[A][c] = en[(sl + 1) * CH0 + c];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        cb[A][q] = en[OC + 3 * sl + q];
+        ct[A][q] = en[OC + 3 * (sl + 1) + q];
+      }
+      vo[A] = (int64_t)rv[A] * col0;
+      vlive[A] = act;
+      if (FILL) {
+        load_e(A_, en + OE1, e_start + (int64_t)re1[A] * col1, act);
+      } else {
+        load_e(I1{}, en + OE1, e_start + (int64_t)re1[A] * col1, act);
+        load_e(I2{}, en + OE2, e_start + (int64_t)re2[A] * col1, act);
+      }
+      __syncwarp();
+      fetch(k + kSrDepth, A);
+      if (FILL && A < 2) return; // window not full yet
+      double X[6], Y[6], Z[6];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        X[2 * a] = cb[a][0], Y[2 * a] = cb[a][1], Z[2 * a] = cb[a][2];
+        X[2 * a + 1] = ct[a][0], Y[2 * a + 1] = ct[a][1];
+        Z[2 * a + 1] = ct[a][2];
+      }
+      const double det = (act && lane_ok) ? prism_abs_detj(X, Y, Z) : 0.0;
+      double xv[K], yv[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const int p = T.pos[j];
+        if (p < 3)
+          xv[j] = T.level[j] == 2 ? vt[p][T.ch[j]] : vb[p][T.ch[j]];
+        else
+          xv[j] = T.level[j] == 2 ? et[p - 3][T.ch[j]] : eb[p - 3][T.ch[j]];
+      }
+      kron_apply<LY>(M, xv, det, yv);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const int p = T.pos[j];
+        if (p < 3) {
+          if (T.level[j] == 2)
+            vat[p][T.ch[j]] += yv[j];
+          else
+            vab[p][T.ch[j]] += yv[j];
+        } else {
+          if (T.level[j] == 2)
+            eat[p - 3][T.ch[j]] += yv[j];
+          else
+            eab[p - 3][T.ch[j]] += yv[j];
+        }
+      }
+    };
+    using S0 = std::integral_constant<int, 0>;
+    using S1 = std::integral_constant<int, 1>;
+    using S2 = std::integral_constant<int, 2>;
+    using TF = std::true_type;
+    using FF = std::false_type;
+    step(S0{}, TF{}, 0);
+    step(S1{}, TF{}, 1);
+    step(S2{}, TF{}, 2);
+    for (int k = 3; k < maxlen; k += 3) {
+      step(S0{}, FF{}, k);
+      step(S1{}, FF{}, k + 1);
+      step(S2{}, FF{}, k + 2);
+    }
+    flush_v(S0{});
+    flush_v(S1{});
+    flush_v(S2{});
+    flush_e(S0{});
+    flush_e(S1{});
+    flush_e(S2{});
+  }
+}
+
+template <class LY>
+static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
+                         const int32_t *steps, const int32_t *steps_e,
+                         int64_t n_strips, int W, int64_t e_start) {
+  if (!a.mtri || !a.mline) {
+    set_error("the strip kernel needs the Kronecker factors mtri/mline");
+    return PM_EINVAL;
+  }
+  if (!steps_e) {
+    set_error("edge layouts need the strips' edge records (steps_e)");
+    return PM_EINVAL;
+  }
+  KronMat M;
+  for (int i = 0; i < LY::NH * LY::NH; ++i) M.t[i] = a.mtri[i];
+  for (int i = 0; i < LY::NV * LY::NV; ++i) M.l[i] = a.mline[i];
+  const int segs = 32 / W;
+  const int64_t items = n_strips * ((a.layers + W - 1) / W);
+  const int64_t warps = (items + segs - 1) / segs;
+  const unsigned grid = grid_for(warps * 32, 256, 4);
+#define PM_SRE(WW)                                                           \
+  do {                                                                       \
+    const size_t smem =                                                      \
+        sizeof(double) * 8 * kSrDepth * (32 / WW) * sre_entry<LY, WW>();     \
+    PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
+        k_strip_red_e<LY, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+        (int)smem));                                                         \
+    k_strip_red_e<LY, WW><<<grid, 256, smem, a.s>>>(                         \
+        M, strip_ptr, steps, steps_e, n_strips, a.layers, e_start, a.coords, \
+        a.x, a.y);                                                           \
+  } while (0)
+  if (W == 32)
+    PM_SRE(32);
+  else if (W == 16)
+    PM_SRE(16);
+  else if (W == 8)
+    PM_SRE(8);
+  else {
+    set_error("strip chunk width must be 8, 16 or 32 (got %d)", W);
+    return PM_EINVAL;
+  }
+#undef PM_SRE
+  PM_LAUNCH_CHECK("k_strip_red_e");
+  return PM_OK;
+}
+
 #define PM_STRIPRED_LAYOUTS(X)                                               \
   X(1, 0, 0, 0, 0, 0)                                                        \
   X(0, 1, 0, 0, 0, 0)                                                        \
@@ -281,7 +590,8 @@ extern "C" int pm_column_mass_strip_red(
     const double *mref, const double *mtri, const double *mline,
     const double *x, double *y, int64_t n_dofs, int32_t accumulate,
     int64_t n_strips, int32_t chunk, const int32_t *strip_ptr,
-    const int32_t *steps, void *stream) {
+    const int32_t *steps, const int32_t *steps_e, int64_t n_vertices,
+    void *stream) {
   pm::clear_error();
   pm::LoopArgs a;
   int rc = pm::make_slot_table(delta6, &a.st);
@@ -312,6 +622,11 @@ extern "C" int pm_column_mass_strip_red(
         a, strip_ptr, steps, n_strips, chunk);
   PM_STRIPRED_LAYOUTS(PM_DISPATCH)
 #undef PM_DISPATCH
+  if (pm::Layout<1, 1, 1, 1, 0, 0>::matches(delta6)) {
+    const int64_t col0 = (int64_t)layers * 2 + 1;
+    return pm::strip_red_e_k<pm::Layout<1, 1, 1, 1, 0, 0>>(
+        a, strip_ptr, steps, steps_e, n_strips, chunk, col0 * n_vertices);
+  }
   pm::set_error("layout not supported by the strip schedule");
   return PM_EINVAL;
 }

@@ -161,11 +161,11 @@ class MassOperator:
         if self._gstrips is None or cells is not None:
             import torch
             n = self.n_cells if cells is None else len(cells)
-            sp, st = _lib.build_global_strips(
+            edges = bool(self.fs.layout.dofs(1, 0) or self.fs.layout.dofs(1, 1))
+            res = _lib.build_global_strips(
                 self.fs.mesh.base, max_len=strip_max_len(n, self.layers),
-                cells=cells)
-            g = ((torch.from_numpy(sp).to(self._dev),
-                  torch.from_numpy(st).to(self._dev)),
+                cells=cells, edges=edges)
+            g = (tuple(torch.from_numpy(a).to(self._dev) for a in res),
                  strip_chunk_width(self.layers))
             if cells is not None:
                 return g
@@ -219,9 +219,10 @@ class MassOperator:
         if sched == "auto" and self.share == 2:
             # measured fastest (profiles/): global strips for vertex-column
             # layouts, the warp-per-column kernel otherwise
-            sched = "stripred" if self.strip_ok else "column"
+            sched = "stripred" if tuple(self.fs.layout.delta6()) in \
+                _STRIPRED_LAYOUTS else "column"
         if sched == "stripred":
-            if not self.strip_ok:
+            if tuple(self.fs.layout.delta6()) not in _STRIPRED_LAYOUTS:
                 raise ValueError(
                     f"the strip schedule needs a vertex-column layout, got "
                     f"{self.fs.layout.name}")
@@ -229,7 +230,8 @@ class MassOperator:
             _lib.column_mass_strip_red(self.fs.layout, self.k, self.layers,
                                        coords, self.mref, x, y, n, strips,
                                        self.kron, W, accumulate=accumulate,
-                                       stream=stream)
+                                       stream=stream,
+                                       n_vertices=self.fs.mesh.base.num_vertices)
             return y
         if sched == "strip":
             if not self.strip_ok:
@@ -295,9 +297,10 @@ class MassOperator:
 _PATCH_LAYOUTS = {(1, 0, 0, 0, 0, 0), (0, 1, 0, 0, 0, 0), (0, 2, 0, 0, 0, 0),
                   (1, 1, 1, 1, 0, 0), (3, 0, 0, 0, 0, 0)}
 
-#: layouts compiled into the strip kernel (csrc/strip.cu)
+#: layouts compiled into the strip kernels (csrc/strip.cu, strip_red.cu)
 _STRIP_LAYOUTS = {(1, 0, 0, 0, 0, 0), (0, 1, 0, 0, 0, 0), (0, 2, 0, 0, 0, 0),
                   (3, 0, 0, 0, 0, 0)}
+_STRIPRED_LAYOUTS = _STRIP_LAYOUTS | {(1, 1, 1, 1, 0, 0)}
 
 _VARIANTS = {"auto": _lib.VARIANT_AUTO, "atomic": _lib.VARIANT_ATOMIC,
              "column": _lib.VARIANT_COLUMN, "stream": _lib.VARIANT_STREAM,

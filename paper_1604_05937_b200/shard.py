@@ -200,8 +200,10 @@ class ShardedMassOperator:
         dev = self.op._dev
         self.d_cells = torch.from_numpy(self.shard.cells).to(dev)
         # vertex-column layouts: sequential strips over the rank's block
+        from .kernels import _STRIPRED_LAYOUTS
         self.strips = (self.op._global_strips(cells=self.shard.cells)
-                       if self.op.strip_ok and self.op.kron_ok else None)
+                       if tuple(fs.layout.delta6()) in _STRIPRED_LAYOUTS and
+                       self.op.kron_ok else None)
         self.halo = HaloExchange(fs, self.shard, device=dev)
         self._lib = _lib
 
@@ -223,7 +225,8 @@ class ShardedMassOperator:
             self._lib.column_mass_strip_red(
                 op.fs.layout, op.k, op.layers, coords_window, op.mref,
                 x_window, y_window, hi - lo, strips, op.kron, W,
-                accumulate=True, x_base=lo, y_base=lo, coords_base=clo)
+                accumulate=True, x_base=lo, y_base=lo, coords_base=clo,
+                n_vertices=op.fs.mesh.base.num_vertices)
         else:
             self._lib.column_mass(
                 op.fs.layout, op.k, op.n_cells, op.layers, op.cmap, op.offs,

@@ -133,8 +133,10 @@ SCHEDULES = ("auto", "atomic", "colored", "column", "patch", "strip",
 def _schedule_applies(lname, schedule):
     if schedule == "patch":
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "P2xP2", "VP1")
-    if schedule in ("strip", "stripred"):
+    if schedule == "strip":
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1")
+    if schedule == "stripred":
+        return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1", "P2xP2")
     return True
 
 
@@ -384,7 +386,8 @@ def test_strip_chunk_widths(lname, W, layers):
     assert _rel(y, ref) <= 1e-10
 
 
-@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1", "CG1xDG1", "CG1xDG0"))
+@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1", "CG1xDG1", "CG1xDG0",
+                                   "P2xP2"))
 @pytest.mark.parametrize("layers", (1, 5, 16, 33, 64))
 def test_stripred_layers(lname, layers):
     from paper_1604_05937_b200 import configs, extrude_coordinates

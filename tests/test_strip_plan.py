@@ -145,3 +145,28 @@ def test_global_strips_invariants(n, ordering, max_len):
             win[k % 3] = v            # the oldest slot is replaced
             seen.append(key[tuple(sorted(win))])
     assert sorted(seen) == list(range(base.num_cells))
+
+
+@pytest.mark.parametrize("n,ordering,max_len", ((6, "rcm", 64), (12, "random", 7)))
+def test_global_strip_edges(n, ordering, max_len):
+    """Edge slot a always holds the edge opposite window vertex a."""
+    from paper_1604_05937_b200 import _lib
+    from paper_1604_05937_b200.configs import base_mesh
+    base, _ = base_mesh(n, ordering, 0.2)
+    sp, st, se = _lib.build_global_strips(base, max_len, edges=True)
+    ev = base.edge_vertices
+    for s in range(len(sp) - 1):
+        win, ewin = [None] * 3, [None] * 3
+        for k in range(sp[s], sp[s + 1]):
+            i = k - sp[s]
+            a = i % 3
+            win[a] = int(st[k])
+            if i < 3:
+                ewin[a] = int(se[k, 0])
+            else:
+                ewin[(a + 1) % 3] = int(se[k, 0])
+                ewin[(a + 2) % 3] = int(se[k, 1])
+            if i >= 2:
+                for b in range(3):
+                    others = {win[(b + 1) % 3], win[(b + 2) % 3]}
+                    assert set(ev[ewin[b]].tolist()) == others
