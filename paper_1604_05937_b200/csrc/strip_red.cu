@@ -206,16 +206,15 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         }
         kron_apply<LY>(M, xv, det, yv);
         // steps past this segment's strip see stale ring data (possibly
-        // NaN): never let them touch the live accumulators
-        if (act) {
+        // NaN): select it away without branching
 #pragma unroll
-          for (int j = 0; j < K; ++j) {
-            const int a = T.pos[j];
-            if (T.level[j] == 2)
-              at[a][T.ch[j]] += yv[j];
-            else
-              ab[a][T.ch[j]] += yv[j];
-          }
+        for (int j = 0; j < K; ++j) {
+          const int a = T.pos[j];
+          const double v = act ? yv[j] : 0.0;
+          if (T.level[j] == 2)
+            at[a][T.ch[j]] += v;
+          else
+            ab[a][T.ch[j]] += v;
         }
       };
       using S0 = std::integral_constant<int, 0>;
@@ -498,7 +497,10 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
           xv[j] = T.level[j] == 2 ? et[p - 3][T.ch[j]] : eb[p - 3][T.ch[j]];
       }
       kron_apply<LY>(M, xv, det, yv);
-      if (!act) return; // stale ring data past the strip's end
+      // stale ring data past the strip's end (possibly NaN): select, no
+      // branch, so the step stays convergent
+#pragma unroll
+      for (int j = 0; j < K; ++j) yv[j] = act ? yv[j] : 0.0;
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         const int p = T.pos[j];
