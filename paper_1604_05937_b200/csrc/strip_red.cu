@@ -68,6 +68,13 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t col = (int64_t)layers * CH + LV; // vertex column length
   const int64_t ccol = 3 * (int64_t)(layers + 1);
+  {
+    extern __shared__ double sr_ring[];
+    constexpr int ESZ = sr_entry<LY, W>();
+    double *z = sr_ring + (size_t)8 * kSrDepth * SEGS * ESZ;
+    for (int i = threadIdx.x; i < ESZ; i += blockDim.x) z[i] = 0.0;
+    __syncthreads();
+  }
 
   // work item = (strip, layer chunk), chunk fastest: the chunks of a strip
   // run side by side, so the sectors two chunks of a vertex column share
@@ -113,6 +120,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       constexpr int ES = sr_entry<LY, W>();
       extern __shared__ double sr_ring[];
       double *ring = sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
+      const double *sr_zero = sr_ring + (size_t)8 * kSrDepth * SEGS * ES;
       auto entry = [&](int slot) {
         return ring + (size_t)(slot * SEGS + seg) * ES;
       };
@@ -174,7 +182,9 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         sr_wait<kSrDepth - 1>(); // this lane's copies of step k landed
         __syncwarp();            // ... and the other lanes' ones
         const int64_t vcol = (int64_t)rv[A];
-        const double *e = entry(A);
+        // steps past this segment's strip read a zero block instead of the
+        // (stale, possibly non-finite) ring slot: their contribution is 0
+        const double *e = act ? entry(A) : sr_zero;
 #pragma unroll
         for (int c = 0; c < CH; ++c) fb[A][c] = e[sl * CH + c];
 #pragma unroll
@@ -205,16 +215,13 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
           xv[j] = T.level[j] == 2 ? ft[a][T.ch[j]] : fb[a][T.ch[j]];
         }
         kron_apply<LY>(M, xv, det, yv);
-        // steps past this segment's strip see stale ring data (possibly
-        // NaN): select it away without branching
 #pragma unroll
         for (int j = 0; j < K; ++j) {
           const int a = T.pos[j];
-          const double v = act ? yv[j] : 0.0;
           if (T.level[j] == 2)
-            at[a][T.ch[j]] += v;
+            at[a][T.ch[j]] += yv[j];
           else
-            ab[a][T.ch[j]] += v;
+            ab[a][T.ch[j]] += yv[j];
         }
       };
       using S0 = std::integral_constant<int, 0>;
@@ -248,7 +255,7 @@ static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
   const unsigned grid = grid_for(warps * 32, 256, 8);
 #define PM_SR(WW)                                                            \
   do {                                                                       \
-    const size_t smem = sizeof(double) * 8 * kSrDepth * (32 / WW) *          \
+    const size_t smem = sizeof(double) * (8 * kSrDepth * (32 / WW) + 1) *    \
                         sr_entry<LY, WW>();                                  \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
         k_strip_red<LY, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
@@ -310,6 +317,10 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
   extern __shared__ double sr_ring[];
   double *ring =
       sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
+  const double *sr_zero = sr_ring + (size_t)8 * kSrDepth * SEGS * ES;
+  for (int i = threadIdx.x; i < ES; i += blockDim.x)
+    sr_ring[(size_t)8 * kSrDepth * SEGS * ES + i] = 0.0;
+  __syncthreads();
 
   const int n_chunks = (layers + W - 1) / W;
   const int64_t n_items = n_strips * n_chunks;
@@ -458,7 +469,8 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
       const bool act = k < len;
       sr_wait<kSrDepth - 1>();
       __syncwarp();
-      const double *en = entry(A);
+      // past the strip's end: read the zero block (contribution exactly 0)
+      const double *en = act ? entry(A) : sr_zero;
 #pragma unroll
       for (int c = 0; c < CH0; ++c) vb[A][c] = en[sl * CH0 + c];
 #pragma unroll
@@ -497,10 +509,6 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
           xv[j] = T.level[j] == 2 ? et[p - 3][T.ch[j]] : eb[p - 3][T.ch[j]];
       }
       kron_apply<LY>(M, xv, det, yv);
-      // stale ring data past the strip's end (possibly NaN): select, no
-      // branch, so the step stays convergent
-#pragma unroll
-      for (int j = 0; j < K; ++j) yv[j] = act ? yv[j] : 0.0;
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         const int p = T.pos[j];
@@ -560,8 +568,8 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
   const unsigned grid = grid_for(warps * 32, 256, 4);
 #define PM_SRE(WW)                                                           \
   do {                                                                       \
-    const size_t smem =                                                      \
-        sizeof(double) * 8 * kSrDepth * (32 / WW) * sre_entry<LY, WW>();     \
+    const size_t smem = sizeof(double) * (8 * kSrDepth * (32 / WW) + 1) *    \
+                        sre_entry<LY, WW>();                                 \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
         k_strip_red_e<LY, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
         (int)smem));                                                         \
