@@ -325,7 +325,7 @@ def strip_max_len(n_cells: int, layers: int) -> int:
     """Strip length cap: long strips amortise the 3-vertex fill, but small
     meshes need enough (strip, chunk) items to fill 148 SMs."""
     chunks = -(-layers // strip_chunk_width(layers))
-    return int(max(4, min(32, n_cells * chunks // 24000)))
+    return int(max(4, min(32, n_cells * chunks // 12000)))
 
 
 _COLORINGS = {}
