@@ -16,8 +16,8 @@ CPU execution path).
 Schedules (``schedule=``):
 
 ``"auto"``      DG (2,1) fields in overwrite mode: ``"stream"``; CG
-                fields on vertex/edge columns: ``"patch"``; otherwise
-                ``"column"``.
+                fields on vertex (P1, 3-vector P1, CG1xDGk) or vertex + edge
+                (P2) columns: ``"stripred"``; otherwise ``"column"``.
 ``"patch"``     owner-computes over compact patches, shared-memory
                 accumulation, no atomics, deterministic (schedule.py).
 ``"stripred"``  vertex-column layouts: global sequential strips, one
