@@ -24,6 +24,7 @@
  *   pm_build_strips          <- host planner of that schedule
  *   pm_column_mass_strip_red <- same, global strips + REDG
  *   pm_build_global_strips   <- host planner of that schedule
+ *   pm_column_mass_strip_bulk<- same, TMA bulk-copy prefetch
  *   pm_column_probe          <- SPEC.md:338-340 counting / gather kernels
  *                               (verification.py:47-75 materialized maps)
  *   pm_halo_pack / _unpack   <- PAPER.md:770-775 (halo exchange between
@@ -165,6 +166,20 @@ int pm_column_mass_strip_red(const int32_t *delta6, int32_t k, int32_t layers,
                              const int32_t *steps,
                              const int32_t *steps_e /* P2: 2 edges/step */,
                              int64_t n_vertices, void *stream);
+
+/* The same schedule with TMA bulk-copy prefetch (one lane per segment issues
+ * cp.async.bulk copies completing on per-slot mbarriers).  x/y hold global
+ * DoF indices [x_lo, x_hi) (y has the same numbering), coords [c_lo, c_hi);
+ * accumulate = 0 zeroes y[x_lo:x_hi] first. */
+int pm_column_mass_strip_bulk(const int32_t *delta6, int32_t k,
+                              int32_t layers, const double *coords,
+                              const double *mref, const double *mtri,
+                              const double *mline, const double *x, double *y,
+                              int64_t x_lo, int64_t x_hi, int64_t c_lo,
+                              int64_t c_hi, int32_t accumulate,
+                              int64_t n_strips, int32_t chunk,
+                              const int32_t *strip_ptr, const int32_t *steps,
+                              void *stream);
 
 /* --- probes for the par-loop itself (exact integer checks) -------------
  * mode 0: out_i64[(c*layers+l)*k + j] = cell_map[c*k+j] + l*offsets[j]

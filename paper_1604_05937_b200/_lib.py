@@ -68,6 +68,13 @@ SIGNATURES = {
                                                 ctypes.POINTER(_f64), _vp,
                                                 _vp, _i64, _i32, _i64, _i32,
                                                 _vp, _vp, _vp, _i64, _vp]),
+    "pm_column_mass_strip_bulk": (ctypes.c_int, [_i32p, _i32, _i32, _vp,
+                                                 ctypes.POINTER(_f64),
+                                                 ctypes.POINTER(_f64),
+                                                 ctypes.POINTER(_f64), _vp,
+                                                 _vp, _i64, _i64, _i64, _i64,
+                                                 _i32, _i64, _i32, _vp, _vp,
+                                                 _vp]),
     "pm_build_global_strips": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp,
                                               _i32, _vp, _vp, _vp, _vp]),
     "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
@@ -333,6 +340,24 @@ def column_mass_strip_red(layout, k, layers, coords, mref, x, y, n_dofs,
         _f64ptr(m), _f64ptr(mt), _f64ptr(ml), ptr(x, x_base), ptr(y, y_base),
         n_dofs, 1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp),
         ptr(st), ptr(se), n_vertices, stream_ptr(stream))
+    check(rc)
+
+
+def column_mass_strip_bulk(layout, k, layers, coords, mref, x, y, x_range,
+                           c_range, strips, kron, chunk, accumulate=False,
+                           stream=None, x_base=0, coords_base=0):
+    """pm_column_mass_strip_bulk (vertex layouts): TMA-prefetched strips."""
+    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
+    ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
+    d = layout.delta6()
+    sp, st = strips[0], strips[1]
+    rc = host_lib().pm_column_mass_strip_bulk(
+        d.ctypes.data_as(_i32p), k, layers, ptr(coords, coords_base),
+        _f64ptr(m), _f64ptr(mt), _f64ptr(ml), ptr(x, x_base), ptr(y, x_base),
+        x_range[0], x_range[1], c_range[0], c_range[1],
+        1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp), ptr(st),
+        stream_ptr(stream))
     check(rc)
 
 

@@ -90,5 +90,9 @@ int launch_generic(const LoopArgs &a, bool atomic, int64_t cl_begin);
 int launch_dg_stream(const LoopArgs &a, bool *handled);
 int launch_column(const LoopArgs &a, const int32_t *delta6, bool colored);
 bool column_supports(const int32_t *delta6);
+int launch_strip_bulk(const LoopArgs &a, const int32_t *delta6,
+                      const int32_t *strip_ptr, const int32_t *steps,
+                      int64_t n_strips, int W, int64_t x_lo, int64_t x_hi,
+                      int64_t c_lo, int64_t c_hi);
 
 } // namespace pm

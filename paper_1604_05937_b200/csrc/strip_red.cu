@@ -19,6 +19,7 @@
 // One vertex load and one partial flush per cell instead of three gathers
 // and three scatters per cell-layer.  Needs y zeroed first (overwrite mode).
 #include "column_layout.cuh"
+#include "pm_ptx.cuh"
 
 #include <type_traits>
 
@@ -37,11 +38,25 @@ template <int N> __device__ __forceinline__ void sr_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+__device__ __forceinline__ void sr_mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
 // ring entry per segment: the vertex's chunk of the field column
 // (W*CH + LV values) and of the coordinate column (3*(W+1) values)
 template <class LY, int W> constexpr int sr_fs() { return W * LY::CH0 + LY::LV0; }
 template <class LY, int W> constexpr int sr_entry() {
   return sr_fs<LY, W>() + 3 * (W + 1);
+}
+// bulk (TMA) ring entries: both parts start 16-byte aligned and leave room
+// for the 8-byte alignment shift and the rounding to 16-byte sizes
+template <class LY, int W> constexpr int srb_fpart() {
+  return ((sr_fs<LY, W>() + 3) / 2) * 2;
+}
+template <class LY, int W> constexpr int srb_entry() {
+  return srb_fpart<LY, W>() + ((3 * (W + 1) + 3) / 2) * 2;
 }
 constexpr int kSrDepth = 3; // steps in flight per segment
 

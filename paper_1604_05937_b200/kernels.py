@@ -227,6 +227,14 @@ class MassOperator:
                     f"the strip schedule needs a vertex-column layout, got "
                     f"{self.fs.layout.name}")
             strips, W = self._global_strips()
+            import os
+            if os.environ.get("PM_STRIP_BULK", "0") == "1" and \
+                    len(strips) == 2:
+                _lib.column_mass_strip_bulk(
+                    self.fs.layout, self.k, self.layers, coords, self.mref,
+                    x, y, (0, n), (0, self.coord_fs.total_dofs), strips,
+                    self.kron, W, accumulate=accumulate, stream=stream)
+                return y
             _lib.column_mass_strip_red(self.fs.layout, self.k, self.layers,
                                        coords, self.mref, x, y, n, strips,
                                        self.kron, W, accumulate=accumulate,
