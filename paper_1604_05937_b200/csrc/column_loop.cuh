@@ -12,6 +12,17 @@ template <int K> struct MassMat {
   double m[K * K]; // reference-prism mass matrix, row-major, slot order
 };
 
+// The same |det J| from per-vertex mid-layer positions and heights
+// (xm_a, ym_a, dz_a), identical operation order.
+__device__ __forceinline__ double
+prism_abs_detj_mid(double xm0, double ym0, double dz0, double xm1, double ym1,
+                   double dz1, double xm2, double ym2, double dz2) {
+  const double a2 = (xm1 - xm0) * (ym2 - ym0) - (xm2 - xm0) * (ym1 - ym0);
+  constexpr double kThird = 1.0 / 3.0;
+  const double h = (dz0 + dz1 + dz2) * kThird;
+  return fabs(a2 * h);
+}
+
 // Reference-prism mass matrix as the tensor product of its triangle and
 // interval factors: Mref[(c,h,v),(c,h',v')] = Mtri[h][h'] * Mline[v][v'].
 struct KronMat {

@@ -62,7 +62,7 @@ constexpr int kSrDepth = 3; // steps in flight per segment
 
 // 3-vector windows need more registers: one CTA per SM there
 template <class LY> constexpr int sr_min_blocks() {
-  return LY::CH0 > 2 ? 1 : 2;
+  return LY::CH0 > 2 ? 1 : 3; // scalar windows fit 85 registers
 }
 
 template <class LY, int W, int K = LY::K>
@@ -111,7 +111,9 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       const int nl = has ? min(W, layers - l0) : 0;
       const int l = l0 + sl;
       const bool lane_ok = sl < nl;
-      double fb[3][CH], ft[3][LVA], cb[3][3], ct[3][3];
+      // window vertex: field at l (CH) and l+1 (LV) and the geometry the
+      // Jacobian needs, derived once on entry: xm, ym (mid-layer), dz
+      double fb[3][CH], ft[3][LVA], gm[3][3];
       double ab[3][CH], at[3][LVA];
       int64_t vo[3] = {0, 0, 0}; // field column origin of the window slot
       bool live[3] = {false, false, false};
@@ -122,7 +124,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
 #pragma unroll
         for (int c = 0; c < LVA; ++c) ft[a][c] = 0.0, at[a][c] = 0.0;
 #pragma unroll
-        for (int q = 0; q < 3; ++q) cb[a][q] = 0.0, ct[a][q] = 0.0;
+        for (int q = 0; q < 3; ++q) gm[a][q] = 0.0;
       }
       // vertex ids of the strip, W at a time (lane sl holds step base+sl)
       int vbuf = (has && sl < len) ? __ldg(steps + k0 + sl) : 0;
@@ -204,10 +206,11 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         for (int c = 0; c < CH; ++c) fb[A][c] = e[sl * CH + c];
 #pragma unroll
         for (int c = 0; c < LV; ++c) ft[A][c] = e[(sl + 1) * CH + c];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          cb[A][q] = e[FS + 3 * sl + q];
-          ct[A][q] = e[FS + 3 * (sl + 1) + q];
+        {
+          const double *g = e + FS + 3 * sl;
+          gm[A][0] = 0.5 * (g[0] + g[3]); // same operations as
+          gm[A][1] = 0.5 * (g[1] + g[4]); // prism_abs_detj
+          gm[A][2] = g[5] - g[2];
         }
         __syncwarp(); // reads done before the slot is refilled
         vo[A] = vcol * col;
@@ -215,14 +218,12 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         // refill ring slot A with the step kSrDepth ahead
         rv[A] = fetch(k + kSrDepth, A);
         if (k < 2) return; // window not full yet
-        double X[6], Y[6], Z[6];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          X[2 * a] = cb[a][0], Y[2 * a] = cb[a][1], Z[2 * a] = cb[a][2];
-          X[2 * a + 1] = ct[a][0], Y[2 * a + 1] = ct[a][1];
-          Z[2 * a + 1] = ct[a][2];
-        }
-        const double det = (act && lane_ok) ? prism_abs_detj(X, Y, Z) : 0.0;
+        const double det =
+            (act && lane_ok)
+                ? prism_abs_detj_mid(gm[0][0], gm[0][1], gm[0][2], gm[1][0],
+                                     gm[1][1], gm[1][2], gm[2][0], gm[2][1],
+                                     gm[2][2])
+                : 0.0;
         double xv[K], yv[K];
 #pragma unroll
         for (int j = 0; j < K; ++j) {
