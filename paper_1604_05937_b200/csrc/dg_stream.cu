@@ -17,17 +17,17 @@
 
 namespace pm {
 
-constexpr int kStreamT = 256;  // cell-layers per unit (= threads per CTA)
+constexpr int kStreamT = 256;  // default cell-layers per unit (threads/CTA)
 
-// S pipeline stages, MINB resident CTAs per SM (register budget)
-template <int D, int S, int MINB>
-__global__ void __launch_bounds__(kStreamT, MINB)
+// S pipeline stages, MINB resident CTAs per SM (register budget), T
+// cell-layers per unit (= threads per CTA)
+template <int D, int S, int MINB, int T = kStreamT>
+__global__ void __launch_bounds__(T, MINB)
 k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
             const int32_t *__restrict__ xmap,
             const int32_t *__restrict__ xoff,
             const double *__restrict__ coords,
             const double *__restrict__ x, double *__restrict__ y) {
-  constexpr int T = kStreamT;
   constexpr uint32_t BYTES = T * D * sizeof(double);
   extern __shared__ __align__(128) unsigned char smem[];
   double *buf = reinterpret_cast<double *>(smem);
@@ -184,21 +184,21 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
   if (t == 0) bulk_wait<0>();
 }
 
-template <int D, int S, int MINB>
+template <int D, int S, int MINB, int T = kStreamT>
 static int dg_stream_launch(const LoopArgs &a, const MassMat<D> &M,
                             int64_t n_units) {
-  const size_t smem = S * kStreamT * D * sizeof(double) + S * sizeof(uint64_t);
-  auto kern = k_dg_stream<D, S, MINB>;
+  const size_t smem = S * T * D * sizeof(double) + S * sizeof(uint64_t);
+  auto kern = k_dg_stream<D, S, MINB, T>;
   PM_CUDA_TRY(cudaFuncSetAttribute(
       kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   PM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
-                                                            kStreamT, smem));
+                                                            T, smem));
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sm_count() * per_sm;
   if (grid > n_units) grid = n_units;
-  kern<<<(unsigned)grid, kStreamT, smem, a.s>>>(M, n_units, a.layers, a.xmap,
-                                                a.xoff, a.coords, a.x, a.y);
+  kern<<<(unsigned)grid, T, smem, a.s>>>(M, n_units, a.layers, a.xmap,
+                                         a.xoff, a.coords, a.x, a.y);
   PM_LAUNCH_CHECK("k_dg_stream");
   return PM_OK;
 }
@@ -218,7 +218,9 @@ static int stream_cfg() {
 template <int D> static int dg_stream_k(const LoopArgs &a, bool *handled) {
   *handled = false;
   const int64_t n_cl = a.n_cells * (int64_t)a.layers;
-  const int64_t n_units = n_cl / kStreamT;
+  const int cfg = stream_cfg();
+  const int T = cfg == 2 ? 128 : cfg == 3 ? 512 : kStreamT;
+  const int64_t n_units = n_cl / T;
   if ((reinterpret_cast<uintptr_t>(a.x) | reinterpret_cast<uintptr_t>(a.y)) &
       15)
     return PM_OK; // not aligned for bulk copies: caller picks another kernel
@@ -226,14 +228,18 @@ template <int D> static int dg_stream_k(const LoopArgs &a, bool *handled) {
   MassMat<D> M;
   for (int i = 0; i < D * D; ++i) M.m[i] = a.mref[i];
   if (n_units > 0) {
-    const int rc = stream_cfg() == 1 ? dg_stream_launch<D, 8, 2>(a, M, n_units)
-                                     : dg_stream_launch<D, 6, 3>(a, M, n_units);
+    int rc;
+    switch (cfg) {
+    case 0: rc = dg_stream_launch<D, 6, 3>(a, M, n_units); break;
+    case 2: rc = dg_stream_launch<D, 8, 4, 128>(a, M, n_units); break;
+    case 3: rc = dg_stream_launch<D, 4, 1, 512>(a, M, n_units); break;
+    default: rc = dg_stream_launch<D, 8, 2>(a, M, n_units); break;
+    }
     if (rc) return rc;
   }
   *handled = true;
   // ragged tail (< one unit): flattened generic kernel, plain stores
-  if (n_units * kStreamT < n_cl)
-    return launch_generic(a, false, n_units * kStreamT);
+  if (n_units * T < n_cl) return launch_generic(a, false, n_units * T);
   return PM_OK;
 }
 
