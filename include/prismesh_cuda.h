@@ -25,6 +25,7 @@
  *   pm_column_mass_strip_red <- same, global strips + REDG
  *   pm_build_global_strips   <- host planner of that schedule
  *   pm_column_mass_strip_bulk<- same, TMA bulk-copy prefetch
+ *   pm_column_mass_dg_range  <- the DG loop over a cell range (pipelining)
  *   pm_column_probe          <- SPEC.md:338-340 counting / gather kernels
  *                               (verification.py:47-75 materialized maps)
  *   pm_halo_pack / _unpack   <- PAPER.md:770-775 (halo exchange between
@@ -180,6 +181,17 @@ int pm_column_mass_strip_bulk(const int32_t *delta6, int32_t k,
                               int64_t n_strips, int32_t chunk,
                               const int32_t *strip_ptr, const int32_t *steps,
                               void *stream);
+
+/* DG (2,1) fields: the stream kernel over the cell range
+ * [cell_begin, cell_end) only (cell_begin*layers a multiple of 256); y is
+ * overwritten there.  Used to pipeline host<->device copies with compute. */
+int pm_column_mass_dg_range(const int32_t *delta6, int32_t k,
+                            int64_t cell_begin, int64_t cell_end,
+                            int32_t layers, const int32_t *cell_map,
+                            const int32_t *offsets, const int32_t *coord_map,
+                            const int32_t *coord_offsets, const double *coords,
+                            const double *mref, const double *x, double *y,
+                            void *stream);
 
 /* --- probes for the par-loop itself (exact integer checks) -------------
  * mode 0: out_i64[(c*layers+l)*k + j] = cell_map[c*k+j] + l*offsets[j]

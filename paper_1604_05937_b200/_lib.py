@@ -75,6 +75,10 @@ SIGNATURES = {
                                                  _vp, _i64, _i64, _i64, _i64,
                                                  _i32, _i64, _i32, _vp, _vp,
                                                  _vp]),
+    "pm_column_mass_dg_range": (ctypes.c_int, [_i32p, _i32, _i64, _i64, _i32,
+                                               _vp, _vp, _vp, _vp, _vp,
+                                               ctypes.POINTER(_f64), _vp,
+                                               _vp, _vp]),
     "pm_build_global_strips": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp,
                                               _i32, _vp, _vp, _vp, _vp]),
     "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
@@ -359,6 +363,16 @@ def column_mass_strip_bulk(layout, k, layers, coords, mref, x, y, x_range,
         1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp), ptr(st),
         stream_ptr(stream))
     check(rc)
+
+
+def column_mass_dg_range(layout, k, c0, c1, layers, cmap, offs, xmap, xoffs,
+                         coords, mref, x, y, stream=None):
+    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    d = layout.delta6()
+    check(host_lib().pm_column_mass_dg_range(
+        d.ctypes.data_as(_i32p), k, c0, c1, layers, ptr(cmap), ptr(offs),
+        ptr(xmap), ptr(xoffs), ptr(coords), _f64ptr(m), ptr(x), ptr(y),
+        stream_ptr(stream)))
 
 
 def greedy_color_cells(cell_vertices, vc_offsets, vc_cells):

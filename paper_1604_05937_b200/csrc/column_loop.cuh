@@ -98,7 +98,8 @@ __device__ __forceinline__ void kron_apply(const KronMat &M, const double *xv,
 
 // Kernel launchers (one translation unit each).
 int launch_generic(const LoopArgs &a, bool atomic, int64_t cl_begin);
-int launch_dg_stream(const LoopArgs &a, bool *handled);
+int launch_dg_stream(const LoopArgs &a, bool *handled, int64_t cl_begin = 0);
+constexpr int kStreamT = 256; // cell-layers per DG stream unit (default)
 int launch_column(const LoopArgs &a, const int32_t *delta6, bool colored);
 bool column_supports(const int32_t *delta6);
 int launch_strip_bulk(const LoopArgs &a, const int32_t *delta6,

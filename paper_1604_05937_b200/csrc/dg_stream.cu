@@ -17,13 +17,12 @@
 
 namespace pm {
 
-constexpr int kStreamT = 256;  // default cell-layers per unit (threads/CTA)
 
 // S pipeline stages, MINB resident CTAs per SM (register budget), T
 // cell-layers per unit (= threads per CTA)
 template <int D, int S, int MINB, int T = kStreamT>
 __global__ void __launch_bounds__(T, MINB)
-k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
+k_dg_stream(const MassMat<D> M, int64_t n_units, int64_t cl_begin, int layers,
             const int32_t *__restrict__ xmap,
             const int32_t *__restrict__ xoff,
             const double *__restrict__ coords,
@@ -54,7 +53,7 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
     for (int64_t i = 0; i < S - 1 && i < n_mine; ++i) {
       const int64_t u = first + i * stride;
       mbar_arrive_expect_tx(&bar[i], BYTES);
-      bulk_g2s(buf + i * T * D, x + u * T * D, BYTES, &bar[i]);
+      bulk_g2s(buf + i * T * D, x + (cl_begin + u * T) * D, BYTES, &bar[i]);
     }
   }
 
@@ -71,7 +70,7 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
     int l;
   };
   auto where = [&](int64_t u) {
-    const uint32_t g = (uint32_t)(u * T + t);
+    const uint32_t g = (uint32_t)(cl_begin + u * T + t);
     const uint32_t c = g / (uint32_t)layers;
     return Where{c, (int)(g - c * (uint32_t)layers)};
   };
@@ -159,7 +158,7 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
     fence_proxy_async_smem();
     __syncthreads();
     if (t == 0) {
-      bulk_s2g(y + u * T * D, b, BYTES);
+      bulk_s2g(y + (cl_begin + u * T) * D, b, BYTES);
       bulk_commit();
       const int64_t nxt = i + S - 1;
       if (nxt < n_mine) {
@@ -167,7 +166,8 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
         bulk_wait_read<1>();
         const int sn = (int)(nxt % S);
         mbar_arrive_expect_tx(&bar[sn], BYTES);
-        bulk_g2s(buf + sn * T * D, x + (first + nxt * stride) * T * D, BYTES,
+        bulk_g2s(buf + sn * T * D,
+                 x + (cl_begin + (first + nxt * stride) * T) * D, BYTES,
                  &bar[sn]);
       }
     }
@@ -186,7 +186,7 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int layers,
 
 template <int D, int S, int MINB, int T = kStreamT>
 static int dg_stream_launch(const LoopArgs &a, const MassMat<D> &M,
-                            int64_t n_units) {
+                            int64_t n_units, int64_t cl_begin) {
   const size_t smem = S * T * D * sizeof(double) + S * sizeof(uint64_t);
   auto kern = k_dg_stream<D, S, MINB, T>;
   PM_CUDA_TRY(cudaFuncSetAttribute(
@@ -197,8 +197,8 @@ static int dg_stream_launch(const LoopArgs &a, const MassMat<D> &M,
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sm_count() * per_sm;
   if (grid > n_units) grid = n_units;
-  kern<<<(unsigned)grid, T, smem, a.s>>>(M, n_units, a.layers, a.xmap,
-                                         a.xoff, a.coords, a.x, a.y);
+  kern<<<(unsigned)grid, T, smem, a.s>>>(M, n_units, cl_begin, a.layers,
+                                         a.xmap, a.xoff, a.coords, a.x, a.y);
   PM_LAUNCH_CHECK("k_dg_stream");
   return PM_OK;
 }
@@ -215,9 +215,12 @@ static int stream_cfg() {
   return cfg;
 }
 
-template <int D> static int dg_stream_k(const LoopArgs &a, bool *handled) {
+// cell-layers [cl_begin, n_cells*layers) of the DG field (cl_begin must be
+// a multiple of the unit size so the bulk copies stay 16-byte aligned)
+template <int D>
+static int dg_stream_k(const LoopArgs &a, bool *handled, int64_t cl_begin) {
   *handled = false;
-  const int64_t n_cl = a.n_cells * (int64_t)a.layers;
+  const int64_t n_cl = a.n_cells * (int64_t)a.layers - cl_begin;
   const int cfg = stream_cfg();
   const int T = cfg == 2 ? 128 : cfg == 3 ? 512 : kStreamT;
   const int64_t n_units = n_cl / T;
@@ -230,25 +233,30 @@ template <int D> static int dg_stream_k(const LoopArgs &a, bool *handled) {
   if (n_units > 0) {
     int rc;
     switch (cfg) {
-    case 0: rc = dg_stream_launch<D, 6, 3>(a, M, n_units); break;
-    case 2: rc = dg_stream_launch<D, 8, 4, 128>(a, M, n_units); break;
-    case 3: rc = dg_stream_launch<D, 4, 1, 512>(a, M, n_units); break;
-    default: rc = dg_stream_launch<D, 8, 2>(a, M, n_units); break;
+    case 0: rc = dg_stream_launch<D, 6, 3>(a, M, n_units, cl_begin); break;
+    case 2:
+      rc = dg_stream_launch<D, 8, 4, 128>(a, M, n_units, cl_begin);
+      break;
+    case 3:
+      rc = dg_stream_launch<D, 4, 1, 512>(a, M, n_units, cl_begin);
+      break;
+    default: rc = dg_stream_launch<D, 8, 2>(a, M, n_units, cl_begin); break;
     }
     if (rc) return rc;
   }
   *handled = true;
   // ragged tail (< one unit): flattened generic kernel, plain stores
-  if (n_units * T < n_cl) return launch_generic(a, false, n_units * T);
+  if (n_units * T < n_cl)
+    return launch_generic(a, false, cl_begin + n_units * T);
   return PM_OK;
 }
 
-int launch_dg_stream(const LoopArgs &a, bool *handled) {
+int launch_dg_stream(const LoopArgs &a, bool *handled, int64_t cl_begin) {
   switch (a.k) {
-  case 1: return dg_stream_k<1>(a, handled);
-  case 2: return dg_stream_k<2>(a, handled);
-  case 3: return dg_stream_k<3>(a, handled);
-  case 6: return dg_stream_k<6>(a, handled);
+  case 1: return dg_stream_k<1>(a, handled, cl_begin);
+  case 2: return dg_stream_k<2>(a, handled, cl_begin);
+  case 3: return dg_stream_k<3>(a, handled, cl_begin);
+  case 6: return dg_stream_k<6>(a, handled, cl_begin);
   default:
     *handled = false;
     return PM_OK;
@@ -256,3 +264,56 @@ int launch_dg_stream(const LoopArgs &a, bool *handled) {
 }
 
 } // namespace pm
+
+// DG stream over the cell range [cell_begin, cell_end): the pipelined host
+// path of kernels.mass_action launches one chunk per call.
+extern "C" int pm_column_mass_dg_range(const int32_t *delta6, int32_t k,
+                                       int64_t cell_begin, int64_t cell_end,
+                                       int32_t layers, const int32_t *cell_map,
+                                       const int32_t *offsets,
+                                       const int32_t *coord_map,
+                                       const int32_t *coord_offsets,
+                                       const double *coords,
+                                       const double *mref, const double *x,
+                                       double *y, void *stream) {
+  pm::clear_error();
+  pm::LoopArgs a;
+  int rc = pm::make_slot_table(delta6, &a.st);
+  if (rc) return rc;
+  const bool dg_only = !delta6[0] && !delta6[1] && !delta6[2] &&
+                       !delta6[3] && !delta6[4];
+  if (k != a.st.k || layers < 1 || cell_begin < 0 || cell_end < cell_begin ||
+      !mref || !dg_only) {
+    pm::set_error("bad arguments to pm_column_mass_dg_range");
+    return PM_EINVAL;
+  }
+  if (cell_end == cell_begin) return PM_OK;
+  if (((cell_begin * (int64_t)layers) % pm::kStreamT) != 0) {
+    pm::set_error("cell_begin*layers must be a multiple of %d",
+                  pm::kStreamT);
+    return PM_EINVAL;
+  }
+  a.k = k;
+  a.layers = layers;
+  a.n_cells = cell_end;
+  a.cells = nullptr;
+  a.cmap = cell_map; // the ragged tail (generic kernel) addresses via the map
+  a.coff = offsets;
+  a.xmap = coord_map;
+  a.xoff = coord_offsets;
+  a.coords = coords;
+  a.mref = mref;
+  a.x = x;
+  a.y = y;
+  a.accumulate = 0;
+  a.dg_only = true;
+  a.hshared = false;
+  a.s = (cudaStream_t)stream;
+  bool handled = false;
+  rc = pm::launch_dg_stream(a, &handled, cell_begin * (int64_t)layers);
+  if (!rc && !handled) {
+    pm::set_error("DG range needs 16-byte aligned fields");
+    return PM_EINVAL;
+  }
+  return rc;
+}

@@ -121,6 +121,7 @@ class MassOperator:
         self._patch = None
         self._strip = None
         self._gstrips = None
+        self._hbuf = None
         self._dev = _lib.cuda_device()
         self.cmap = fs.device_cell_map()
         self.offs = fs.device_offsets()
@@ -155,6 +156,58 @@ class MassOperator:
     def strip_ok(self) -> bool:
         d = tuple(self.fs.layout.delta6())
         return d in _STRIP_LAYOUTS
+
+    @property
+    def dg_only(self) -> bool:
+        d = self.fs.layout.delta6()
+        return not (d[0] or d[1] or d[2] or d[3] or d[4])
+
+    def apply_host(self, x_host, coords, y_host, chunks=8):
+        """``y_host = M x_host`` for pinned host tensors, with the copies
+        pipelined against the compute: for DG (2,1) fields the cell columns
+        are contiguous, so chunk j+1 goes up, chunk j is computed and chunk
+        j-1 comes down at the same time (three streams).  Other layouts:
+        one copy each way around the device call."""
+        import torch
+        n = self.fs.total_dofs
+        if self._hbuf is None:
+            self._hbuf = (torch.empty(n, dtype=torch.float64, device=self._dev),
+                          torch.empty(n, dtype=torch.float64, device=self._dev),
+                          torch.cuda.Stream(self._dev),
+                          torch.cuda.Stream(self._dev),
+                          torch.cuda.Stream(self._dev))
+        xd, yd, s_up, s_cmp, s_down = self._hbuf
+        cur = torch.cuda.current_stream()
+        if not (self.dg_only and self.kron_ok and x_host.is_pinned() and
+                y_host.is_pinned()):
+            xd.copy_(x_host, non_blocking=True)
+            self.apply(xd, coords, yd)
+            y_host.copy_(yd, non_blocking=True)
+            cur.synchronize()
+            return y_host
+        L, nc = self.layers, self.n_cells
+        # chunk boundaries on whole DG stream units (256 cell-layers)
+        q = 256 // np.gcd(256, L)
+        per = max(q, -(-nc // chunks // q) * q)
+        bounds = list(range(0, nc, per)) + [nc]
+        dpl = self.k * L                       # DoFs per cell column
+        for s_ in (s_up, s_cmp, s_down):
+            s_.wait_stream(cur)
+        for c0, c1 in zip(bounds[:-1], bounds[1:]):
+            r = slice(c0 * dpl, c1 * dpl)
+            with torch.cuda.stream(s_up):
+                xd[r].copy_(x_host[r], non_blocking=True)
+            s_cmp.wait_stream(s_up)
+            _lib.column_mass_dg_range(self.fs.layout, self.k, c0, c1, L,
+                                      self.cmap, self.offs, self.xmap,
+                                      self.xoffs, coords, self.mref, xd, yd,
+                                      stream=s_cmp)
+            s_down.wait_stream(s_cmp)
+            with torch.cuda.stream(s_down):
+                y_host[r].copy_(yd[r], non_blocking=True)
+        cur.wait_stream(s_down)
+        cur.synchronize()
+        return y_host
 
     def _global_strips(self, cells=None):
         """Sequential strips over the mesh (cached) or over ``cells``."""
@@ -416,8 +469,13 @@ def mass_action(fs, x, coords=None, quadrature=None, schedule="auto",
     if op.fs is not fs:
         raise ValueError("operator was prepared for another space")
     dev = op._dev
-    d_x, x_host = _as_device(x, dev)
     d_c = _coords_device(fs, coords, dev)
+    if (out is not None and isinstance(x, torch.Tensor) and
+            x.device.type == "cpu" and out.device.type == "cpu" and
+            schedule == "auto"):
+        # host in, host out: copies pipelined with the compute
+        return op.apply_host(x, d_c, out)
+    d_x, x_host = _as_device(x, dev)
     y = op.apply(d_x, d_c, schedule=schedule)
     if out is not None:
         out.copy_(y, non_blocking=out.device.type == "cpu" and out.is_pinned())

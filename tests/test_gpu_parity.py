@@ -421,3 +421,25 @@ def test_strip_bulk_variant(lname, layers, monkeypatch):
     coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
     y = op.apply(torch.from_numpy(x).cuda(), coords).cpu().numpy()
     assert _rel(y, _oracle_for(w, fs).assemble(x)) <= 1e-10
+
+
+@pytest.mark.parametrize("lname,layers,n", (("DG1xDG1", 50, 32),
+                                            ("DG1xDG1", 7, 24),
+                                            ("DG0xDG1", 33, 20),
+                                            ("CG1xCG1", 10, 16)))
+def test_host_pipelined_mass_action(lname, layers, n):
+    """mass_action with pinned host buffers (chunked H2D / compute / D2H
+    for DG fields) equals the device path and the oracle."""
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator, mass_action
+    w = configs.Workload("hp", n, layers, lname, quad_degrees(lname))
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    op = MassOperator(fs, quad)
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    got = mass_action(fs, xh, coords, operator=op, out=yh).numpy()
+    dev = op.apply(torch.from_numpy(x).cuda(), coords).cpu().numpy()
+    assert np.array_equal(got, dev)
+    assert _rel(got, _oracle_for(w, fs).assemble(x)) <= _tol(lname)
