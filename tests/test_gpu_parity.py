@@ -441,5 +441,7 @@ def test_host_pipelined_mass_action(lname, layers, n):
     yh = torch.empty_like(xh).pin_memory()
     got = mass_action(fs, xh, coords, operator=op, out=yh).numpy()
     dev = op.apply(torch.from_numpy(x).cuda(), coords).cpu().numpy()
-    assert np.array_equal(got, dev)
+    if lname.startswith("DG"):   # deterministic kernels: bitwise equal
+        assert np.array_equal(got, dev)
+    assert _rel(got, dev) <= _tol(lname)
     assert _rel(got, _oracle_for(w, fs).assemble(x)) <= _tol(lname)

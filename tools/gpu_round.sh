@@ -5,7 +5,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err
 : > gpurun_out/sweep.jsonl
-for cs in "C5b stripred" "C4-CG1xCG1-rcm-L100 stripred"; do
+for cs in "C2 auto"; do
   set -- $cs
   timeout 300 python bench.py --config $1 --schedule $2 --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/sweep.jsonl
 done
