@@ -65,6 +65,11 @@ template <class LY> constexpr int sr_min_blocks() {
   return LY::CH0 > 2 ? 1 : 2; // measured: 3/SM (scalar) and 2/SM (3-vector) slower
 }
 
+// The element kernel split along the window: y = det (Mtri (x) Mline) x.
+// The interval stage z = Mline x only involves one vertex column, so it is
+// applied once when the vertex enters the window (not in each of its three
+// cells); per cell only the triangle stage runs, with det folded into the
+// accumulation: acc[h] = fma(det, sum_g Mtri[h][g] z[g], acc[h]).
 template <class LY, int W, int K = LY::K>
 __global__ void __launch_bounds__(256, sr_min_blocks<LY>())
 k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
@@ -73,16 +78,22 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
             double *__restrict__ y) {
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int SEGS = 32 / W;
-  constexpr typename LY::Tab T = LY::make();
   constexpr int LV = LY::LV0;
   constexpr int CH = LY::CH0;
   constexpr int LVA = LV > 0 ? LV : 1;
+  constexpr int NC = LY::NC, NV = LY::NV, NH = LY::NH;
+  // (component c, interval function v) of a vertex layer block: level
+  // copies bottom fb[c] (v = 0) / top ft[c] (v = 1), or, without level
+  // copies, connecting channel v*NC + c (the slot table of fspace.py)
+  static_assert(NH == 3 && NC * NV == CH + LV, "vertex-column layout");
+  static_assert(LV == 0 || (LV == NC && NV == 2 && CH == LV), "strip layout");
   const int lane = threadIdx.x & 31;
   const int sl = lane % W, seg = lane / W;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t col = (int64_t)layers * CH + LV; // vertex column length
-  const int64_t ccol = 3 * (int64_t)(layers + 1);
+  // column lengths fit 32 bits: a column origin is one IMAD.WIDE
+  const int col = layers * CH + LV; // vertex column length
+  const int ccol = 3 * (layers + 1);
   {
     extern __shared__ double sr_ring[];
     constexpr int ESZ = sr_entry<LY, W>();
@@ -109,20 +120,23 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
     {
       const int nl = has ? min(W, layers - l0) : 0;
-      const int l = l0 + sl;
       const bool lane_ok = sl < nl;
-      // window vertex: field at l (CH) and l+1 (LV) and the geometry the
-      // Jacobian needs, derived once on entry: xm, ym (mid-layer), dz
-      double fb[3][CH], ft[3][LVA], gm[3][3];
-      double ab[3][CH], at[3][LVA];
-      int64_t vo[3] = {0, 0, 0}; // field column origin of the window slot
+      // the lane's element of every column chunk it touches
+      const double *xl = x + (int64_t)l0 * CH + sl;
+      const double *cl0 = coords + 3 * (int64_t)l0 + sl;
+      double *yl = y + ((int64_t)l0 + sl) * CH;
+      // window vertex: interval-stage values z[c][v] at the lane's cell
+      // layer and the geometry the Jacobian needs, derived once on entry:
+      // xm, ym (mid-layer), dz; per-vertex accumulators acc[c][v]
+      double zv[3][NC][NV], gm[3][3], acc[3][NC][NV];
+      double *yc[3] = {yl, yl, yl}; // lane's element of the slot's column
       bool live[3] = {false, false, false};
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
 #pragma unroll
-        for (int c = 0; c < CH; ++c) fb[a][c] = 0.0, ab[a][c] = 0.0;
+        for (int c = 0; c < NC; ++c)
 #pragma unroll
-        for (int c = 0; c < LVA; ++c) ft[a][c] = 0.0, at[a][c] = 0.0;
+          for (int v = 0; v < NV; ++v) zv[a][c][v] = 0.0, acc[a][c][v] = 0.0;
 #pragma unroll
         for (int q = 0; q < 3; ++q) gm[a][q] = 0.0;
       }
@@ -151,19 +165,15 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         }
         const int v = __shfl_sync(FULL, vbuf, (k - vbase) & (W - 1), W);
         if (k < len) {
-          const double *fp = x + (int64_t)v * col + (int64_t)l0 * CH;
-          const double *cp = coords + (int64_t)v * ccol + 3 * (int64_t)l0;
-          double *e = entry(slot);
+          const double *fp = xl + (int64_t)v * col;
+          const double *cp = cl0 + (int64_t)v * ccol;
+          double *e = entry(slot) + sl;
 #pragma unroll
-          for (int r = 0; r < (FS + W - 1) / W; ++r) {
-            const int i = sl + W * r;
-            if (i < fl) sr_cp8(e + i, fp + i);
-          }
+          for (int r = 0; r < (FS + W - 1) / W; ++r)
+            if (sl + W * r < fl) sr_cp8(e + W * r, fp + W * r);
 #pragma unroll
-          for (int r = 0; r < (3 * (W + 1) + W - 1) / W; ++r) {
-            const int i = sl + W * r;
-            if (i < cl) sr_cp8(e + FS + i, cp + i);
-          }
+          for (int r = 0; r < (3 * (W + 1) + W - 1) / W; ++r)
+            if (sl + W * r < cl) sr_cp8(e + FS + W * r, cp + W * r);
         }
         sr_commit(); // one group per step (possibly empty)
         return v;
@@ -173,22 +183,33 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
 
       auto flush = [&](auto A_) {
         constexpr int A = decltype(A_)::value;
+        // back to the vertex column's layer block: bottom / connecting
+        // channels vb, top copies vt
+        double vb[CH], vt[LVA];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            if (LV == 0)
+              vb[v * NC + c] = acc[A][c][v];
+            else if (v == 0)
+              vb[c] = acc[A][c][v];
+            else
+              vt[c < LVA ? c : 0] = acc[A][c][v];
+            acc[A][c][v] = 0.0;
+          }
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
-          double v = ab[A][c];
+          double v = vb[c];
           if (c < LV) {
-            const double below = __shfl_up_sync(FULL, at[A][c], 1, W);
+            const double below = __shfl_up_sync(FULL, vt[c < LV ? c : 0], 1, W);
             if (sl > 0) v += below;
           }
           if (live[A] && lane_ok) {
-            double *yp = y + vo[A] + (int64_t)l * CH + c;
-            atomicAdd(yp, v);
-            if (c < LV && sl == nl - 1) atomicAdd(yp + CH, at[A][c]);
+            atomicAdd(yc[A] + c, v);
+            if (c < LV && sl == nl - 1) atomicAdd(yc[A] + CH + c, vt[c < LV ? c : 0]);
           }
-          ab[A][c] = 0.0;
         }
-#pragma unroll
-        for (int c = 0; c < LVA; ++c) at[A][c] = 0.0;
       };
 
       auto step = [&](auto A_, int k) {
@@ -198,14 +219,14 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         // the vertex of ring slot A (step k) enters window slot A
         sr_wait<kSrDepth - 1>(); // this lane's copies of step k landed
         __syncwarp();            // ... and the other lanes' ones
-        const int64_t vcol = (int64_t)rv[A];
         // steps past this segment's strip read a zero block instead of the
         // (stale, possibly non-finite) ring slot: their contribution is 0
         const double *e = act ? entry(A) : sr_zero;
+        double fb[CH], ft[LVA];
 #pragma unroll
-        for (int c = 0; c < CH; ++c) fb[A][c] = e[sl * CH + c];
+        for (int c = 0; c < CH; ++c) fb[c] = e[sl * CH + c];
 #pragma unroll
-        for (int c = 0; c < LV; ++c) ft[A][c] = e[(sl + 1) * CH + c];
+        for (int c = 0; c < LV; ++c) ft[c] = e[(sl + 1) * CH + c];
         {
           const double *g = e + FS + 3 * sl;
           gm[A][0] = 0.5 * (g[0] + g[3]); // same operations as
@@ -213,8 +234,23 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
           gm[A][2] = g[5] - g[2];
         }
         __syncwarp(); // reads done before the slot is refilled
-        vo[A] = vcol * col;
+        yc[A] = yl + (int64_t)rv[A] * col;
         live[A] = act;
+        // interval stage of the entering vertex
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NV; ++w) {
+              const double xw = LV == 0 ? fb[w * NC + c]
+                                : w == 0 ? fb[c]
+                                         : ft[c < LVA ? c : 0];
+              s = fma(M.l[v * NV + w], xw, s);
+            }
+            zv[A][c][v] = s;
+          }
         // refill ring slot A with the step kSrDepth ahead
         rv[A] = fetch(k + kSrDepth, A);
         if (k < 2) return; // window not full yet
@@ -224,21 +260,19 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
                                      gm[1][1], gm[1][2], gm[2][0], gm[2][1],
                                      gm[2][2])
                 : 0.0;
-        double xv[K], yv[K];
+        // triangle stage, det folded into the accumulation
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const int a = T.pos[j];
-          xv[j] = T.level[j] == 2 ? ft[a][T.ch[j]] : fb[a][T.ch[j]];
-        }
-        kron_apply<LY>(M, xv, det, yv);
+        for (int c = 0; c < NC; ++c)
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const int a = T.pos[j];
-          if (T.level[j] == 2)
-            at[a][T.ch[j]] += yv[j];
-          else
-            ab[a][T.ch[j]] += yv[j];
-        }
+          for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int h = 0; h < 3; ++h) {
+              double s = 0.0;
+#pragma unroll
+              for (int g = 0; g < 3; ++g)
+                s = fma(M.t[h * 3 + g], zv[g][c][v], s);
+              acc[h][c][v] = fma(det, s, acc[h][c][v]);
+            }
       };
       using S0 = std::integral_constant<int, 0>;
       using S1 = std::integral_constant<int, 1>;
