@@ -352,8 +352,11 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
               const double *__restrict__ x, double *__restrict__ y) {
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int SEGS = 32 / W;
-  constexpr typename LY::Tab T = LY::make();
   constexpr int LV0 = LY::LV0, CH0 = LY::CH0, LV1 = LY::LV1, CH1 = LY::CH1;
+  constexpr int NV = LY::NV;
+  static_assert(LY::NH == 6 && LY::NC == 1 && LV0 == 1 && LV1 == 1 &&
+                    CH0 == NV - 1 && CH1 == NV - 1,
+                "P2-type layout: level copies + NV-2 connecting functions");
   constexpr int FS0 = sre_fs0<LY, W>(), FS1 = sre_fs1<LY, W>();
   constexpr int ES = sre_entry<LY, W>();
   constexpr int OC = FS0, OE1 = FS0 + 3 * (W + 1), OE2 = OE1 + FS1;
@@ -361,9 +364,10 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
   const int sl = lane % W, seg = lane / W;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t col0 = (int64_t)layers * CH0 + LV0;
-  const int64_t col1 = (int64_t)layers * CH1 + LV1;
-  const int64_t ccol = 3 * (int64_t)(layers + 1);
+  // column lengths fit 32 bits: a column origin is one IMAD.WIDE
+  const int col0 = layers * CH0 + LV0;
+  const int col1 = layers * CH1 + LV1;
+  const int ccol = 3 * (layers + 1);
   extern __shared__ double sr_ring[];
   double *ring =
       sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
@@ -386,27 +390,29 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
     for (int o = W; o < 32; o <<= 1)
       maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
     const int nl = has ? min(W, layers - l0) : 0;
-    const int l = l0 + sl;
     const bool lane_ok = sl < nl;
     const int fl0 = nl * CH0 + LV0, fl1 = nl * CH1 + LV1, cl = 3 * (nl + 1);
+    // the segment's chunk of every column (copies) and the lane's element
+    // (flushes)
+    const double *xv0 = x + (int64_t)l0 * CH0;
+    const double *xe0 = x + e_start + (int64_t)l0 * CH1;
+    const double *cc0 = coords + 3 * (int64_t)l0;
+    double *yv0 = y + ((int64_t)l0 + sl) * CH0;
+    double *ye0 = y + e_start + ((int64_t)l0 + sl) * CH1;
 
-    // window: vertices (field, coordinates) and edges (field)
-    double vb[3][CH0], vt[3][LV0], cb[3][3], ct[3][3], eb[3][CH1], et[3][LV1];
-    double vab[3][CH0], vat[3][LV0], eab[3][CH1], eat[3][LV1];
-    int64_t vo[3] = {0, 0, 0}, eo[3] = {0, 0, 0};
+    // window: per vertex / edge the interval stage z[v] = (Mline x)[v] at
+    // the lane's cell-layer, per vertex the Jacobian geometry (xm, ym, dz);
+    // accumulators per entity and interval function
+    double zv[3][NV], ze[3][NV], gm[3][3], av[3][NV], ae[3][NV];
+    double *yvc[3] = {yv0, yv0, yv0}, *yec[3] = {ye0, ye0, ye0};
     bool vlive[3] = {false, false, false}, elive[3] = {false, false, false};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
 #pragma unroll
-      for (int c = 0; c < CH0; ++c) vb[a][c] = 0.0, vab[a][c] = 0.0;
+      for (int v = 0; v < NV; ++v)
+        zv[a][v] = 0.0, ze[a][v] = 0.0, av[a][v] = 0.0, ae[a][v] = 0.0;
 #pragma unroll
-      for (int c = 0; c < LV0; ++c) vt[a][c] = 0.0, vat[a][c] = 0.0;
-#pragma unroll
-      for (int c = 0; c < CH1; ++c) eb[a][c] = 0.0, eab[a][c] = 0.0;
-#pragma unroll
-      for (int c = 0; c < LV1; ++c) et[a][c] = 0.0, eat[a][c] = 0.0;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) cb[a][q] = 0.0, ct[a][q] = 0.0;
+      for (int q = 0; q < 3; ++q) gm[a][q] = 0.0;
     }
     // ids of the strip's steps, W at a time
     int vbuf = (has && sl < len) ? __ldg(steps + k0 + sl) : 0;
@@ -438,14 +444,10 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
       const int e2 = __shfl_sync(FULL, e2buf, idx, W);
       if (k < len) {
         double *en = entry(slot);
-        seg_copy(en, x + (int64_t)v * col0 + (int64_t)l0 * CH0, fl0, FS0);
-        seg_copy(en + OC, coords + (int64_t)v * ccol + 3 * (int64_t)l0, cl,
-                 3 * (W + 1));
-        seg_copy(en + OE1, x + e_start + (int64_t)e1 * col1 +
-                               (int64_t)l0 * CH1, fl1, FS1);
-        if (k >= 3)
-          seg_copy(en + OE2, x + e_start + (int64_t)e2 * col1 +
-                                 (int64_t)l0 * CH1, fl1, FS1);
+        seg_copy(en, xv0 + (int64_t)v * col0, fl0, FS0);
+        seg_copy(en + OC, cc0 + (int64_t)v * ccol, cl, 3 * (W + 1));
+        seg_copy(en + OE1, xe0 + (int64_t)e1 * col1, fl1, FS1);
+        if (k >= 3) seg_copy(en + OE2, xe0 + (int64_t)e2 * col1, fl1, FS1);
       }
       sr_commit();
       rv[slot] = v, re1[slot] = e1, re2[slot] = e2;
@@ -453,53 +455,33 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
 #pragma unroll
     for (int d = 0; d < kSrDepth; ++d) fetch(d, d);
 
-    // flush a vertex / edge residency (top contributions one lane up)
-    auto flush_v = [&](auto A_) {
-      constexpr int A = decltype(A_)::value;
+    // flush an entity residency: accumulators back to the layer block
+    // (bottom copy v = 0, connecting v = 1..NV-2, top copy v = NV-1 added
+    // one lane up; the chunk's top level by the last lane)
+    auto flush = [&](double (&acc)[NV], double *yp, bool live) {
+      const double below = __shfl_up_sync(FULL, acc[NV - 1], 1, W);
+      if (live && lane_ok) {
+        atomicAdd(yp, sl > 0 ? acc[0] + below : acc[0]);
 #pragma unroll
-      for (int c = 0; c < CH0; ++c) {
-        double v = vab[A][c];
-        if (c < LV0) {
-          const double below = __shfl_up_sync(FULL, vat[A][c], 1, W);
-          if (sl > 0) v += below;
-        }
-        if (vlive[A] && lane_ok) {
-          double *yp = y + vo[A] + (int64_t)l * CH0 + c;
-          atomicAdd(yp, v);
-          if (c < LV0 && sl == nl - 1) atomicAdd(yp + CH0, vat[A][c]);
-        }
-        vab[A][c] = 0.0;
+        for (int v = 1; v < NV - 1; ++v) atomicAdd(yp + v, acc[v]);
+        if (sl == nl - 1) atomicAdd(yp + (NV - 1), acc[NV - 1]);
       }
 #pragma unroll
-      for (int c = 0; c < LV0; ++c) vat[A][c] = 0.0;
+      for (int v = 0; v < NV; ++v) acc[v] = 0.0;
     };
-    auto flush_e = [&](auto A_) {
-      constexpr int A = decltype(A_)::value;
+    // interval stage of an entering entity from its layer block in the ring
+    auto enter = [&](double (&z)[NV], const double *src) {
+      double b[NV];
 #pragma unroll
-      for (int c = 0; c < CH1; ++c) {
-        double v = eab[A][c];
-        if (c < LV1) {
-          const double below = __shfl_up_sync(FULL, eat[A][c], 1, W);
-          if (sl > 0) v += below;
-        }
-        if (elive[A] && lane_ok) {
-          double *yp = y + eo[A] + (int64_t)l * CH1 + c;
-          atomicAdd(yp, v);
-          if (c < LV1 && sl == nl - 1) atomicAdd(yp + CH1, eat[A][c]);
-        }
-        eab[A][c] = 0.0;
+      for (int v = 0; v < NV - 1; ++v) b[v] = src[sl * (NV - 1) + v];
+      b[NV - 1] = src[(sl + 1) * (NV - 1)];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NV; ++w) s = fma(M.l[v * NV + w], b[w], s);
+        z[v] = s;
       }
-#pragma unroll
-      for (int c = 0; c < LV1; ++c) eat[A][c] = 0.0;
-    };
-    auto load_e = [&](auto A_, const double *src, int64_t origin, bool act) {
-      constexpr int A = decltype(A_)::value;
-#pragma unroll
-      for (int c = 0; c < CH1; ++c) eb[A][c] = src[sl * CH1 + c];
-#pragma unroll
-      for (int c = 0; c < LV1; ++c) et[A][c] = src[(sl + 1) * CH1 + c];
-      eo[A] = origin;
-      elive[A] = act;
     };
     // one strip step into vertex slot A; FILL: edge slot A, else the edge
     // slots A+1, A+2
@@ -507,73 +489,65 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
       constexpr int A = decltype(A_)::value;
       constexpr bool FILL = decltype(FILL_)::value;
       constexpr int B1 = (A + 1) % 3, B2 = (A + 2) % 3;
-      using I1 = std::integral_constant<int, B1>;
-      using I2 = std::integral_constant<int, B2>;
-      flush_v(A_);
+      flush(av[A], yvc[A], vlive[A]);
       if (FILL) {
-        flush_e(A_);
+        flush(ae[A], yec[A], elive[A]);
       } else {
-        flush_e(I1{});
-        flush_e(I2{});
+        flush(ae[B1], yec[B1], elive[B1]);
+        flush(ae[B2], yec[B2], elive[B2]);
       }
       const bool act = k < len;
       sr_wait<kSrDepth - 1>();
       __syncwarp();
       // past the strip's end: read the zero block (contribution exactly 0)
       const double *en = act ? entry(A) : sr_zero;
-#pragma unroll
-      for (int c = 0; c < CH0; ++c) vb[A][c] = en[sl * CH0 + c];
-#pragma unroll
-      for (int c = 0; c < LV0; ++c) vt[A][c] = en[(sl + 1) * CH0 + c];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        cb[A][q] = en[OC + 3 * sl + q];
-        ct[A][q] = en[OC + 3 * (sl + 1) + q];
+      enter(zv[A], en);
+      {
+        const double *g = en + OC + 3 * sl;
+        gm[A][0] = 0.5 * (g[0] + g[3]); // same operations as
+        gm[A][1] = 0.5 * (g[1] + g[4]); // prism_abs_detj
+        gm[A][2] = g[5] - g[2];
       }
-      vo[A] = (int64_t)rv[A] * col0;
+      yvc[A] = yv0 + (int64_t)rv[A] * col0;
       vlive[A] = act;
       if (FILL) {
-        load_e(A_, en + OE1, e_start + (int64_t)re1[A] * col1, act);
+        enter(ze[A], en + OE1);
+        yec[A] = ye0 + (int64_t)re1[A] * col1;
+        elive[A] = act;
       } else {
-        load_e(I1{}, en + OE1, e_start + (int64_t)re1[A] * col1, act);
-        load_e(I2{}, en + OE2, e_start + (int64_t)re2[A] * col1, act);
+        enter(ze[B1], en + OE1);
+        yec[B1] = ye0 + (int64_t)re1[A] * col1;
+        elive[B1] = act;
+        enter(ze[B2], en + OE2);
+        yec[B2] = ye0 + (int64_t)re2[A] * col1;
+        elive[B2] = act;
       }
       __syncwarp();
       fetch(k + kSrDepth, A);
       if (FILL && A < 2) return; // window not full yet
-      double X[6], Y[6], Z[6];
+      const double det =
+          (act && lane_ok)
+              ? prism_abs_detj_mid(gm[0][0], gm[0][1], gm[0][2], gm[1][0],
+                                   gm[1][1], gm[1][2], gm[2][0], gm[2][1],
+                                   gm[2][2])
+              : 0.0;
+      // triangle stage (h: vertices 0-2, edges 3-5), det folded into the
+      // accumulation
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        X[2 * a] = cb[a][0], Y[2 * a] = cb[a][1], Z[2 * a] = cb[a][2];
-        X[2 * a + 1] = ct[a][0], Y[2 * a + 1] = ct[a][1];
-        Z[2 * a + 1] = ct[a][2];
-      }
-      const double det = (act && lane_ok) ? prism_abs_detj(X, Y, Z) : 0.0;
-      double xv[K], yv[K];
+      for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const int p = T.pos[j];
-        if (p < 3)
-          xv[j] = T.level[j] == 2 ? vt[p][T.ch[j]] : vb[p][T.ch[j]];
-        else
-          xv[j] = T.level[j] == 2 ? et[p - 3][T.ch[j]] : eb[p - 3][T.ch[j]];
-      }
-      kron_apply<LY>(M, xv, det, yv);
+        for (int h = 0; h < 6; ++h) {
+          double s = 0.0;
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const int p = T.pos[j];
-        if (p < 3) {
-          if (T.level[j] == 2)
-            vat[p][T.ch[j]] += yv[j];
+          for (int g = 0; g < 3; ++g) s = fma(M.t[h * 6 + g], zv[g][v], s);
+#pragma unroll
+          for (int g = 0; g < 3; ++g)
+            s = fma(M.t[h * 6 + 3 + g], ze[g][v], s);
+          if (h < 3)
+            av[h][v] = fma(det, s, av[h][v]);
           else
-            vab[p][T.ch[j]] += yv[j];
-        } else {
-          if (T.level[j] == 2)
-            eat[p - 3][T.ch[j]] += yv[j];
-          else
-            eab[p - 3][T.ch[j]] += yv[j];
+            ae[h - 3][v] = fma(det, s, ae[h - 3][v]);
         }
-      }
     };
     using S0 = std::integral_constant<int, 0>;
     using S1 = std::integral_constant<int, 1>;
@@ -588,12 +562,11 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
       step(S1{}, FF{}, k + 1);
       step(S2{}, FF{}, k + 2);
     }
-    flush_v(S0{});
-    flush_v(S1{});
-    flush_v(S2{});
-    flush_e(S0{});
-    flush_e(S1{});
-    flush_e(S2{});
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      flush(av[a], yvc[a], vlive[a]);
+      flush(ae[a], yec[a], elive[a]);
+    }
   }
 }
 
