@@ -343,8 +343,16 @@ template <class LY, int W> constexpr int sre_entry() {
   return sre_fs0<LY, W>() + 3 * (W + 1) + 2 * sre_fs1<LY, W>();
 }
 
+// CTA size of the P2 kernel (measured: 384 threads at <= 168 registers
+// spill and run 8 % slower)
+#ifndef PM_SRE_THREADS
+#define PM_SRE_THREADS 256
+#endif
+constexpr int kSreThreads = PM_SRE_THREADS;
+constexpr int kSreWarps = kSreThreads / 32;
+
 template <class LY, int W, int K = LY::K>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kSreThreads, 1)
 k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
               const int32_t *__restrict__ steps,
               const int32_t *__restrict__ steps_e, int64_t n_strips,
@@ -371,9 +379,9 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
   extern __shared__ double sr_ring[];
   double *ring =
       sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
-  const double *sr_zero = sr_ring + (size_t)8 * kSrDepth * SEGS * ES;
+  const double *sr_zero = sr_ring + (size_t)kSreWarps * kSrDepth * SEGS * ES;
   for (int i = threadIdx.x; i < ES; i += blockDim.x)
-    sr_ring[(size_t)8 * kSrDepth * SEGS * ES + i] = 0.0;
+    sr_ring[(size_t)kSreWarps * kSrDepth * SEGS * ES + i] = 0.0;
   __syncthreads();
 
   const int n_chunks = (layers + W - 1) / W;
@@ -588,15 +596,16 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
   const int segs = 32 / W;
   const int64_t items = n_strips * ((a.layers + W - 1) / W);
   const int64_t warps = (items + segs - 1) / segs;
-  const unsigned grid = grid_for(warps * 32, 256, 4);
+  const unsigned grid = grid_for(warps * 32, kSreThreads, 4);
 #define PM_SRE(WW)                                                           \
   do {                                                                       \
-    const size_t smem = sizeof(double) * (8 * kSrDepth * (32 / WW) + 1) *    \
+    const size_t smem = sizeof(double) *                                     \
+                        (kSreWarps * kSrDepth * (32 / WW) + 1) *             \
                         sre_entry<LY, WW>();                                 \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
         k_strip_red_e<LY, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
         (int)smem));                                                         \
-    k_strip_red_e<LY, WW><<<grid, 256, smem, a.s>>>(                         \
+    k_strip_red_e<LY, WW><<<grid, kSreThreads, smem, a.s>>>(                         \
         M, strip_ptr, steps, steps_e, n_strips, a.layers, e_start, a.coords, \
         a.x, a.y);                                                           \
   } while (0)
