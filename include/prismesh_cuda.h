@@ -252,6 +252,13 @@ int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                            int32_t *steps_e /* NULL, or 2 edges per step */,
                            int64_t *totals);
 
+/* STREAM triad a = b + alpha*c over n doubles (16-byte aligned arrays):
+ * the bandwidth reference of the perfbench module (replaces SPEC.md
+ * perfbench "stream_triad", the paper's Table "Maximum
+ * STREAM triad"); 24 bytes per element per pass. */
+int pm_stream_triad(double *a, const double *b, const double *c, double alpha,
+                    int64_t n, void *stream);
+
 /* Device properties used to size grids (SM count, L2 bytes). */
 int pm_device_info(int32_t *sm_count, int64_t *l2_bytes);
 

@@ -87,6 +87,8 @@ SIGNATURES = {
     "pm_halo_unpack_add": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "pm_rcm_order": (ctypes.c_int, [_i64p, _i64p, _i64, _i64p]),
     "pm_device_info": (ctypes.c_int, [_i32p, _i64p]),
+    "pm_stream_triad": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, _i64,
+                                       _vp]),
 }
 
 
@@ -398,6 +400,15 @@ def halo_unpack_add(y, cols, col, buf, base=0, stream=None):
     check(host_lib().pm_halo_unpack_add(ptr(y, base), ptr(cols),
                                         cols.shape[0], col, ptr(buf),
                                         stream_ptr(stream)))
+
+
+def stream_triad(a, b, c, alpha, stream=None):
+    """``a = b + alpha * c`` on the device (float64 CUDA tensors)."""
+    n = a.numel()
+    if b.numel() != n or c.numel() != n:
+        raise ValueError("triad arrays differ in length")
+    check(host_lib().pm_stream_triad(ptr(a), ptr(b), ptr(c), float(alpha),
+                                     n, stream_ptr(stream)))
 
 
 def device_info():
