@@ -252,6 +252,27 @@ int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                            int32_t *steps_e /* NULL, or 2 edges per step */,
                            int64_t *totals);
 
+/* Device derive_edges (replaces mesh.py:33-84 derive_edges): edge set of a
+ * triangle mesh as the sorted unique vertex pairs, cell_edges[c][k] = the
+ * edge opposite local vertex k.  Device arrays: cell_vertices (n_cells,3)
+ * int32; edge_vertices needs room for 3*n_cells rows of 2 int32; cell_edges
+ * (n_cells,3) int32.  n_vertices < 0: unbounded.  Host outputs: *n_edges,
+ * *status = topology error bits (1 negative index, 2 index >= n_vertices,
+ * 4 repeated vertex, 8 duplicate cell, 16 edge on > 2 cells; outputs
+ * undefined when nonzero).  Synchronises the stream. */
+int pm_derive_edges(const int32_t *cell_vertices, int64_t n_cells,
+                    int64_t n_vertices, int32_t *edge_vertices,
+                    int32_t *cell_edges, int64_t *n_edges, int32_t *status,
+                    void *stream);
+
+/* Device cell re-sort of apply_ordering (replaces ordering.py:142-152):
+ * cells_out = forward[cell_vertices][perm] with perm the stable lexsort of
+ * the rows' sorted new vertex triples; perm_out (optional) receives perm.
+ * Device arrays; synchronises the stream. */
+int pm_reorder_cells(const int32_t *cell_vertices, int64_t n_cells,
+                     const int64_t *forward, int64_t n_vertices,
+                     int32_t *cells_out, int32_t *perm_out, void *stream);
+
 /* STREAM triad a = b + alpha*c over n doubles (16-byte aligned arrays):
  * the bandwidth reference of the perfbench module (replaces SPEC.md
  * perfbench "stream_triad", the paper's Table "Maximum

@@ -87,6 +87,10 @@ SIGNATURES = {
     "pm_halo_unpack_add": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "pm_rcm_order": (ctypes.c_int, [_i64p, _i64p, _i64, _i64p]),
     "pm_device_info": (ctypes.c_int, [_i32p, _i64p]),
+    "pm_derive_edges": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64p,
+                                       _i32p, _vp]),
+    "pm_reorder_cells": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _vp,
+                                        _vp]),
     "pm_stream_triad": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, _i64,
                                        _vp]),
 }
@@ -144,6 +148,17 @@ def stream_ptr(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def host_tensor(a, dtype):
+    """CPU tensor of a contiguous ``dtype`` view of ``a`` (copied only when
+    ``a`` is read-only, e.g. the frozen mesh arrays, or needs converting)."""
+    import numpy as np
+    import torch
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    if not arr.flags.writeable:
+        arr = arr.copy()
+    return torch.from_numpy(arr)
+
+
 def ptr(t, base=0):
     """Device address of tensor ``t``; ``base`` (elements) shifts it so that
     global indices land inside a window tensor that starts at ``base``."""
@@ -169,10 +184,8 @@ def mesh_device_arrays(base, device):
     cache = getattr(base, "__dict__", {}).get("_pm_device")
     if cache is not None and cache["device"] == device:
         return cache
-    cv = torch.from_numpy(np.ascontiguousarray(base.cell_vertices,
-                                               dtype=np.int32)).to(device)
-    ce = torch.from_numpy(np.ascontiguousarray(base.cell_edges,
-                                               dtype=np.int32)).to(device)
+    cv = host_tensor(base.cell_vertices, np.int32).to(device)
+    ce = host_tensor(base.cell_edges, np.int32).to(device)
     cache = {"device": device, "cv": cv, "ce": ce}
     try:
         base.__dict__["_pm_device"] = cache
@@ -400,6 +413,41 @@ def halo_unpack_add(y, cols, col, buf, base=0, stream=None):
     check(host_lib().pm_halo_unpack_add(ptr(y, base), ptr(cols),
                                         cols.shape[0], col, ptr(buf),
                                         stream_ptr(stream)))
+
+
+def derive_edges_device(cell_vertices, num_vertices=None):
+    """Device derive_edges: ``(edge_vertices, cell_edges, status)`` as numpy
+    int32 arrays; ``status`` != 0 flags a topology error (see the header)."""
+    import numpy as np
+    import torch
+    dev = cuda_device()
+    cells = host_tensor(cell_vertices, np.int32).to(dev)
+    n_cells = cells.shape[0]
+    ev = torch.empty((3 * n_cells, 2), dtype=torch.int32, device=dev)
+    ce = torch.empty((n_cells, 3), dtype=torch.int32, device=dev)
+    n = ctypes.c_int64(0)
+    st = ctypes.c_int32(0)
+    check(host_lib().pm_derive_edges(
+        ptr(cells), n_cells, -1 if num_vertices is None else int(num_vertices),
+        ptr(ev), ptr(ce), ctypes.byref(n), ctypes.byref(st),
+        stream_ptr(None)))
+    if st.value:
+        return None, None, st.value
+    return ev[:n.value].cpu().numpy(), ce.cpu().numpy(), 0
+
+
+def reorder_cells_device(cell_vertices, forward):
+    """Device apply_ordering cell re-sort: ``forward[cells][perm]``."""
+    import numpy as np
+    import torch
+    dev = cuda_device()
+    cells = host_tensor(cell_vertices, np.int32).to(dev)
+    fwd = host_tensor(forward, np.int64).to(dev)
+    out = torch.empty_like(cells)
+    check(host_lib().pm_reorder_cells(ptr(cells), cells.shape[0], ptr(fwd),
+                                      fwd.shape[0], ptr(out), None,
+                                      stream_ptr(None)))
+    return out.cpu().numpy()
 
 
 def stream_triad(a, b, c, alpha, stream=None):

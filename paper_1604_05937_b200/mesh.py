@@ -44,14 +44,46 @@ def _pair_keys(lo, hi):
     return (lo.astype(np.int64) << 32) | hi.astype(np.int64)
 
 
-def derive_edges(cell_vertices, num_vertices=None):
+# Meshes with at least this many cells derive their edges on the GPU when
+# one is present (csrc/mesh_pipeline.cu; PM_DEVICE_MESH=0 disables).
+DEVICE_MESH_MIN_CELLS = 1 << 16
+
+
+def device_mesh_ok(n_cells: int) -> bool:
+    """Use the device mesh pipeline for a mesh of ``n_cells`` cells?"""
+    import os
+    if n_cells < DEVICE_MESH_MIN_CELLS or \
+            os.environ.get("PM_DEVICE_MESH", "1") == "0":
+        return False
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return False
+        from . import _lib
+        _lib.host_lib()
+    except Exception:
+        return False
+    return True
+
+
+def derive_edges(cell_vertices, num_vertices=None, device=None):
     """Edge set and cell->edge incidence of a triangle mesh.
 
     Returns ``(edge_vertices int32 (E,2), cell_edges int32 (C,3))``; see
     reference ``mesh.py:33-84`` for the contract (same errors, same
-    numbering).
+    numbering).  ``device`` (default: large meshes when a GPU is present)
+    runs the sort-based device pipeline (``pm_derive_edges``), bit-exact
+    with the host path below; on a topology error the host path runs and
+    raises the reference's message.
     """
     cells = np.asarray(cell_vertices)
+    if device is None:
+        device = cells.ndim == 2 and device_mesh_ok(cells.shape[0])
+    if device and cells.ndim == 2 and cells.shape[1] == 3:
+        from . import _lib
+        ev, ce, status = _lib.derive_edges_device(cells, num_vertices)
+        if not status:
+            return ev, ce
     if cells.ndim != 2 or cells.shape[1] != 3:
         raise MeshTopologyError(
             f"cell_vertices must have shape (n_cells, 3), got {cells.shape}")
