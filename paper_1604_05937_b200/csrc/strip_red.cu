@@ -65,6 +65,43 @@ template <class LY> constexpr int sr_min_blocks() {
   return LY::CH0 > 2 ? 1 : 2; // measured: 3/SM (scalar) and 2/SM (3-vector) slower
 }
 
+// Padded ring entries of the strip kernel: the field part and the
+// coordinate part are whole rows of W values, so every lane issues every
+// copy (cp.async with a 0/8-byte source size: lanes past the chunk
+// zero-fill their row slot instead of being predicated off).
+template <class LY, int W> constexpr int sr_frows() {
+  return (sr_fs<LY, W>() + W - 1) / W;
+}
+template <class LY, int W> constexpr int sr_crows() {
+  return (3 * (W + 1) + W - 1) / W;
+}
+template <class LY, int W> constexpr int sr_pentry() {
+  return (sr_frows<LY, W>() + sr_crows<LY, W>()) * W;
+}
+constexpr int kSrIds = 64; // strip vertex ids staged per segment
+template <class LY, int W> constexpr size_t sr_smem() {
+  return sizeof(double) * ((size_t)8 * kSrDepth * (32 / W) + 1) *
+             sr_pentry<LY, W>() +
+         sizeof(int) * 8 * (32 / W) * kSrIds;
+}
+
+__device__ __forceinline__ void sr_cp8z(double *dst, const double *src,
+                                        int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+
+// element `v` of a column family with a stride in bytes (one IMAD.WIDE)
+template <class T>
+__device__ __forceinline__ T *col_at(T *base, int v, int stride_bytes) {
+  using C = typename std::conditional<std::is_const<T>::value, const char,
+                                      char>::type;
+  return reinterpret_cast<T *>(reinterpret_cast<C *>(base) +
+                               (int64_t)v * stride_bytes);
+}
+
 // The element kernel split along the window: y = det (Mtri (x) Mline) x.
 // The interval stage z = Mline x only involves one vertex column, so it is
 // applied once when the vertex enters the window (not in each of its three
@@ -87,20 +124,26 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
   // copies, connecting channel v*NC + c (the slot table of fspace.py)
   static_assert(NH == 3 && NC * NV == CH + LV, "vertex-column layout");
   static_assert(LV == 0 || (LV == NC && NV == 2 && CH == LV), "strip layout");
+  constexpr int FR = sr_frows<LY, W>(), CR = sr_crows<LY, W>();
+  constexpr int FP = FR * W;                 // coordinate part offset
+  constexpr int ES = sr_pentry<LY, W>();
   const int lane = threadIdx.x & 31;
   const int sl = lane % W, seg = lane / W;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // column lengths fit 32 bits: a column origin is one IMAD.WIDE
-  const int col = layers * CH + LV; // vertex column length
-  const int ccol = 3 * (layers + 1);
-  {
-    extern __shared__ double sr_ring[];
-    constexpr int ESZ = sr_entry<LY, W>();
-    double *z = sr_ring + (size_t)8 * kSrDepth * SEGS * ESZ;
-    for (int i = threadIdx.x; i < ESZ; i += blockDim.x) z[i] = 0.0;
-    __syncthreads();
-  }
+  // column lengths in bytes fit 32 bits: a column origin is one IMAD.WIDE
+  const int colb = 8 * (layers * CH + LV); // vertex column
+  const int ccolb = 8 * 3 * (layers + 1);  // coordinate column
+  extern __shared__ double sr_ring[];
+  double *const ring =
+      sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
+  const double *const sr_zero = sr_ring + (size_t)8 * kSrDepth * SEGS * ES;
+  int *const sid = reinterpret_cast<int *>(sr_ring + (size_t)(8 * kSrDepth *
+                                                              SEGS + 1) * ES) +
+                   ((threadIdx.x >> 5) * SEGS + seg) * kSrIds;
+  for (int i = threadIdx.x; i < ES; i += blockDim.x)
+    sr_ring[(size_t)8 * kSrDepth * SEGS * ES + i] = 0.0;
+  __syncthreads();
 
   // work item = (strip, layer chunk), chunk fastest: the chunks of a strip
   // run side by side, so the sectors two chunks of a vertex column share
@@ -118,174 +161,189 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
 #pragma unroll
     for (int o = W; o < 32; o <<= 1)
       maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
-    {
-      const int nl = has ? min(W, layers - l0) : 0;
-      const bool lane_ok = sl < nl;
-      // the lane's element of every column chunk it touches
-      const double *xl = x + (int64_t)l0 * CH + sl;
-      const double *cl0 = coords + 3 * (int64_t)l0 + sl;
-      double *yl = y + ((int64_t)l0 + sl) * CH;
-      // window vertex: interval-stage values z[c][v] at the lane's cell
-      // layer and the geometry the Jacobian needs, derived once on entry:
-      // xm, ym (mid-layer), dz; per-vertex accumulators acc[c][v]
-      double zv[3][NC][NV], gm[3][3], acc[3][NC][NV];
-      double *yc[3] = {yl, yl, yl}; // lane's element of the slot's column
-      bool live[3] = {false, false, false};
+    const int nl = has ? min(W, layers - l0) : 0;
+    const bool lane_ok = sl < nl;
+    // source sizes of the lane's copies (8 inside the chunk, else 0)
+    int fz[FR], cz[CR];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
+    for (int r = 0; r < FR; ++r) fz[r] = sl + W * r < nl * CH + LV ? 8 : 0;
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
+    for (int r = 0; r < CR; ++r) cz[r] = sl + W * r < 3 * (nl + 1) ? 8 : 0;
+    // the lane's element of every column chunk it touches
+    const double *xl = x + (int64_t)l0 * CH + sl;
+    const double *cl0 = coords + 3 * (int64_t)l0 + sl;
+    double *yl = y + ((int64_t)l0 + sl) * CH;
+    // window vertex: interval-stage values z[c][v] at the lane's cell
+    // layer and the geometry the Jacobian needs, derived once on entry:
+    // xm, ym (mid-layer), dz; per-vertex accumulators acc[c][v]
+    double zv[3][NC][NV], gm[3][3], acc[3][NC][NV];
+    double *yc[3] = {yl, yl, yl}; // lane's element of the slot's column
+    bool live[3] = {false, false, false};
 #pragma unroll
-          for (int v = 0; v < NV; ++v) zv[a][c][v] = 0.0, acc[a][c][v] = 0.0;
+    for (int a = 0; a < 3; ++a) {
 #pragma unroll
-        for (int q = 0; q < 3; ++q) gm[a][q] = 0.0;
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) zv[a][c][v] = 0.0, acc[a][c][v] = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) gm[a][q] = 0.0;
+    }
+    // the strip's vertex ids, staged kSrIds at a time (one broadcast LDS
+    // per step)
+    auto load_ids = [&](int base) {
+#pragma unroll
+      for (int r = 0; r < kSrIds / W; ++r) {
+        const int i = base + sl + W * r;
+        sid[sl + W * r] = i < len ? __ldg(steps + k0 + i) : 0;
       }
-      // vertex ids of the strip, W at a time (lane sl holds step base+sl)
-      int vbuf = (has && sl < len) ? __ldg(steps + k0 + sl) : 0;
-      int vbase = 0;
-      // per-warp shared-memory prefetch ring, kSrDepth steps deep: the
-      // segment copies its vertex's chunk of the field and coordinate
-      // columns contiguously (coalesced cp.async); lanes then read their
-      // own level (and the level above) out of shared memory.
-      constexpr int FS = sr_fs<LY, W>();
-      constexpr int ES = sr_entry<LY, W>();
-      extern __shared__ double sr_ring[];
-      double *ring = sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
-      const double *sr_zero = sr_ring + (size_t)8 * kSrDepth * SEGS * ES;
-      auto entry = [&](int slot) {
-        return ring + (size_t)(slot * SEGS + seg) * ES;
-      };
-      const int fl = nl * CH + LV, cl = 3 * (nl + 1);
-      int rv[kSrDepth];
-      auto fetch = [&](int k, int slot) {
-        if (k - vbase >= W) { // all segments advance in lockstep
-          vbase += W;
-          vbuf = (has && vbase + sl < len) ? __ldg(steps + k0 + vbase + sl)
-                                           : 0;
-        }
-        const int v = __shfl_sync(FULL, vbuf, (k - vbase) & (W - 1), W);
-        if (k < len) {
-          const double *fp = xl + (int64_t)v * col;
-          const double *cp = cl0 + (int64_t)v * ccol;
-          double *e = entry(slot) + sl;
+      __syncwarp();
+    };
+    __syncwarp(); // the previous item's last id reads are done
+    load_ids(0);
+    // per-warp shared-memory prefetch ring, kSrDepth steps deep: the
+    // segment copies its vertex's chunk of the field and coordinate
+    // columns contiguously (coalesced cp.async); lanes then read their
+    // own level (and the level above) out of shared memory.
+    auto entry = [&](int slot) {
+      return ring + (size_t)(slot * SEGS + seg) * ES;
+    };
+    int rv[kSrDepth];
+    auto fetch = [&](int k, int slot) {
+      if ((k & (kSrIds - 1)) == 0 && k > 0) { // warp-uniform
+        __syncwarp();
+        load_ids(k);
+      }
+      const int v = sid[k & (kSrIds - 1)];
+      if (k < len) {
+        const double *fp = col_at(xl, v, colb);
+        const double *cp = col_at(cl0, v, ccolb);
+        double *e = entry(slot) + sl;
 #pragma unroll
-          for (int r = 0; r < (FS + W - 1) / W; ++r)
-            if (sl + W * r < fl) sr_cp8(e + W * r, fp + W * r);
+        for (int r = 0; r < FR; ++r) sr_cp8z(e + W * r, fp + W * r, fz[r]);
 #pragma unroll
-          for (int r = 0; r < (3 * (W + 1) + W - 1) / W; ++r)
-            if (sl + W * r < cl) sr_cp8(e + FS + W * r, cp + W * r);
-        }
-        sr_commit(); // one group per step (possibly empty)
-        return v;
-      };
+        for (int r = 0; r < CR; ++r)
+          sr_cp8z(e + FP + W * r, cp + W * r, cz[r]);
+      }
+      sr_commit(); // one group per step (possibly empty)
+      return v;
+    };
 #pragma unroll
-      for (int d = 0; d < kSrDepth; ++d) rv[d] = fetch(d, d);
+    for (int d = 0; d < kSrDepth; ++d) rv[d] = fetch(d, d);
 
-      auto flush = [&](auto A_) {
-        constexpr int A = decltype(A_)::value;
-        // back to the vertex column's layer block: bottom / connecting
-        // channels vb, top copies vt
-        double vb[CH], vt[LVA];
+    auto flush = [&](auto A_) {
+      constexpr int A = decltype(A_)::value;
+      // back to the vertex column's layer block: bottom / connecting
+      // channels vb, top copies vt
+      double vb[CH], vt[LVA];
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
+      for (int c = 0; c < NC; ++c)
 #pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            if (LV == 0)
-              vb[v * NC + c] = acc[A][c][v];
-            else if (v == 0)
-              vb[c] = acc[A][c][v];
-            else
-              vt[c < LVA ? c : 0] = acc[A][c][v];
-            acc[A][c][v] = 0.0;
-          }
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          double v = vb[c];
-          if (c < LV) {
-            const double below = __shfl_up_sync(FULL, vt[c < LV ? c : 0], 1, W);
-            if (sl > 0) v += below;
-          }
-          if (live[A] && lane_ok) {
-            atomicAdd(yc[A] + c, v);
-            if (c < LV && sl == nl - 1) atomicAdd(yc[A] + CH + c, vt[c < LV ? c : 0]);
-          }
+        for (int v = 0; v < NV; ++v) {
+          if (LV == 0)
+            vb[v * NC + c] = acc[A][c][v];
+          else if (v == 0)
+            vb[c] = acc[A][c][v];
+          else
+            vt[c < LVA ? c : 0] = acc[A][c][v];
+          acc[A][c][v] = 0.0;
         }
-      };
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        double v = vb[c];
+        if (c < LV) {
+          const double below = __shfl_up_sync(FULL, vt[c < LV ? c : 0], 1, W);
+          if (sl > 0) v += below;
+        }
+        if (live[A] && lane_ok) {
+          atomicAdd(yc[A] + c, v);
+          if (c < LV && sl == nl - 1) atomicAdd(yc[A] + CH + c, vt[c < LV ? c : 0]);
+        }
+      }
+    };
 
-      auto step = [&](auto A_, int k) {
-        constexpr int A = decltype(A_)::value;
-        flush(A_);
-        const bool act = k < len;
-        // the vertex of ring slot A (step k) enters window slot A
-        sr_wait<kSrDepth - 1>(); // this lane's copies of step k landed
-        __syncwarp();            // ... and the other lanes' ones
-        // steps past this segment's strip read a zero block instead of the
-        // (stale, possibly non-finite) ring slot: their contribution is 0
-        const double *e = act ? entry(A) : sr_zero;
-        double fb[CH], ft[LVA];
+    // one strip step into window slot A; FILL: the first three steps (the
+    // window fills, nothing to flush, no cell before the third vertex)
+    auto step = [&](auto A_, auto FILL_, int k) {
+      constexpr int A = decltype(A_)::value;
+      constexpr bool FILL = decltype(FILL_)::value;
+      if (!FILL) flush(A_);
+      const bool act = k < len;
+      // the vertex of ring slot A (step k) enters window slot A
+      sr_wait<kSrDepth - 1>(); // this lane's copies of step k landed
+      __syncwarp();            // ... and the other lanes' ones
+      // steps past this segment's strip read a zero block instead of the
+      // (stale, possibly non-finite) ring slot; lanes past the chunk read
+      // zero-filled values and are never flushed.
+      const double *e = act ? entry(A) : sr_zero;
+      double fb[CH], ft[LVA];
 #pragma unroll
-        for (int c = 0; c < CH; ++c) fb[c] = e[sl * CH + c];
+      for (int c = 0; c < CH; ++c) fb[c] = e[sl * CH + c];
 #pragma unroll
-        for (int c = 0; c < LV; ++c) ft[c] = e[(sl + 1) * CH + c];
-        {
-          const double *g = e + FS + 3 * sl;
-          gm[A][0] = 0.5 * (g[0] + g[3]); // same operations as
-          gm[A][1] = 0.5 * (g[1] + g[4]); // prism_abs_detj
-          gm[A][2] = g[5] - g[2];
+      for (int c = 0; c < LV; ++c) ft[c] = e[(sl + 1) * CH + c];
+      {
+        const double *g = e + FP + 3 * sl;
+        gm[A][0] = 0.5 * (g[0] + g[3]); // same operations as
+        gm[A][1] = 0.5 * (g[1] + g[4]); // prism_abs_detj
+        gm[A][2] = g[5] - g[2];
+      }
+      __syncwarp(); // reads done before the slot is refilled
+      yc[A] = col_at(yl, rv[A], colb);
+      live[A] = act;
+      // interval stage of the entering vertex
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double s = 0.0;
+#pragma unroll
+          for (int w = 0; w < NV; ++w) {
+            const double xw = LV == 0 ? fb[w * NC + c]
+                              : w == 0 ? fb[c]
+                                       : ft[c < LVA ? c : 0];
+            s = fma(M.l[v * NV + w], xw, s);
+          }
+          zv[A][c][v] = s;
         }
-        __syncwarp(); // reads done before the slot is refilled
-        yc[A] = yl + (int64_t)rv[A] * col;
-        live[A] = act;
-        // interval stage of the entering vertex
+      // refill ring slot A with the step kSrDepth ahead
+      rv[A] = fetch(k + kSrDepth, A);
+      if (FILL && A < 2) return; // window not full yet
+      // past the strip's end the window still holds two live vertices:
+      // the step contributes nothing
+      const double dj = prism_abs_detj_mid(gm[0][0], gm[0][1], gm[0][2],
+                                           gm[1][0], gm[1][1], gm[1][2],
+                                           gm[2][0], gm[2][1], gm[2][2]);
+      const double det = act ? dj : 0.0;
+      // triangle stage, det folded into the accumulation
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
+      for (int c = 0; c < NC; ++c)
 #pragma unroll
-          for (int v = 0; v < NV; ++v) {
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int h = 0; h < 3; ++h) {
             double s = 0.0;
 #pragma unroll
-            for (int w = 0; w < NV; ++w) {
-              const double xw = LV == 0 ? fb[w * NC + c]
-                                : w == 0 ? fb[c]
-                                         : ft[c < LVA ? c : 0];
-              s = fma(M.l[v * NV + w], xw, s);
-            }
-            zv[A][c][v] = s;
+            for (int g = 0; g < 3; ++g)
+              s = fma(M.t[h * 3 + g], zv[g][c][v], s);
+            acc[h][c][v] = fma(det, s, acc[h][c][v]);
           }
-        // refill ring slot A with the step kSrDepth ahead
-        rv[A] = fetch(k + kSrDepth, A);
-        if (k < 2) return; // window not full yet
-        const double det =
-            (act && lane_ok)
-                ? prism_abs_detj_mid(gm[0][0], gm[0][1], gm[0][2], gm[1][0],
-                                     gm[1][1], gm[1][2], gm[2][0], gm[2][1],
-                                     gm[2][2])
-                : 0.0;
-        // triangle stage, det folded into the accumulation
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-#pragma unroll
-          for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int h = 0; h < 3; ++h) {
-              double s = 0.0;
-#pragma unroll
-              for (int g = 0; g < 3; ++g)
-                s = fma(M.t[h * 3 + g], zv[g][c][v], s);
-              acc[h][c][v] = fma(det, s, acc[h][c][v]);
-            }
-      };
-      using S0 = std::integral_constant<int, 0>;
-      using S1 = std::integral_constant<int, 1>;
-      using S2 = std::integral_constant<int, 2>;
-      for (int k = 0; k < maxlen; k += 3) {
-        step(S0{}, k);
-        step(S1{}, k + 1);
-        step(S2{}, k + 2);
-      }
-      flush(S0{});
-      flush(S1{});
-      flush(S2{});
+    };
+    using S0 = std::integral_constant<int, 0>;
+    using S1 = std::integral_constant<int, 1>;
+    using S2 = std::integral_constant<int, 2>;
+    using TF = std::true_type;
+    using FF = std::false_type;
+    step(S0{}, TF{}, 0);
+    step(S1{}, TF{}, 1);
+    step(S2{}, TF{}, 2);
+    for (int k = 3; k < maxlen; k += 3) {
+      step(S0{}, FF{}, k);
+      step(S1{}, FF{}, k + 1);
+      step(S2{}, FF{}, k + 2);
     }
+    flush(S0{});
+    flush(S1{});
+    flush(S2{});
+    sr_wait<0>(); // no copy in flight into the ring across items
   }
 }
 
@@ -305,8 +363,7 @@ static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
   const unsigned grid = grid_for(warps * 32, 256, 8);
 #define PM_SR(WW)                                                            \
   do {                                                                       \
-    const size_t smem = sizeof(double) * (8 * kSrDepth * (32 / WW) + 1) *    \
-                        sr_entry<LY, WW>();                                  \
+    const size_t smem = sr_smem<LY, WW>();                                   \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
         k_strip_red<LY, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
         (int)smem));                                                         \
