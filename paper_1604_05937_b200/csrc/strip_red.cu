@@ -429,14 +429,19 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
   const int sl = lane % W, seg = lane / W;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // column lengths fit 32 bits: a column origin is one IMAD.WIDE
-  const int col0 = layers * CH0 + LV0;
-  const int col1 = layers * CH1 + LV1;
-  const int ccol = 3 * (layers + 1);
+  // column lengths in bytes fit 32 bits: a column origin is one IMAD.WIDE
+  const int col0 = 8 * (layers * CH0 + LV0);
+  const int col1 = 8 * (layers * CH1 + LV1);
+  const int ccol = 8 * 3 * (layers + 1);
   extern __shared__ double sr_ring[];
   double *ring =
       sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
   const double *sr_zero = sr_ring + (size_t)kSreWarps * kSrDepth * SEGS * ES;
+  // the strip's vertex and edge ids, staged kSrIds steps at a time
+  int *const sid = reinterpret_cast<int *>(
+                       sr_ring + (size_t)(kSreWarps * kSrDepth * SEGS + 1) * ES) +
+                   ((threadIdx.x >> 5) * SEGS + (threadIdx.x & 31) / W) * 3 *
+                       kSrIds;
   for (int i = threadIdx.x; i < ES; i += blockDim.x)
     sr_ring[(size_t)kSreWarps * kSrDepth * SEGS * ES + i] = 0.0;
   __syncthreads();
@@ -479,11 +484,19 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
 #pragma unroll
       for (int q = 0; q < 3; ++q) gm[a][q] = 0.0;
     }
-    // ids of the strip's steps, W at a time
-    int vbuf = (has && sl < len) ? __ldg(steps + k0 + sl) : 0;
-    int e1buf = (has && sl < len) ? __ldg(steps_e + 2 * (k0 + sl)) : 0;
-    int e2buf = (has && sl < len) ? __ldg(steps_e + 2 * (k0 + sl) + 1) : 0;
-    int vbase = 0;
+    auto load_ids = [&](int base) {
+#pragma unroll
+      for (int r = 0; r < kSrIds / W; ++r) {
+        const int j = sl + W * r, i = base + j;
+        const bool ok = i < len;
+        sid[j] = ok ? __ldg(steps + k0 + i) : 0;
+        sid[kSrIds + 2 * j] = ok ? __ldg(steps_e + 2 * (k0 + i)) : 0;
+        sid[kSrIds + 2 * j + 1] = ok ? __ldg(steps_e + 2 * (k0 + i) + 1) : 0;
+      }
+      __syncwarp();
+    };
+    __syncwarp(); // the previous item's last id reads are done
+    load_ids(0);
     auto entry = [&](int slot) {
       return ring + (size_t)(slot * SEGS + seg) * ES;
     };
@@ -496,23 +509,19 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
       }
     };
     auto fetch = [&](int k, int slot) {
-      if (k - vbase >= W) { // all segments advance in lockstep
-        vbase += W;
-        const bool ok = has && vbase + sl < len;
-        vbuf = ok ? __ldg(steps + k0 + vbase + sl) : 0;
-        e1buf = ok ? __ldg(steps_e + 2 * (k0 + vbase + sl)) : 0;
-        e2buf = ok ? __ldg(steps_e + 2 * (k0 + vbase + sl) + 1) : 0;
+      if ((k & (kSrIds - 1)) == 0 && k > 0) { // warp-uniform
+        __syncwarp();
+        load_ids(k);
       }
-      const int idx = (k - vbase) & (W - 1);
-      const int v = __shfl_sync(FULL, vbuf, idx, W);
-      const int e1 = __shfl_sync(FULL, e1buf, idx, W);
-      const int e2 = __shfl_sync(FULL, e2buf, idx, W);
+      const int j = k & (kSrIds - 1);
+      const int v = sid[j];
+      const int e1 = sid[kSrIds + 2 * j], e2 = sid[kSrIds + 2 * j + 1];
       if (k < len) {
         double *en = entry(slot);
-        seg_copy(en, xv0 + (int64_t)v * col0, fl0, FS0);
-        seg_copy(en + OC, cc0 + (int64_t)v * ccol, cl, 3 * (W + 1));
-        seg_copy(en + OE1, xe0 + (int64_t)e1 * col1, fl1, FS1);
-        if (k >= 3) seg_copy(en + OE2, xe0 + (int64_t)e2 * col1, fl1, FS1);
+        seg_copy(en, col_at(xv0, v, col0), fl0, FS0);
+        seg_copy(en + OC, col_at(cc0, v, ccol), cl, 3 * (W + 1));
+        seg_copy(en + OE1, col_at(xe0, e1, col1), fl1, FS1);
+        if (k >= 3) seg_copy(en + OE2, col_at(xe0, e2, col1), fl1, FS1);
       }
       sr_commit();
       rv[slot] = v, re1[slot] = e1, re2[slot] = e2;
@@ -573,29 +582,29 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
         gm[A][1] = 0.5 * (g[1] + g[4]); // prism_abs_detj
         gm[A][2] = g[5] - g[2];
       }
-      yvc[A] = yv0 + (int64_t)rv[A] * col0;
+      yvc[A] = col_at(yv0, rv[A], col0);
       vlive[A] = act;
       if (FILL) {
         enter(ze[A], en + OE1);
-        yec[A] = ye0 + (int64_t)re1[A] * col1;
+        yec[A] = col_at(ye0, re1[A], col1);
         elive[A] = act;
       } else {
         enter(ze[B1], en + OE1);
-        yec[B1] = ye0 + (int64_t)re1[A] * col1;
+        yec[B1] = col_at(ye0, re1[A], col1);
         elive[B1] = act;
         enter(ze[B2], en + OE2);
-        yec[B2] = ye0 + (int64_t)re2[A] * col1;
+        yec[B2] = col_at(ye0, re2[A], col1);
         elive[B2] = act;
       }
       __syncwarp();
       fetch(k + kSrDepth, A);
       if (FILL && A < 2) return; // window not full yet
-      const double det =
-          (act && lane_ok)
-              ? prism_abs_detj_mid(gm[0][0], gm[0][1], gm[0][2], gm[1][0],
-                                   gm[1][1], gm[1][2], gm[2][0], gm[2][1],
-                                   gm[2][2])
-              : 0.0;
+      // lanes past the chunk are never flushed; past the strip's end the
+      // window still holds live entities: no contribution
+      const double dj = prism_abs_detj_mid(gm[0][0], gm[0][1], gm[0][2],
+                                           gm[1][0], gm[1][1], gm[1][2],
+                                           gm[2][0], gm[2][1], gm[2][2]);
+      const double det = act ? dj : 0.0;
       // triangle stage (h: vertices 0-2, edges 3-5), det folded into the
       // accumulation
 #pragma unroll
@@ -657,8 +666,9 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
 #define PM_SRE(WW)                                                           \
   do {                                                                       \
     const size_t smem = sizeof(double) *                                     \
-                        (kSreWarps * kSrDepth * (32 / WW) + 1) *             \
-                        sre_entry<LY, WW>();                                 \
+                            (kSreWarps * kSrDepth * (32 / WW) + 1) *         \
+                            sre_entry<LY, WW>() +                            \
+                        sizeof(int) * kSreWarps * (32 / WW) * 3 * kSrIds;    \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
         k_strip_red_e<LY, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
         (int)smem));                                                         \
