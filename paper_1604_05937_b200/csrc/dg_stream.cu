@@ -85,13 +85,29 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int64_t cl_begin, int layers,
       for (int q = 0; q < 3; ++q)
         dst[3 * a + q] = __ldg(coords + lx[a] + q + 3 * w.l);
   };
+  // lanes whose top level is not the next lane's bottom (warp edge, last
+  // layer of a column) prefetch it too
+  auto load_top = [&](const Where &w, const int32_t *lx, double *dst) {
+    const uint32_t c_up = __shfl_down_sync(0xffffffffu, w.c, 1);
+    const bool own = lane == 31 || w.l == layers - 1 || c_up != w.c;
+    if (own) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          dst[3 * a + q] = __ldg(coords + lx[a] + 3 + q + 3 * w.l);
+    }
+    return own;
+  };
   Where w0{0, 0}, w1{0, 0}, w2{0, 0};
   int32_t lx0[3] = {0, 0, 0}, lx1[3] = {0, 0, 0}, lx2[3] = {0, 0, 0};
-  double cb[9], nb[9];
+  double cb[9], nb[9], ct[9], nt[9];
+  bool own0 = false, own1 = false;
   if (n_mine > 0) {
     w0 = where(first);
     load_map(w0, lx0);
     load_xyz(w0, lx0, cb);
+    own0 = load_top(w0, lx0, ct);
   }
   if (n_mine > 1) {
     w1 = where(first + stride);
@@ -103,15 +119,16 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int64_t cl_begin, int layers,
     const int s = (int)(i % S);
     const int64_t u = first + i * stride;
     double *b = buf + s * T * D;
-    if (i + 1 < n_mine) load_xyz(w1, lx1, nb);
+    if (i + 1 < n_mine) {
+      load_xyz(w1, lx1, nb);
+      own1 = load_top(w1, lx1, nt);
+    }
     if (i + 2 < n_mine) {
       w2 = where(u + 2 * stride);
       load_map(w2, lx2);
     }
 
-    // top level of this cell-layer
-    const uint32_t c_up = __shfl_down_sync(0xffffffffu, w0.c, 1);
-    const bool own_top = lane == 31 || w0.l == layers - 1 || c_up != w0.c;
+    // top level of this cell-layer: the next lane's bottom, or prefetched
     double X[6], Y[6], Z[6];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -119,7 +136,7 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int64_t cl_begin, int layers,
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const double up = __shfl_down_sync(0xffffffffu, cb[3 * a + q], 1);
-        top[q] = own_top ? __ldg(coords + lx0[a] + 3 + q + 3 * w0.l) : up;
+        top[q] = own0 ? ct[3 * a + q] : up;
       }
       X[2 * a] = cb[3 * a], Y[2 * a] = cb[3 * a + 1], Z[2 * a] = cb[3 * a + 2];
       X[2 * a + 1] = top[0], Y[2 * a + 1] = top[1], Z[2 * a + 1] = top[2];
@@ -172,7 +189,8 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int64_t cl_begin, int layers,
       }
     }
 #pragma unroll
-    for (int q = 0; q < 9; ++q) cb[q] = nb[q];
+    for (int q = 0; q < 9; ++q) cb[q] = nb[q], ct[q] = nt[q];
+    own0 = own1;
     w0 = w1;
     w1 = w2;
 #pragma unroll

@@ -1,0 +1,6 @@
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "DG or stream or host" 2>&1 | tail -1
+: > gpurun_out/dg.jsonl
+for c in C2 C2 C4-DG1xDG1-rcm-L20 C4-DG1xDG1-rcm-L100 C4-DG1xDG1-random-L100 C4-DG0xDG0-rcm-L50; do
+timeout 300 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/dg.jsonl
+done
+python tools/summarize.py gpurun_out/dg.jsonl
