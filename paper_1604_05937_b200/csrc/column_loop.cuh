@@ -28,7 +28,29 @@ prism_abs_detj_mid(double xm0, double ym0, double dz0, double xm1, double ym1,
 struct KronMat {
   double t[36]; // Mtri, row-major (<= 6 x 6)
   double l[9];  // Mline, row-major (<= 3 x 3)
+  // Mtri = ta I + tb J (3 x 3 with equal diagonal and equal off-diagonal
+  // entries: P1 triangles under any symmetric rule), see kron_sym3
+  double ta, tb;
 };
+
+// Does the 3 x 3 triangle factor have the form ta I + tb J (to a relative
+// 4 ulp)?  Fills ta, tb from the averaged diagonal / off-diagonal.
+inline bool kron_sym3(KronMat &M) {
+  double d = 0, o = 0, big = 0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      (i == j ? d : o) += M.t[3 * i + j];
+      big = fmax(big, fabs(M.t[3 * i + j]));
+    }
+  d /= 3, o /= 6;
+  const double tol = 4 * 2.220446049250313e-16 * big;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (fabs(M.t[3 * i + j] - (i == j ? d : o)) > tol) return false;
+  M.ta = d - o;
+  M.tb = o;
+  return true;
+}
 
 // |det J| of the affine map reference prism -> physical prism cell-layer.
 // Vertex index v = 2a + b (a: triangle vertex, b: 0 bottom / 1 top level).

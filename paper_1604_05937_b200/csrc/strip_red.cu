@@ -107,7 +107,7 @@ __device__ __forceinline__ T *col_at(T *base, int v, int stride_bytes) {
 // applied once when the vertex enters the window (not in each of its three
 // cells); per cell only the triangle stage runs, with det folded into the
 // accumulation: acc[h] = fma(det, sum_g Mtri[h][g] z[g], acc[h]).
-template <class LY, int W, int K = LY::K>
+template <class LY, int W, bool SYM, int K = LY::K>
 __global__ void __launch_bounds__(256, sr_min_blocks<LY>())
 k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
             const int32_t *__restrict__ steps, int64_t n_strips, int layers,
@@ -314,18 +314,31 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
                                            gm[2][0], gm[2][1], gm[2][2]);
       const double det = act ? dj : 0.0;
       // triangle stage, det folded into the accumulation
+      if constexpr (SYM) { // Mtri = ta I + tb J
+        const double dta = det * M.ta, dtb = det * M.tb;
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
+        for (int c = 0; c < NC; ++c)
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
+          for (int v = 0; v < NV; ++v) {
+            const double d = dtb * (zv[0][c][v] + zv[1][c][v] + zv[2][c][v]);
 #pragma unroll
-          for (int h = 0; h < 3; ++h) {
-            double s = 0.0;
-#pragma unroll
-            for (int g = 0; g < 3; ++g)
-              s = fma(M.t[h * 3 + g], zv[g][c][v], s);
-            acc[h][c][v] = fma(det, s, acc[h][c][v]);
+            for (int h = 0; h < 3; ++h)
+              acc[h][c][v] = fma(dta, zv[h][c][v], acc[h][c][v] + d);
           }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int h = 0; h < 3; ++h) {
+              double s = 0.0;
+#pragma unroll
+              for (int g = 0; g < 3; ++g)
+                s = fma(M.t[h * 3 + g], zv[g][c][v], s);
+              acc[h][c][v] = fma(det, s, acc[h][c][v]);
+            }
+      }
     };
     using S0 = std::integral_constant<int, 0>;
     using S1 = std::integral_constant<int, 1>;
@@ -361,14 +374,22 @@ static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
   const int64_t items = n_strips * ((a.layers + W - 1) / W);
   const int64_t warps = (items + segs - 1) / segs;
   const unsigned grid = grid_for(warps * 32, 256, 8);
-#define PM_SR(WW)                                                            \
+  const bool sym = kron_sym3(M);
+#define PM_SR2(WW, SS)                                                       \
   do {                                                                       \
     const size_t smem = sr_smem<LY, WW>();                                   \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
-        k_strip_red<LY, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-        (int)smem));                                                         \
-    k_strip_red<LY, WW><<<grid, 256, smem, a.s>>>(                           \
+        k_strip_red<LY, WW, SS>,                                             \
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
+    k_strip_red<LY, WW, SS><<<grid, 256, smem, a.s>>>(                       \
         M, strip_ptr, steps, n_strips, a.layers, a.coords, a.x, a.y);        \
+  } while (0)
+#define PM_SR(WW)                                                            \
+  do {                                                                       \
+    if (sym)                                                                 \
+      PM_SR2(WW, true);                                                      \
+    else                                                                     \
+      PM_SR2(WW, false);                                                     \
   } while (0)
   if (W == 32)
     PM_SR(32);
@@ -381,6 +402,7 @@ static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
     return PM_EINVAL;
   }
 #undef PM_SR
+#undef PM_SR2
   PM_LAUNCH_CHECK("k_strip_red");
   return PM_OK;
 }

@@ -77,6 +77,20 @@ def default_quadrature(element: PrismElement) -> QuadratureRule:
                             max(2, 2 * deg[element.line]))
 
 
+def kron_reproduces(element: PrismElement, kron, mref) -> bool:
+    """``Mref[j,j'] == δ(comp) Mtri[h,h'] Mline[v,v']`` to round-off?"""
+    if kron is None:
+        return False
+    mtri, mline = kron
+    h = np.asarray(element.slot_h)
+    v = np.asarray(element.slot_v)
+    c = np.asarray(element.slot_comp)
+    rebuilt = (mtri[h[:, None], h[None, :]] * mline[v[:, None], v[None, :]] *
+               (c[:, None] == c[None, :]))
+    scale = max(float(np.abs(mref).max()), 1e-300)
+    return bool(np.abs(rebuilt - mref).max() <= 1e-13 * scale)
+
+
 def _as_device(a, dev):
     import torch
     if isinstance(a, Field):
@@ -113,7 +127,10 @@ class MassOperator:
         # element (their slot -> basis map is a compile-time table)
         default = element_for_layout(fs.layout) if element is not None \
             else self.element
-        self.kron_ok = default == self.element
+        # ... and factors whose tensor product is Mref (a rule that is not
+        # the tensor rule of its degrees would get the dense generic kernel)
+        self.kron_ok = default == self.element and \
+            kron_reproduces(self.element, self.kron, self.mref)
         self.share = sharing_class(fs.layout)
         self.k = fs.num_slots
         self.schedule = schedule

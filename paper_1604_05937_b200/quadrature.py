@@ -241,12 +241,45 @@ def reference_mass_matrix(element: PrismElement, rule: QuadratureRule):
     return np.ascontiguousarray(M)
 
 
+def tensor_factors(rule: QuadratureRule):
+    """Split a prism rule into its triangle and interval rules:
+    ``((tri points (nt,2), tri weights), (line points (nl,), line weights))``
+    when the points are the product grid (triangle index slowest, as
+    ``prism_quadrature`` builds them) and the weights the outer product;
+    ``None`` otherwise."""
+    pts = np.asarray(rule.points, dtype=np.float64)
+    w = np.asarray(rule.weights, dtype=np.float64)
+    n = w.shape[0]
+    if n == 0:
+        return None
+    same = np.all(pts[:, :2] == pts[0, :2], axis=1)
+    nl = int(np.argmin(same)) if not same.all() else n
+    if n % nl:
+        return None
+    nt = n // nl
+    P = pts.reshape(nt, nl, 3)
+    W = w.reshape(nt, nl)
+    tri, line = P[:, 0, :2], P[0, :, 2]
+    wt = W.sum(axis=1)
+    if wt[0] == 0:
+        return None
+    wl = W[0] / wt[0]
+    ok = (np.array_equal(P[:, :, :2], np.broadcast_to(tri[:, None, :],
+                                                        (nt, nl, 2))) and
+          np.array_equal(P[:, :, 2], np.broadcast_to(line[None, :], (nt, nl)))
+          and np.allclose(W, np.outer(wt, wl), rtol=1e-14, atol=0))
+    return ((tri, wt), (line, wl)) if ok else None
+
+
 def kronecker_factors(element: PrismElement, rule: QuadratureRule):
     """(Mtri, Mline) with Mref[j,j'] = delta(comp) Mtri[h,h'] Mline[v,v']:
-    the triangle / interval mass matrices under the rule's two factors
-    (exact product structure of the tensor-product rule)."""
-    tp, tw = triangle_rule(rule.tri_degree)
-    lp, lw = line_rule(rule.line_degree)
+    the triangle / interval mass matrices under the rule's own two factors
+    (``tensor_factors``); ``None`` for a rule that is not a tensor product
+    (the dense generic kernel then applies Mref)."""
+    f = tensor_factors(rule)
+    if f is None:
+        return None
+    (tp, tw), (lp, lw) = f
     T = tri_basis(element.tri, tp[:, 0], tp[:, 1])
     L = line_basis(element.line, lp)
     return (np.ascontiguousarray((T * tw) @ T.T),

@@ -1,6 +1,14 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "DG or stream or host" 2>&1 | tail -1
-: > gpurun_out/dg.jsonl
-for c in C2 C2 C4-DG1xDG1-rcm-L20 C4-DG1xDG1-rcm-L100 C4-DG1xDG1-random-L100 C4-DG0xDG0-rcm-L50; do
-timeout 300 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/dg.jsonl
-done
-python tools/summarize.py gpurun_out/dg.jsonl
+bash tools/ncu_one.sh C5a auto "k_strip_red" C5a_sr_r2
+python tools/ncu_summary.py gpurun_out/prof_C5a_sr_r2.ncu-rep > gpurun_out/ncu_C5a_sr_r2.txt 2>&1
+cat gpurun_out/ncu_C5a_sr_r2.txt
+ncu -i gpurun_out/prof_C5a_sr_r2.ncu-rep --page raw --csv 2>/dev/null | python -c "
+import csv,sys
+r=list(csv.reader(sys.stdin))
+h=r[0]; v=r[2] if len(r)>2 else r[1]
+for name,val in zip(h,v):
+    if 'warp_issue_stalled' in name and 'pct' in name and 'not_issued' not in name:
+        try:
+            if float(val)>2: print(name,val)
+        except: pass
+" > gpurun_out/stalls_C5a.txt
+cat gpurun_out/stalls_C5a.txt
