@@ -77,6 +77,22 @@ def default_quadrature(element: PrismElement) -> QuadratureRule:
                             max(2, 2 * deg[element.line]))
 
 
+def tri_permutation_invariant(mtri) -> bool:
+    """``Mtri[p(i), p(j)] == Mtri[i, j]`` for every permutation p of the
+    three vertices (edges, NH = 6, follow: edge e is opposite vertex e)."""
+    from itertools import permutations
+    mtri = np.asarray(mtri)
+    nh = mtri.shape[0]
+    tol = 1e-14 * max(float(np.abs(mtri).max()), 1e-300)
+    for p in permutations(range(3)):
+        idx = list(p) + ([3 + q for q in p] if nh == 6 else [])
+        if nh not in (3, 6):
+            return False
+        if np.abs(mtri[np.ix_(idx, idx)] - mtri).max() > tol:
+            return False
+    return True
+
+
 def kron_reproduces(element: PrismElement, kron, mref) -> bool:
     """``Mref[j,j'] == δ(comp) Mtri[h,h'] Mline[v,v']`` to round-off?"""
     if kron is None:
@@ -172,7 +188,19 @@ class MassOperator:
     @property
     def strip_ok(self) -> bool:
         d = tuple(self.fs.layout.delta6())
-        return d in _STRIP_LAYOUTS
+        return d in _STRIP_LAYOUTS and self.strip_invariant
+
+    @property
+    def stripred_ok(self) -> bool:
+        d = tuple(self.fs.layout.delta6())
+        return d in _STRIPRED_LAYOUTS and self.strip_invariant
+
+    @property
+    def strip_invariant(self) -> bool:
+        """The strip kernels place a cell's vertices by window slot, not by
+        the cell's local vertex order: valid when the triangle factor is
+        invariant under the vertex permutations (every symmetric rule)."""
+        return self.kron_ok and tri_permutation_invariant(self.kron[0])
 
     @property
     def dg_only(self) -> bool:
@@ -289,12 +317,12 @@ class MassOperator:
         if sched == "auto" and self.share == 2:
             # measured fastest (profiles/): global strips for vertex-column
             # layouts, the warp-per-column kernel otherwise
-            sched = "stripred" if tuple(self.fs.layout.delta6()) in \
-                _STRIPRED_LAYOUTS else "column"
+            sched = "stripred" if self.stripred_ok else "column"
         if sched == "stripred":
-            if tuple(self.fs.layout.delta6()) not in _STRIPRED_LAYOUTS:
+            if not self.stripred_ok:
                 raise ValueError(
-                    f"the strip schedule needs a vertex-column layout, got "
+                    f"the strip schedule needs a vertex-column layout and a "
+                    f"vertex-permutation invariant triangle factor, got "
                     f"{self.fs.layout.name}")
             strips, W = self._global_strips()
             import os
@@ -314,7 +342,8 @@ class MassOperator:
         if sched == "strip":
             if not self.strip_ok:
                 raise ValueError(
-                    f"the strip schedule needs a vertex-column layout, got "
+                    f"the strip schedule needs a vertex-column layout and a "
+                    f"vertex-permutation invariant triangle factor, got "
                     f"{self.fs.layout.name}")
             plan, dplan = self._strip_plan()
             out = torch.empty_like(y) if accumulate else y

@@ -200,10 +200,8 @@ class ShardedMassOperator:
         dev = self.op._dev
         self.d_cells = torch.from_numpy(self.shard.cells).to(dev)
         # vertex-column layouts: sequential strips over the rank's block
-        from .kernels import _STRIPRED_LAYOUTS
         self.strips = (self.op._global_strips(cells=self.shard.cells)
-                       if tuple(fs.layout.delta6()) in _STRIPRED_LAYOUTS and
-                       self.op.kron_ok else None)
+                       if self.op.stripred_ok else None)
         self.halo = HaloExchange(fs, self.shard, device=dev)
         self._lib = _lib
 

@@ -45,6 +45,20 @@ def test_asymmetric_tensor_rule_factors():
     assert not np.allclose(np.diag(t), t[0, 0])
 
 
+def test_default_rules_are_permutation_invariant():
+    from paper_1604_05937_b200.fspace import P2_LAYOUT, VP1_LAYOUT
+    from paper_1604_05937_b200.kernels import (default_quadrature,
+                                               tri_permutation_invariant)
+    for lay in (builtin_layout("CG1", "CG1"), builtin_layout("CG1", "DG1"),
+                P2_LAYOUT, VP1_LAYOUT):
+        el = element_for_layout(lay)
+        assert tri_permutation_invariant(
+            kronecker_factors(el, default_quadrature(el))[0]), lay.name
+    el = element_for_layout(builtin_layout("CG1", "CG1"))
+    assert not tri_permutation_invariant(
+        kronecker_factors(el, _asym_tensor_rule())[0])
+
+
 def test_non_tensor_rule_has_no_factors():
     el = element_for_layout(builtin_layout("CG1", "CG1"))
     rule = _non_tensor_rule()
@@ -74,8 +88,16 @@ def test_custom_rule_matches_dense_assembler(rule, layout, schedule):
     q = _asym_tensor_rule() if rule == "asym" else _non_tensor_rule()
     op = MassOperator(fs, q, schedule=schedule)
     assert op.kron_ok == (rule == "asym")
+    # an unsymmetric triangle rule is not invariant under vertex
+    # permutations: the strip kernels (window-slot placement) refuse it; a
+    # non-tensor rule has no factors (every schedule: dense generic kernel)
+    assert not op.strip_invariant
     coords = extrude_coordinates(base.coords, 5, mesh.layer_height)
     x = np.random.default_rng(1).uniform(-1, 1, fs.total_dofs)
+    if schedule == "stripred" and rule == "asym":
+        with pytest.raises(ValueError, match="permutation invariant"):
+            op.apply(torch.from_numpy(x).cuda(), coords)
+        return
     y = op.apply(torch.from_numpy(x).cuda(), coords).cpu().numpy()
     ref = verification.dense_mass_action(fs, x, coords.cpu().numpy(), op.mref)
     assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()

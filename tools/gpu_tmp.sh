@@ -1,14 +1,6 @@
-bash tools/ncu_one.sh C5a auto "k_strip_red" C5a_sr_r2
-python tools/ncu_summary.py gpurun_out/prof_C5a_sr_r2.ncu-rep > gpurun_out/ncu_C5a_sr_r2.txt 2>&1
-cat gpurun_out/ncu_C5a_sr_r2.txt
-ncu -i gpurun_out/prof_C5a_sr_r2.ncu-rep --page raw --csv 2>/dev/null | python -c "
-import csv,sys
-r=list(csv.reader(sys.stdin))
-h=r[0]; v=r[2] if len(r)>2 else r[1]
-for name,val in zip(h,v):
-    if 'warp_issue_stalled' in name and 'pct' in name and 'not_issued' not in name:
-        try:
-            if float(val)>2: print(name,val)
-        except: pass
-" > gpurun_out/stalls_C5a.txt
-cat gpurun_out/stalls_C5a.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_quadrature_rules.py -m gpu -x -q -k "strip or P2 or smoke or host or custom or VP1 or CG1" 2>&1 | tail -2
+: > gpurun_out/cg.jsonl
+for c in C5a C5b C4-CG1xCG1-rcm-L100 C4-VP1-rcm-L50 C4-CG1xDG1-rcm-L50; do
+  timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/cg.jsonl
+done
+python tools/summarize.py gpurun_out/cg.jsonl
