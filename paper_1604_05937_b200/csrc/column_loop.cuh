@@ -31,7 +31,42 @@ struct KronMat {
   // Mtri = ta I + tb J (3 x 3 with equal diagonal and equal off-diagonal
   // entries: P1 triangles under any symmetric rule), see kron_sym3
   double ta, tb;
+  // 6 x 6 (vertices 0-2, edges 3-5, edge e opposite vertex e) invariant
+  // under the vertex permutations: every 3 x 3 block is a I + b J,
+  // p = {a1, a2 (vertex-vertex), c1, c2 (edge-edge), bm, b2 (vertex-edge)}
+  double p[6];
 };
+
+// Does the 3 x 3 block at (r0, c0) of the nh x nh matrix t have the form
+// a I + b J (to a relative 4 ulp of `big`)?
+inline bool block_sym(const double *t, int nh, int r0, int c0, double big,
+                      double *a, double *b) {
+  double d = 0, o = 0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) (i == j ? d : o) += t[(r0 + i) * nh + c0 + j];
+  d /= 3, o /= 6;
+  const double tol = 4 * 2.220446049250313e-16 * big;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (fabs(t[(r0 + i) * nh + c0 + j] - (i == j ? d : o)) > tol)
+        return false;
+  *a = d - o;
+  *b = o;
+  return true;
+}
+
+// The 6 x 6 triangle factor of P2 in the block form of KronMat::p?
+inline bool kron_sym6(KronMat &M) {
+  double big = 0;
+  for (int i = 0; i < 36; ++i) big = fmax(big, fabs(M.t[i]));
+  double q[2];
+  return block_sym(M.t, 6, 0, 0, big, &M.p[0], &M.p[1]) &&
+         block_sym(M.t, 6, 3, 3, big, &M.p[2], &M.p[3]) &&
+         block_sym(M.t, 6, 0, 3, big, &M.p[4], &M.p[5]) &&
+         block_sym(M.t, 6, 3, 0, big, &q[0], &q[1]) &&
+         fabs(q[0] - M.p[4]) <= 8 * 2.220446049250313e-16 * big &&
+         fabs(q[1] - M.p[5]) <= 8 * 2.220446049250313e-16 * big;
+}
 
 // Does the 3 x 3 triangle factor have the form ta I + tb J (to a relative
 // 4 ulp)?  Fills ta, tb from the averaged diagonal / off-diagonal.

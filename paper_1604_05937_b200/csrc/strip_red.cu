@@ -430,7 +430,7 @@ template <class LY, int W> constexpr int sre_entry() {
 constexpr int kSreThreads = PM_SRE_THREADS;
 constexpr int kSreWarps = kSreThreads / 32;
 
-template <class LY, int W, int K = LY::K>
+template <class LY, int W, bool SYM, int K = LY::K>
 __global__ void __launch_bounds__(kSreThreads, 1)
 k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
               const int32_t *__restrict__ steps,
@@ -629,21 +629,39 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
       const double det = act ? dj : 0.0;
       // triangle stage (h: vertices 0-2, edges 3-5), det folded into the
       // accumulation
+      if constexpr (SYM) { // block form a I + b J (KronMat::p)
+        const double da1 = det * M.p[0], da2 = det * M.p[1];
+        const double dc1 = det * M.p[2], dc2 = det * M.p[3];
+        const double dbm = det * M.p[4], db2 = det * M.p[5];
 #pragma unroll
-      for (int v = 0; v < NV; ++v)
+        for (int v = 0; v < NV; ++v) {
+          const double sv = zv[0][v] + zv[1][v] + zv[2][v];
+          const double se = ze[0][v] + ze[1][v] + ze[2][v];
+          const double tv = fma(da2, sv, db2 * se);
+          const double te = fma(db2, sv, dc2 * se);
 #pragma unroll
-        for (int h = 0; h < 6; ++h) {
-          double s = 0.0;
-#pragma unroll
-          for (int g = 0; g < 3; ++g) s = fma(M.t[h * 6 + g], zv[g][v], s);
-#pragma unroll
-          for (int g = 0; g < 3; ++g)
-            s = fma(M.t[h * 6 + 3 + g], ze[g][v], s);
-          if (h < 3)
-            av[h][v] = fma(det, s, av[h][v]);
-          else
-            ae[h - 3][v] = fma(det, s, ae[h - 3][v]);
+          for (int h = 0; h < 3; ++h) {
+            av[h][v] = fma(da1, zv[h][v], fma(dbm, ze[h][v], av[h][v] + tv));
+            ae[h][v] = fma(dbm, zv[h][v], fma(dc1, ze[h][v], ae[h][v] + te));
+          }
         }
+      } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int h = 0; h < 6; ++h) {
+            double s = 0.0;
+#pragma unroll
+            for (int g = 0; g < 3; ++g) s = fma(M.t[h * 6 + g], zv[g][v], s);
+#pragma unroll
+            for (int g = 0; g < 3; ++g)
+              s = fma(M.t[h * 6 + 3 + g], ze[g][v], s);
+            if (h < 3)
+              av[h][v] = fma(det, s, av[h][v]);
+            else
+              ae[h - 3][v] = fma(det, s, ae[h - 3][v]);
+          }
+      }
     };
     using S0 = std::integral_constant<int, 0>;
     using S1 = std::integral_constant<int, 1>;
@@ -685,16 +703,24 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
   const int64_t items = n_strips * ((a.layers + W - 1) / W);
   const int64_t warps = (items + segs - 1) / segs;
   const unsigned grid = grid_for(warps * 32, kSreThreads, 4);
+  const bool sym = kron_sym6(M);
 #define PM_SRE(WW)                                                           \
+  do {                                                                       \
+    if (sym)                                                                 \
+      PM_SRE2(WW, true);                                                     \
+    else                                                                     \
+      PM_SRE2(WW, false);                                                    \
+  } while (0)
+#define PM_SRE2(WW, SS)                                                      \
   do {                                                                       \
     const size_t smem = sizeof(double) *                                     \
                             (kSreWarps * kSrDepth * (32 / WW) + 1) *         \
                             sre_entry<LY, WW>() +                            \
                         sizeof(int) * kSreWarps * (32 / WW) * 3 * kSrIds;    \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
-        k_strip_red_e<LY, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-        (int)smem));                                                         \
-    k_strip_red_e<LY, WW><<<grid, kSreThreads, smem, a.s>>>(                         \
+        k_strip_red_e<LY, WW, SS>,                                           \
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
+    k_strip_red_e<LY, WW, SS><<<grid, kSreThreads, smem, a.s>>>(                         \
         M, strip_ptr, steps, steps_e, n_strips, a.layers, e_start, a.coords, \
         a.x, a.y);                                                           \
   } while (0)
@@ -709,6 +735,7 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
     return PM_EINVAL;
   }
 #undef PM_SRE
+#undef PM_SRE2
   PM_LAUNCH_CHECK("k_strip_red_e");
   return PM_OK;
 }
