@@ -21,6 +21,7 @@
 #include "column_layout.cuh"
 #include "pm_ptx.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace pm {
@@ -65,23 +66,27 @@ template <class LY> constexpr int sr_min_blocks() {
   return LY::CH0 > 2 ? 1 : 2; // measured: 3/SM (scalar) and 2/SM (3-vector) slower
 }
 
-// Padded ring entries of the strip kernel: the field part and the
-// coordinate part are whole rows of W values, so every lane issues every
-// copy (cp.async with a 0/8-byte source size: lanes past the chunk
-// zero-fill their row slot instead of being predicated off).
-template <class LY, int W> constexpr int sr_frows() {
-  return (sr_fs<LY, W>() + W - 1) / W;
+// Padded ring entries of the strip kernel (a chunk of CW = W*L levels):
+// the field part and the coordinate part are whole rows of W values, so
+// every lane issues every copy (cp.async with a 0/8-byte source size:
+// lanes past the chunk zero-fill their row slot instead of being
+// predicated off).
+template <class LY, int CW> constexpr int sr_fsz() {
+  return CW * LY::CH0 + LY::LV0;
 }
-template <class LY, int W> constexpr int sr_crows() {
-  return (3 * (W + 1) + W - 1) / W;
+template <class LY, int W, int L> constexpr int sr_frows() {
+  return (sr_fsz<LY, W * L>() + W - 1) / W;
 }
-template <class LY, int W> constexpr int sr_pentry() {
-  return (sr_frows<LY, W>() + sr_crows<LY, W>()) * W;
+template <class LY, int W, int L> constexpr int sr_crows() {
+  return (3 * (W * L + 1) + W - 1) / W;
+}
+template <class LY, int W, int L> constexpr int sr_pentry() {
+  return (sr_frows<LY, W, L>() + sr_crows<LY, W, L>()) * W;
 }
 constexpr int kSrIds = 64; // strip vertex ids staged per segment
-template <class LY, int W> constexpr size_t sr_smem() {
+template <class LY, int W, int L> constexpr size_t sr_smem() {
   return sizeof(double) * ((size_t)8 * kSrDepth * (32 / W) + 1) *
-             sr_pentry<LY, W>() +
+             sr_pentry<LY, W, L>() +
          sizeof(int) * 8 * (32 / W) * kSrIds;
 }
 
@@ -102,19 +107,27 @@ __device__ __forceinline__ T *col_at(T *base, int v, int stride_bytes) {
                                (int64_t)v * stride_bytes);
 }
 
+template <class LY, int L> constexpr int sr_blocks() {
+  return (LY::CH0 > 2 || L > 1) ? 1 : 2;
+}
+
 // The element kernel split along the window: y = det (Mtri (x) Mline) x.
 // The interval stage z = Mline x only involves one vertex column, so it is
 // applied once when the vertex enters the window (not in each of its three
 // cells); per cell only the triangle stage runs, with det folded into the
 // accumulation: acc[h] = fma(det, sum_g Mtri[h][g] z[g], acc[h]).
-template <class LY, int W, bool SYM, int K = LY::K>
-__global__ void __launch_bounds__(256, sr_min_blocks<LY>())
+// L consecutive levels per lane (lane sl: levels l0 + L*sl + j, j < L):
+// the level between two of them is read once, and the per-step overhead
+// (ids, ring wait, addressing, loop) is paid once per L cell-layers.
+template <class LY, int W, bool SYM, int L, int K = LY::K>
+__global__ void __launch_bounds__(256, sr_blocks<LY, L>())
 k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
             const int32_t *__restrict__ steps, int64_t n_strips, int layers,
             const double *__restrict__ coords, const double *__restrict__ x,
             double *__restrict__ y) {
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int SEGS = 32 / W;
+  constexpr int CW = W * L; // levels per chunk
   constexpr int LV = LY::LV0;
   constexpr int CH = LY::CH0;
   constexpr int LVA = LV > 0 ? LV : 1;
@@ -124,9 +137,9 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
   // copies, connecting channel v*NC + c (the slot table of fspace.py)
   static_assert(NH == 3 && NC * NV == CH + LV, "vertex-column layout");
   static_assert(LV == 0 || (LV == NC && NV == 2 && CH == LV), "strip layout");
-  constexpr int FR = sr_frows<LY, W>(), CR = sr_crows<LY, W>();
+  constexpr int FR = sr_frows<LY, W, L>(), CR = sr_crows<LY, W, L>();
   constexpr int FP = FR * W;                 // coordinate part offset
-  constexpr int ES = sr_pentry<LY, W>();
+  constexpr int ES = sr_pentry<LY, W, L>();
   const int lane = threadIdx.x & 31;
   const int sl = lane % W, seg = lane / W;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -148,46 +161,50 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
   // work item = (strip, layer chunk), chunk fastest: the chunks of a strip
   // run side by side, so the sectors two chunks of a vertex column share
   // are fetched once (neighbouring strips are still close in time)
-  const int n_chunks = (layers + W - 1) / W;
+  const int n_chunks = (layers + CW - 1) / CW;
   const int64_t n_items = n_strips * n_chunks;
   for (int64_t i0 = warp * SEGS; i0 < n_items; i0 += n_warps * SEGS) {
     const int64_t item = i0 + seg;
     const bool has = item < n_items;
     const int64_t si = has ? item / n_chunks : 0;
-    const int l0 = has ? (int)(item % n_chunks) * W : 0;
+    const int l0 = has ? (int)(item % n_chunks) * CW : 0;
     const int k0 = has ? __ldg(strip_ptr + si) : 0;
     const int len = has ? __ldg(strip_ptr + si + 1) - k0 : 0;
     int maxlen = len;
 #pragma unroll
     for (int o = W; o < 32; o <<= 1)
       maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
-    const int nl = has ? min(W, layers - l0) : 0;
-    const bool lane_ok = sl < nl;
+    const int nl = has ? min(CW, layers - l0) : 0;
+    const int lb = L * sl; // the lane's first level in the chunk
     // source sizes of the lane's copies (8 inside the chunk, else 0)
     int fz[FR], cz[CR];
 #pragma unroll
     for (int r = 0; r < FR; ++r) fz[r] = sl + W * r < nl * CH + LV ? 8 : 0;
 #pragma unroll
     for (int r = 0; r < CR; ++r) cz[r] = sl + W * r < 3 * (nl + 1) ? 8 : 0;
-    // the lane's element of every column chunk it touches
+    // the segment's chunk of every column (copies), the lane's first
+    // element of it (flushes)
     const double *xl = x + (int64_t)l0 * CH + sl;
     const double *cl0 = coords + 3 * (int64_t)l0 + sl;
-    double *yl = y + ((int64_t)l0 + sl) * CH;
-    // window vertex: interval-stage values z[c][v] at the lane's cell
-    // layer and the geometry the Jacobian needs, derived once on entry:
-    // xm, ym (mid-layer), dz; per-vertex accumulators acc[c][v]
-    double zv[3][NC][NV], gm[3][3], acc[3][NC][NV];
-    double *yc[3] = {yl, yl, yl}; // lane's element of the slot's column
+    double *yl = y + ((int64_t)l0 + lb) * CH;
+    // window vertex: interval-stage values z[j][c][v] at the lane's cell
+    // layers and the geometry the Jacobian needs, derived once on entry:
+    // xm, ym (mid-layer), dz; per-vertex accumulators acc[j][c][v]
+    double zv[3][L][NC][NV], gm[3][L][3], acc[3][L][NC][NV];
+    double *yc[3] = {yl, yl, yl}; // lane's first element of the column
     bool live[3] = {false, false, false};
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
+    for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
+      for (int j = 0; j < L; ++j) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) zv[a][c][v] = 0.0, acc[a][c][v] = 0.0;
+        for (int c = 0; c < NC; ++c)
 #pragma unroll
-      for (int q = 0; q < 3; ++q) gm[a][q] = 0.0;
-    }
+          for (int v = 0; v < NV; ++v)
+            zv[a][j][c][v] = 0.0, acc[a][j][c][v] = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) gm[a][j][q] = 0.0;
+      }
     // the strip's vertex ids, staged kSrIds at a time (one broadcast LDS
     // per step)
     auto load_ids = [&](int base) {
@@ -203,7 +220,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
     // per-warp shared-memory prefetch ring, kSrDepth steps deep: the
     // segment copies its vertex's chunk of the field and coordinate
     // columns contiguously (coalesced cp.async); lanes then read their
-    // own level (and the level above) out of shared memory.
+    // own levels (and the level above) out of shared memory.
     auto entry = [&](int slot) {
       return ring + (size_t)(slot * SEGS + seg) * ES;
     };
@@ -232,31 +249,48 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
 
     auto flush = [&](auto A_) {
       constexpr int A = decltype(A_)::value;
-      // back to the vertex column's layer block: bottom / connecting
-      // channels vb, top copies vt
-      double vb[CH], vt[LVA];
+      // back to the vertex column's layer blocks: per level j the bottom /
+      // connecting channels vb[j], the top copies of the lane's last level
+      // vt (added by the lane above, or by the chunk's last lane)
+      double vb[L][CH], vt[LVA];
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
+      for (int j = 0; j < L; ++j)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          if (LV == 0)
-            vb[v * NC + c] = acc[A][c][v];
-          else if (v == 0)
-            vb[c] = acc[A][c][v];
-          else
-            vt[c < LVA ? c : 0] = acc[A][c][v];
-          acc[A][c][v] = 0.0;
-        }
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const double a = acc[A][j][c][v];
+            if (LV == 0)
+              vb[j][v * NC + c] = a;
+            else if (v == 0)
+              vb[j][c] = a + (j > 0 ? vb[j][c] : 0.0);
+            else if (j + 1 < L)
+              vb[j + 1][c < LVA ? c : 0] = a; // summed when j+1 is visited
+            else
+              vt[c < LVA ? c : 0] = a;
+            acc[A][j][c][v] = 0.0;
+          }
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
-        double v = vb[c];
+        double v0 = vb[0][c];
         if (c < LV) {
           const double below = __shfl_up_sync(FULL, vt[c < LV ? c : 0], 1, W);
-          if (sl > 0) v += below;
+          if (sl > 0) v0 += below;
         }
-        if (live[A] && lane_ok) {
-          atomicAdd(yc[A] + c, v);
-          if (c < LV && sl == nl - 1) atomicAdd(yc[A] + CH + c, vt[c < LV ? c : 0]);
+        if (live[A]) {
+#pragma unroll
+          for (int j = 0; j < L; ++j)
+            if (lb + j < nl) atomicAdd(yc[A] + j * CH + c, j ? vb[j][c] : v0);
+          if (c < LV && lb + L - 1 == nl - 1)
+            atomicAdd(yc[A] + L * CH + c, vt[c < LV ? c : 0]);
+          if (c < LV && L > 1 && lb < nl && lb + L - 1 > nl - 1) {
+            // partial chunk ending inside this lane: its top is the level
+            // after the last valid one
+#pragma unroll
+            for (int j = 0; j + 1 < L; ++j)
+              if (lb + j == nl - 1)
+                atomicAdd(yc[A] + (j + 1) * CH + c, vb[j + 1][c]);
+          }
         }
       }
     };
@@ -275,69 +309,83 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       // (stale, possibly non-finite) ring slot; lanes past the chunk read
       // zero-filled values and are never flushed.
       const double *e = act ? entry(A) : sr_zero;
-      double fb[CH], ft[LVA];
+      double f[L + 1][CH], g[L + 1][3];
 #pragma unroll
-      for (int c = 0; c < CH; ++c) fb[c] = e[sl * CH + c];
+      for (int j = 0; j <= L; ++j) {
 #pragma unroll
-      for (int c = 0; c < LV; ++c) ft[c] = e[(sl + 1) * CH + c];
-      {
-        const double *g = e + FP + 3 * sl;
-        gm[A][0] = 0.5 * (g[0] + g[3]); // same operations as
-        gm[A][1] = 0.5 * (g[1] + g[4]); // prism_abs_detj
-        gm[A][2] = g[5] - g[2];
+        for (int c = 0; c < CH; ++c)
+          f[j][c] = (j < L || c < LV) ? e[(lb + j) * CH + c] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) g[j][q] = e[FP + 3 * (lb + j) + q];
+      }
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        gm[A][j][0] = 0.5 * (g[j][0] + g[j + 1][0]); // same operations as
+        gm[A][j][1] = 0.5 * (g[j][1] + g[j + 1][1]); // prism_abs_detj
+        gm[A][j][2] = g[j + 1][2] - g[j][2];
       }
       __syncwarp(); // reads done before the slot is refilled
       yc[A] = col_at(yl, rv[A], colb);
       live[A] = act;
       // interval stage of the entering vertex
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double s = 0.0;
-#pragma unroll
-          for (int w = 0; w < NV; ++w) {
-            const double xw = LV == 0 ? fb[w * NC + c]
-                              : w == 0 ? fb[c]
-                                       : ft[c < LVA ? c : 0];
-            s = fma(M.l[v * NV + w], xw, s);
-          }
-          zv[A][c][v] = s;
-        }
-      // refill ring slot A with the step kSrDepth ahead
-      rv[A] = fetch(k + kSrDepth, A);
-      if (FILL && A < 2) return; // window not full yet
-      // past the strip's end the window still holds two live vertices:
-      // the step contributes nothing
-      const double dj = prism_abs_detj_mid(gm[0][0], gm[0][1], gm[0][2],
-                                           gm[1][0], gm[1][1], gm[1][2],
-                                           gm[2][0], gm[2][1], gm[2][2]);
-      const double det = act ? dj : 0.0;
-      // triangle stage, det folded into the accumulation
-      if constexpr (SYM) { // Mtri = ta I + tb J
-        const double dta = det * M.ta, dtb = det * M.tb;
+      for (int j = 0; j < L; ++j)
 #pragma unroll
         for (int c = 0; c < NC; ++c)
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
-            const double d = dtb * (zv[0][c][v] + zv[1][c][v] + zv[2][c][v]);
+            double s = 0.0;
 #pragma unroll
-            for (int h = 0; h < 3; ++h)
-              acc[h][c][v] = fma(dta, zv[h][c][v], acc[h][c][v] + d);
-          }
-      } else {
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-#pragma unroll
-          for (int v = 0; v < NV; ++v)
-#pragma unroll
-            for (int h = 0; h < 3; ++h) {
-              double s = 0.0;
-#pragma unroll
-              for (int g = 0; g < 3; ++g)
-                s = fma(M.t[h * 3 + g], zv[g][c][v], s);
-              acc[h][c][v] = fma(det, s, acc[h][c][v]);
+            for (int w = 0; w < NV; ++w) {
+              const double xw = LV == 0 ? f[j][w * NC + c]
+                                : w == 0 ? f[j][c]
+                                         : f[j + 1][c];
+              s = fma(M.l[v * NV + w], xw, s);
             }
+            zv[A][j][c][v] = s;
+          }
+      // refill ring slot A with the step kSrDepth ahead
+      rv[A] = fetch(k + kSrDepth, A);
+      if (FILL && A < 2) return; // window not full yet
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        // past the strip's end the window still holds two live vertices:
+        // the step contributes nothing
+        const double dj = prism_abs_detj_mid(
+            gm[0][j][0], gm[0][j][1], gm[0][j][2], gm[1][j][0], gm[1][j][1],
+            gm[1][j][2], gm[2][j][0], gm[2][j][1], gm[2][j][2]);
+        // (with L > 1 a lane's upper level may lie past a partial chunk;
+        // its accumulator feeds the chunk's top level, so it must stay 0)
+        const double det =
+            (act && (L == 1 || lb + j < nl)) ? dj : 0.0;
+        // triangle stage, det folded into the accumulation
+        if constexpr (SYM) { // Mtri = ta I + tb J
+          const double dta = det * M.ta, dtb = det * M.tb;
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              const double d = dtb * (zv[0][j][c][v] + zv[1][j][c][v] +
+                                      zv[2][j][c][v]);
+#pragma unroll
+              for (int h = 0; h < 3; ++h)
+                acc[h][j][c][v] =
+                    fma(dta, zv[h][j][c][v], acc[h][j][c][v] + d);
+            }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+#pragma unroll
+              for (int h = 0; h < 3; ++h) {
+                double s = 0.0;
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                  s = fma(M.t[h * 3 + q], zv[q][j][c][v], s);
+                acc[h][j][c][v] = fma(det, s, acc[h][j][c][v]);
+              }
+        }
       }
     };
     using S0 = std::integral_constant<int, 0>;
@@ -360,6 +408,51 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
   }
 }
 
+// levels per lane (PM_STRIP_L tuning knob: 1 or 2)
+static int strip_levels() {
+  const char *e = getenv("PM_STRIP_L");
+  return e && atoi(e) == 2 ? 2 : 1;
+}
+
+template <class LY, int W, bool SYM, int L>
+static int strip_red_launch(const LoopArgs &a, const KronMat &M,
+                            const int32_t *strip_ptr, const int32_t *steps,
+                            int64_t n_strips) {
+  const int segs = 32 / W;
+  const int64_t items = n_strips * ((a.layers + W * L - 1) / (W * L));
+  const int64_t warps = (items + segs - 1) / segs;
+  const unsigned grid = grid_for(warps * 32, 256, 8);
+  const size_t smem = sr_smem<LY, W, L>();
+  PM_CUDA_TRY(cudaFuncSetAttribute(k_strip_red<LY, W, SYM, L>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+  k_strip_red<LY, W, SYM, L><<<grid, 256, smem, a.s>>>(
+      M, strip_ptr, steps, n_strips, a.layers, a.coords, a.x, a.y);
+  PM_LAUNCH_CHECK("k_strip_red");
+  return PM_OK;
+}
+
+template <class LY, int W>
+static int strip_red_w(const LoopArgs &a, const KronMat &M, bool sym,
+                       int L, const int32_t *strip_ptr, const int32_t *steps,
+                       int64_t n_strips) {
+  if constexpr (LY::CH0 <= 2 && W <= 16) {
+    if (L == 2 && sym)
+      return strip_red_launch<LY, W, true, 2>(a, M, strip_ptr, steps,
+                                              n_strips);
+  }
+  if (false) {
+    if (sym)
+      return strip_red_launch<LY, W, true, 2>(a, M, strip_ptr, steps,
+                                              n_strips);
+    return strip_red_launch<LY, W, false, 2>(a, M, strip_ptr, steps,
+                                             n_strips);
+  }
+  if (sym)
+    return strip_red_launch<LY, W, true, 1>(a, M, strip_ptr, steps, n_strips);
+  return strip_red_launch<LY, W, false, 1>(a, M, strip_ptr, steps, n_strips);
+}
+
 template <class LY>
 static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
                        const int32_t *steps, int64_t n_strips, int W) {
@@ -370,41 +463,16 @@ static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
   KronMat M;
   for (int i = 0; i < LY::NH * LY::NH; ++i) M.t[i] = a.mtri[i];
   for (int i = 0; i < LY::NV * LY::NV; ++i) M.l[i] = a.mline[i];
-  const int segs = 32 / W;
-  const int64_t items = n_strips * ((a.layers + W - 1) / W);
-  const int64_t warps = (items + segs - 1) / segs;
-  const unsigned grid = grid_for(warps * 32, 256, 8);
   const bool sym = kron_sym3(M);
-#define PM_SR2(WW, SS)                                                       \
-  do {                                                                       \
-    const size_t smem = sr_smem<LY, WW>();                                   \
-    PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
-        k_strip_red<LY, WW, SS>,                                             \
-        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
-    k_strip_red<LY, WW, SS><<<grid, 256, smem, a.s>>>(                       \
-        M, strip_ptr, steps, n_strips, a.layers, a.coords, a.x, a.y);        \
-  } while (0)
-#define PM_SR(WW)                                                            \
-  do {                                                                       \
-    if (sym)                                                                 \
-      PM_SR2(WW, true);                                                      \
-    else                                                                     \
-      PM_SR2(WW, false);                                                     \
-  } while (0)
-  if (W == 32)
-    PM_SR(32);
-  else if (W == 16)
-    PM_SR(16);
-  else if (W == 8)
-    PM_SR(8);
-  else {
+  const int L = strip_levels();
+  switch (W) {
+  case 32: return strip_red_w<LY, 32>(a, M, sym, L, strip_ptr, steps, n_strips);
+  case 16: return strip_red_w<LY, 16>(a, M, sym, L, strip_ptr, steps, n_strips);
+  case 8: return strip_red_w<LY, 8>(a, M, sym, L, strip_ptr, steps, n_strips);
+  default:
     set_error("strip chunk width must be 8, 16 or 32 (got %d)", W);
     return PM_EINVAL;
   }
-#undef PM_SR
-#undef PM_SR2
-  PM_LAUNCH_CHECK("k_strip_red");
-  return PM_OK;
 }
 
 

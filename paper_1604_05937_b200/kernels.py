@@ -154,6 +154,7 @@ class MassOperator:
         self._patch = None
         self._strip = None
         self._gstrips = None
+        self._strip_inv = None
         self._hbuf = None
         self._dev = _lib.cuda_device()
         self.cmap = fs.device_cell_map()
@@ -199,8 +200,12 @@ class MassOperator:
     def strip_invariant(self) -> bool:
         """The strip kernels place a cell's vertices by window slot, not by
         the cell's local vertex order: valid when the triangle factor is
-        invariant under the vertex permutations (every symmetric rule)."""
-        return self.kron_ok and tri_permutation_invariant(self.kron[0])
+        invariant under the vertex permutations (every symmetric rule).
+        Evaluated once per operator (apply() is on the timed path)."""
+        if self._strip_inv is None:
+            self._strip_inv = bool(self.kron_ok and
+                                   tri_permutation_invariant(self.kron[0]))
+        return self._strip_inv
 
     @property
     def dg_only(self) -> bool:
@@ -298,6 +303,20 @@ class MassOperator:
             d_order = torch.from_numpy(order).to(self._dev)
             self._coloring = (d_order, ptr)
         return self._coloring
+
+    def graph(self, x, coords, y, accumulate=False, schedule=None):
+        """One ``apply`` on fixed device buffers captured as a CUDA graph
+        (``torch.cuda.CUDAGraph``; ``.replay()`` re-runs it on the current
+        stream): repeated application without per-call host work, for
+        launch-bound sizes and solver loops."""
+        import torch
+        self.apply(x, coords, y, accumulate=accumulate, schedule=schedule)
+        torch.cuda.synchronize()        # plans and kernel attributes ready
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.apply(x, coords, y, accumulate=accumulate, schedule=schedule)
+        torch.cuda.synchronize()
+        return g
 
     def apply(self, x, coords, y=None, accumulate=False, schedule=None,
               stream=None):
