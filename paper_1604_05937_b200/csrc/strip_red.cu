@@ -84,10 +84,19 @@ template <class LY, int W, int L> constexpr int sr_pentry() {
   return (sr_frows<LY, W, L>() + sr_crows<LY, W, L>()) * W;
 }
 constexpr int kSrIds = 64; // strip vertex ids staged per segment
+#ifndef PM_SR_VTHREADS
+#define PM_SR_VTHREADS 384
+#endif
+// CTA size: 256 threads, 384 for the 3-vector layouts (12 warps at <= 168
+// registers instead of 8 at 182)
+template <class LY> constexpr int sr_threads() {
+  return LY::CH0 > 2 ? PM_SR_VTHREADS : 256;
+}
 template <class LY, int W, int L> constexpr size_t sr_smem() {
-  return sizeof(double) * ((size_t)8 * kSrDepth * (32 / W) + 1) *
+  return sizeof(double) *
+             ((size_t)(sr_threads<LY>() / 32) * kSrDepth * (32 / W) + 1) *
              sr_pentry<LY, W, L>() +
-         sizeof(int) * 8 * (32 / W) * kSrIds;
+         sizeof(int) * (sr_threads<LY>() / 32) * (32 / W) * kSrIds;
 }
 
 __device__ __forceinline__ void sr_cp8z(double *dst, const double *src,
@@ -120,7 +129,7 @@ template <class LY, int L> constexpr int sr_blocks() {
 // the level between two of them is read once, and the per-step overhead
 // (ids, ring wait, addressing, loop) is paid once per L cell-layers.
 template <class LY, int W, bool SYM, int L, int K = LY::K>
-__global__ void __launch_bounds__(256, sr_blocks<LY, L>())
+__global__ void __launch_bounds__(sr_threads<LY>(), sr_blocks<LY, L>())
 k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
             const int32_t *__restrict__ steps, int64_t n_strips, int layers,
             const double *__restrict__ coords, const double *__restrict__ x,
@@ -150,12 +159,14 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
   extern __shared__ double sr_ring[];
   double *const ring =
       sr_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
-  const double *const sr_zero = sr_ring + (size_t)8 * kSrDepth * SEGS * ES;
-  int *const sid = reinterpret_cast<int *>(sr_ring + (size_t)(8 * kSrDepth *
+  constexpr int NWARP = sr_threads<LY>() / 32;
+  const double *const sr_zero =
+      sr_ring + (size_t)NWARP * kSrDepth * SEGS * ES;
+  int *const sid = reinterpret_cast<int *>(sr_ring + (size_t)(NWARP * kSrDepth *
                                                               SEGS + 1) * ES) +
                    ((threadIdx.x >> 5) * SEGS + seg) * kSrIds;
   for (int i = threadIdx.x; i < ES; i += blockDim.x)
-    sr_ring[(size_t)8 * kSrDepth * SEGS * ES + i] = 0.0;
+    sr_ring[(size_t)NWARP * kSrDepth * SEGS * ES + i] = 0.0;
   __syncthreads();
 
   // work item = (strip, layer chunk), chunk fastest: the chunks of a strip
@@ -421,12 +432,13 @@ static int strip_red_launch(const LoopArgs &a, const KronMat &M,
   const int segs = 32 / W;
   const int64_t items = n_strips * ((a.layers + W * L - 1) / (W * L));
   const int64_t warps = (items + segs - 1) / segs;
-  const unsigned grid = grid_for(warps * 32, 256, 8);
+  constexpr int T = sr_threads<LY>();
+  const unsigned grid = grid_for(warps * 32, T, 8);
   const size_t smem = sr_smem<LY, W, L>();
   PM_CUDA_TRY(cudaFuncSetAttribute(k_strip_red<LY, W, SYM, L>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-  k_strip_red<LY, W, SYM, L><<<grid, 256, smem, a.s>>>(
+  k_strip_red<LY, W, SYM, L><<<grid, T, smem, a.s>>>(
       M, strip_ptr, steps, n_strips, a.layers, a.coords, a.x, a.y);
   PM_LAUNCH_CHECK("k_strip_red");
   return PM_OK;
@@ -440,13 +452,6 @@ static int strip_red_w(const LoopArgs &a, const KronMat &M, bool sym,
     if (L == 2 && sym)
       return strip_red_launch<LY, W, true, 2>(a, M, strip_ptr, steps,
                                               n_strips);
-  }
-  if (false) {
-    if (sym)
-      return strip_red_launch<LY, W, true, 2>(a, M, strip_ptr, steps,
-                                              n_strips);
-    return strip_red_launch<LY, W, false, 2>(a, M, strip_ptr, steps,
-                                             n_strips);
   }
   if (sym)
     return strip_red_launch<LY, W, true, 1>(a, M, strip_ptr, steps, n_strips);
