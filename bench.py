@@ -71,8 +71,14 @@ def ncu_traffic(config):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: NVML in a tight loop (≈ every 0.2 ms, so even a few-ms region
+    gets many samples), nvidia-smi as the fallback."""
 
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,"
          "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,"
@@ -81,26 +87,60 @@ class ClockSampler:
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.source = None
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def _run_nvml(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        try:
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = [(n, getattr(nv, a)) for n, a in self.REASONS]
+            self.source = "nvml"
+            while True:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                self.mx.append(mx)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.reasons.update(n for n, b in bits if r & b)
+                if self._stop.wait(0.0002):
+                    break
+        finally:
+            nv.nvmlShutdown()
+
+    def _run_smi(self):
+        self.source = "nvidia-smi"
+        names = [n for n, _a in self.REASONS]
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
                     ["nvidia-smi", "-i", str(self.index),
                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
                     capture_output=True, text=True, timeout=5).stdout
-                for line in out.strip().splitlines():
-                    self.rows.append([c.strip() for c in line.split(",")])
             except (OSError, subprocess.SubprocessError):
                 return
+            for line in out.strip().splitlines():
+                r = [c.strip() for c in line.split(",")]
+                if r[1].replace(".", "").isdigit():
+                    self.sm.append(float(r[1]))
+                if r[2].replace(".", "").isdigit():
+                    self.mx.append(float(r[2]))
+                self.reasons.update(names[i] for i in range(4)
+                                    if len(r) > 5 + i and r[5 + i] == "Active")
             self._stop.wait(0.2)
+
+    def _run(self):
+        try:
+            self._run_nvml()
+        except Exception:
+            self._run_smi()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.05)    # the sampler is running before the region starts
         return self
 
     def __exit__(self, *exc):
@@ -108,18 +148,13 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
                     "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
-                 "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 5 + i and r[5 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        return {"sm_mhz": float(np.median(self.sm)),
+                "sm_max_mhz": float(max(self.mx)) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": self.source}
 
 
 def dist_setup():
@@ -290,6 +325,7 @@ def run_sharded(args, w):
         t = torch.tensor([ms, kernel_ms, e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, kernel_ms, e2e_ms = (float(v) for v in t.tolist())
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, fs, x_np, args.cpu_seconds)
@@ -331,6 +367,32 @@ def run_sharded(args, w):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def pcie_duplex(x_host, y_host, xd):
+    """The e2e path's own roofline: the same H2D + D2H bytes as one step,
+    copied concurrently on two streams with no compute (best of 3, ms)."""
+    import torch
+    yd = torch.empty_like(xd)
+    up, down = torch.cuda.Stream(), torch.cuda.Stream()
+    best = None
+    for _ in range(3):
+        torch.cuda.synchronize()
+        e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+        e0.record()
+        up.wait_stream(torch.cuda.current_stream())
+        down.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(up):
+            yd.copy_(x_host, non_blocking=True)
+        with torch.cuda.stream(down):
+            y_host.copy_(xd, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(up)
+        torch.cuda.current_stream().wait_stream(down)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    return best
 
 
 def run_ours(args):
@@ -422,6 +484,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    pcie = pcie_duplex(x_host, y_host, x) if world == 1 else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, fs, x_np, args.cpu_seconds)
@@ -466,7 +530,8 @@ def run_ours(args):
                     "d2h_bytes_per_step": int(x_np.nbytes),
                     "ms_per_step": e2e_ms,
                     "path": "kernels.mass_action(fs, pinned host x, "
-                            "out=pinned host y)"},
+                            "out=pinned host y)",
+                    "copy_only_ms": pcie},
             "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
             "sm_count": sm,

@@ -212,7 +212,7 @@ class MassOperator:
         d = self.fs.layout.delta6()
         return not (d[0] or d[1] or d[2] or d[3] or d[4])
 
-    def apply_host(self, x_host, coords, y_host, chunks=8):
+    def apply_host(self, x_host, coords, y_host, chunks=None):
         """``y_host = M x_host`` for pinned host tensors, with the copies
         pipelined against the compute: for DG (2,1) fields the cell columns
         are contiguous, so chunk j+1 goes up, chunk j is computed and chunk
@@ -236,6 +236,10 @@ class MassOperator:
             cur.synchronize()
             return y_host
         L, nc = self.layers, self.n_cells
+        if chunks is None:  # ~16 MB per chunk: pipeline fill/drain ~1/chunks
+            import os
+            mb = float(os.environ.get("PM_HOST_CHUNK_MB", "16"))
+            chunks = int(min(64, max(4, n * 8 / (mb * 2**20))))
         # chunk boundaries on whole DG stream units (256 cell-layers)
         q = 256 // np.gcd(256, L)
         per = max(q, -(-nc // chunks // q) * q)
