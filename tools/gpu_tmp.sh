@@ -1,5 +1,6 @@
-: > gpurun_out/e2e.jsonl
-for mb in 40 16 8 4; do
-PM_HOST_CHUNK_MB=$mb timeout 300 python bench.py --config C2 --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | sed "s/\"schedule\": \"auto\"/\"schedule\": \"mb$mb\"/" >> gpurun_out/e2e.jsonl
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_edge_cases.py -m gpu -x -q -k "DG or stream or dg" > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
+: > gpurun_out/dg.jsonl
+for c in C2 C2 C4-DG1xDG1-rcm-L100 C4-DG0xDG0-rcm-L100 C4-DG1xDG0-rcm-L100; do
+timeout 300 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/dg.jsonl
 done
-python tools/summarize.py gpurun_out/e2e.jsonl
+python tools/summarize.py gpurun_out/dg.jsonl
