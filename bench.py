@@ -270,7 +270,15 @@ def run_sharded(args, w):
     t_setup = time.perf_counter()
     fs, quad, x_np, _ = configs.build(w)
     m = fs.mesh
-    op = ShardedMassOperator(fs, rank, world, quad)
+    # N > 1: the fused halo (the strip kernel adds ghost columns into the
+    # owner's window over NVLink peer memory, CUDA IPC) unless
+    # PM_FUSED_HALO=0 or it does not apply / cannot be set up on every
+    # rank, then the NCCL send/recv exchange
+    from paper_1604_05937_b200.shard import fused_halo_plan, partition
+    halo = "nccl send/recv"
+    want_fused = (world > 1 and os.environ.get("PM_FUSED_HALO", "1") != "0"
+                  and fused_halo_plan(fs, partition(fs, world)) is not None)
+    op = ShardedMassOperator(fs, rank, world, quad, fused=want_fused)
     lo, hi = op.window
     clo, chi = op.shard.coord_window
     coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
@@ -278,6 +286,14 @@ def run_sharded(args, w):
     del coords
     x = torch.from_numpy(x_np[lo:hi].copy()).cuda()
     y = torch.empty_like(x)
+    if want_fused:
+        try:
+            op.connect(y)
+            halo = "fused: ghost columns REDG'd into the owner's window " \
+                   "(CUDA IPC peer memory), 2 host barriers per step"
+        except (RuntimeError, ValueError) as e:
+            op = ShardedMassOperator(fs, rank, world, quad)
+            halo = f"nccl send/recv (fused halo unavailable: {e})"
     t_setup = time.perf_counter() - t_setup
     V = valuable_volume(fs)
     n_cl = m.base.num_cells * m.layers
@@ -343,8 +359,8 @@ def run_sharded(args, w):
                 "layout": w.layout, "valuable_bytes": V,
                 "map_bytes": map_bytes(fs),
                 "cell_layers_per_s": n_cl / (ms * 1e-3),
-                "parallelism": f"{world} contiguous RCM cell blocks, "
-                               "ghost-column sums over NCCL send/recv",
+                "parallelism": f"{world} contiguous RCM cell blocks",
+                "halo": halo if world > 1 else "none (1 rank)",
                 "halo_bytes_rank0": op.halo.bytes_per_exchange(),
                 "setup_s_rank0": t_setup,
                 "l2": "inputs larger than L2: no flush",
@@ -360,8 +376,9 @@ def run_sharded(args, w):
                     "h2d_bytes_per_step": int(xh.numel() * 8),
                     "d2h_bytes_per_step": int(yh.numel() * 8),
                     "ms_per_step": e2e_ms},
-            "gpu_launches": args.steps * (1 + 2 * len(op.halo.send) +
-                                          2 * len(op.halo.recv)),
+            "gpu_launches": args.steps * (
+                1 if op.fused else
+                1 + 2 * len(op.halo.send) + 2 * len(op.halo.recv)),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

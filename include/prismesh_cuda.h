@@ -252,6 +252,29 @@ int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                            int32_t *steps_e /* NULL, or 2 edges per step */,
                            int64_t *totals);
 
+/* Strip-REDG with the halo exchange fused in (multi-GPU): as
+ * pm_column_mass_strip_red for vertex-column layouts, except that the
+ * partial columns of vertices v < ghost_vertex_end (owned by the peer rank)
+ * are added with REDG straight into y_peer, the peer's y window mapped
+ * into this process (pm_ipc_open) and shifted like y so global DoF numbers
+ * index it.  Replaces the reference-anticipated pack / ncclSend / recv /
+ * owner-add of SURVEY §8e with one kernel.  The peer's window must be
+ * zeroed before and read only after every contributing kernel finished. */
+int pm_column_mass_strip_red_peer(
+    const int32_t *delta6, int32_t k, int32_t layers, const double *coords,
+    const double *mref, const double *mtri, const double *mline,
+    const double *x, double *y, int64_t n_dofs, int32_t accumulate,
+    int64_t n_strips, int32_t chunk, const int32_t *strip_ptr,
+    const int32_t *steps, int64_t n_vertices, double *y_peer,
+    int64_t ghost_vertex_end, void *stream);
+
+/* CUDA IPC of a device buffer for the fused halo: export (64-byte handle +
+ * byte offset inside its allocation), open in another process (returns the
+ * mapped pointer), close.  Replaces the NCCL transport of the exchange. */
+int pm_ipc_export(const void *ptr, void *handle64, int64_t *offset);
+int pm_ipc_open(const void *handle64, int64_t offset, void **ptr);
+int pm_ipc_close(void *ptr, int64_t offset);
+
 /* Device derive_edges (replaces mesh.py:33-84 derive_edges): edge set of a
  * triangle mesh as the sorted unique vertex pairs, cell_edges[c][k] = the
  * edge opposite local vertex k.  Device arrays: cell_vertices (n_cells,3)

@@ -91,6 +91,13 @@ SIGNATURES = {
                                        _i32p, _vp]),
     "pm_reorder_cells": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _vp,
                                         _vp]),
+    "pm_column_mass_strip_red_peer": (ctypes.c_int, [
+        _i32p, _i32, _i32, _vp, ctypes.POINTER(_f64), ctypes.POINTER(_f64),
+        ctypes.POINTER(_f64), _vp, _vp, _i64, _i32, _i64, _i32, _vp, _vp,
+        _i64, _vp, _i64, _vp]),
+    "pm_ipc_export": (ctypes.c_int, [_vp, _vp, _i64p]),
+    "pm_ipc_open": (ctypes.c_int, [_vp, _i64, ctypes.POINTER(_vp)]),
+    "pm_ipc_close": (ctypes.c_int, [_vp, _i64]),
     "pm_stream_triad": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, _i64,
                                        _vp]),
 }
@@ -360,6 +367,47 @@ def column_mass_strip_red(layout, k, layers, coords, mref, x, y, n_dofs,
         n_dofs, 1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp),
         ptr(st), ptr(se), n_vertices, stream_ptr(stream))
     check(rc)
+
+
+def column_mass_strip_red_peer(layout, k, layers, coords, mref, x, y,
+                               n_dofs, strips, kron, chunk, y_peer,
+                               ghost_vertex_end, accumulate=False,
+                               stream=None, x_base=0, y_base=0,
+                               coords_base=0, n_vertices=0):
+    """pm_column_mass_strip_red_peer: ``y_peer`` is a device address (int)
+    already shifted to global DoF indexing (see shard.PeerWindow)."""
+    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
+    ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
+    d = layout.delta6()
+    sp, st = strips[0], strips[1]
+    rc = host_lib().pm_column_mass_strip_red_peer(
+        d.ctypes.data_as(_i32p), k, layers, ptr(coords, coords_base),
+        _f64ptr(m), _f64ptr(mt), _f64ptr(ml), ptr(x, x_base), ptr(y, y_base),
+        n_dofs, 1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp),
+        ptr(st), n_vertices, ctypes.c_void_p(y_peer), ghost_vertex_end,
+        stream_ptr(stream))
+    check(rc)
+
+
+def ipc_export(t):
+    """(64-byte handle, byte offset) of device tensor ``t``'s storage."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    check(host_lib().pm_ipc_export(ptr(t), h, ctypes.byref(off)))
+    return h.raw, off.value
+
+
+def ipc_open(handle, offset):
+    """Map a peer's exported buffer: the device address (int)."""
+    p = ctypes.c_void_p(0)
+    h = ctypes.create_string_buffer(bytes(handle), 64)
+    check(host_lib().pm_ipc_open(h, int(offset), ctypes.byref(p)))
+    return p.value
+
+
+def ipc_close(addr, offset):
+    check(host_lib().pm_ipc_close(ctypes.c_void_p(addr), int(offset)))
 
 
 def column_mass_strip_bulk(layout, k, layers, coords, mref, x, y, x_range,

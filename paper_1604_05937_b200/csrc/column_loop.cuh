@@ -119,6 +119,10 @@ struct LoopArgs {
   bool dg_only;  // DoFs only on (2,1): contiguous (cell, layer, slot) field
   bool hshared;  // some DoF shared between columns
   cudaStream_t s;
+  // fused halo (strip kernel): vertices v < ghost_end are owned by the
+  // peer whose y (global-index window, peer memory) is y_peer
+  double *y_peer = nullptr;
+  int64_t ghost_end = 0;
 };
 
 // y = det * (Mtri (x) Mline) x by sum factorisation over a layout's

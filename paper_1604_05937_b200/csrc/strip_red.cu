@@ -128,12 +128,14 @@ template <class LY, int L> constexpr int sr_blocks() {
 // L consecutive levels per lane (lane sl: levels l0 + L*sl + j, j < L):
 // the level between two of them is read once, and the per-step overhead
 // (ids, ring wait, addressing, loop) is paid once per L cell-layers.
-template <class LY, int W, bool SYM, int L, int K = LY::K>
+template <class LY, int W, bool SYM, int L, bool PEER = false,
+          int K = LY::K>
 __global__ void __launch_bounds__(sr_threads<LY>(), sr_blocks<LY, L>())
 k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
             const int32_t *__restrict__ steps, int64_t n_strips, int layers,
             const double *__restrict__ coords, const double *__restrict__ x,
-            double *__restrict__ y) {
+            double *__restrict__ y, double *__restrict__ y_peer,
+            int ghost_end) {
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int SEGS = 32 / W;
   constexpr int CW = W * L; // levels per chunk
@@ -198,6 +200,10 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
     const double *xl = x + (int64_t)l0 * CH + sl;
     const double *cl0 = coords + 3 * (int64_t)l0 + sl;
     double *yl = y + ((int64_t)l0 + lb) * CH;
+    // fused halo: a ghost vertex's partial columns go straight to its
+    // owner's window (peer memory over NVLink) instead of a local window
+    // that a later exchange would ship
+    double *ylg = PEER ? y_peer + ((int64_t)l0 + lb) * CH : yl;
     // window vertex: interval-stage values z[j][c][v] at the lane's cell
     // layers and the geometry the Jacobian needs, derived once on entry:
     // xm, ym (mid-layer), dz; per-vertex accumulators acc[j][c][v]
@@ -336,7 +342,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         gm[A][j][2] = g[j + 1][2] - g[j][2];
       }
       __syncwarp(); // reads done before the slot is refilled
-      yc[A] = col_at(yl, rv[A], colb);
+      yc[A] = col_at(PEER && rv[A] < ghost_end ? ylg : yl, rv[A], colb);
       live[A] = act;
       // interval stage of the entering vertex
 #pragma unroll
@@ -417,6 +423,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
     flush(S2{});
     sr_wait<0>(); // no copy in flight into the ring across items
   }
+  if constexpr (PEER) __threadfence_system(); // peer REDs land before exit
 }
 
 // levels per lane (PM_STRIP_L tuning knob: 1 or 2)
@@ -425,7 +432,7 @@ static int strip_levels() {
   return e && atoi(e) == 2 ? 2 : 1;
 }
 
-template <class LY, int W, bool SYM, int L>
+template <class LY, int W, bool SYM, int L, bool PEER = false>
 static int strip_red_launch(const LoopArgs &a, const KronMat &M,
                             const int32_t *strip_ptr, const int32_t *steps,
                             int64_t n_strips) {
@@ -435,11 +442,12 @@ static int strip_red_launch(const LoopArgs &a, const KronMat &M,
   constexpr int T = sr_threads<LY>();
   const unsigned grid = grid_for(warps * 32, T, 8);
   const size_t smem = sr_smem<LY, W, L>();
-  PM_CUDA_TRY(cudaFuncSetAttribute(k_strip_red<LY, W, SYM, L>,
+  PM_CUDA_TRY(cudaFuncSetAttribute(k_strip_red<LY, W, SYM, L, PEER>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-  k_strip_red<LY, W, SYM, L><<<grid, T, smem, a.s>>>(
-      M, strip_ptr, steps, n_strips, a.layers, a.coords, a.x, a.y);
+  k_strip_red<LY, W, SYM, L, PEER><<<grid, T, smem, a.s>>>(
+      M, strip_ptr, steps, n_strips, a.layers, a.coords, a.x, a.y, a.y_peer,
+      (int)a.ghost_end);
   PM_LAUNCH_CHECK("k_strip_red");
   return PM_OK;
 }
@@ -448,6 +456,13 @@ template <class LY, int W>
 static int strip_red_w(const LoopArgs &a, const KronMat &M, bool sym,
                        int L, const int32_t *strip_ptr, const int32_t *steps,
                        int64_t n_strips) {
+  if (a.y_peer) { // fused halo
+    if (sym)
+      return strip_red_launch<LY, W, true, 1, true>(a, M, strip_ptr, steps,
+                                                    n_strips);
+    return strip_red_launch<LY, W, false, 1, true>(a, M, strip_ptr, steps,
+                                                   n_strips);
+  }
   if constexpr (LY::CH0 <= 2 && W <= 16) {
     if (L == 2 && sym)
       return strip_red_launch<LY, W, true, 2>(a, M, strip_ptr, steps,
@@ -821,15 +836,23 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
 
 } // namespace pm
 
-extern "C" int pm_column_mass_strip_red(
+static int strip_red_entry(
     const int32_t *delta6, int32_t k, int32_t layers, const double *coords,
     const double *mref, const double *mtri, const double *mline,
     const double *x, double *y, int64_t n_dofs, int32_t accumulate,
     int64_t n_strips, int32_t chunk, const int32_t *strip_ptr,
     const int32_t *steps, const int32_t *steps_e, int64_t n_vertices,
-    void *stream) {
+    double *y_peer, int64_t ghost_end, void *stream) {
   pm::clear_error();
   pm::LoopArgs a;
+  a.y_peer = y_peer;
+  a.ghost_end = y_peer ? ghost_end : 0;
+  if (y_peer && (ghost_end < 0 || ghost_end > INT32_MAX ||
+                 pm::Layout<1, 1, 1, 1, 0, 0>::matches(delta6))) {
+    pm::set_error("the fused halo needs a vertex-column layout and an int32 "
+                  "ghost vertex bound");
+    return PM_EINVAL;
+  }
   int rc = pm::make_slot_table(delta6, &a.st);
   if (rc) return rc;
   if (k != a.st.k || layers < 1 || n_strips < 0 || !mref || n_dofs < 0) {
@@ -865,4 +888,29 @@ extern "C" int pm_column_mass_strip_red(
   }
   pm::set_error("layout not supported by the strip schedule");
   return PM_EINVAL;
+}
+
+extern "C" int pm_column_mass_strip_red(
+    const int32_t *delta6, int32_t k, int32_t layers, const double *coords,
+    const double *mref, const double *mtri, const double *mline,
+    const double *x, double *y, int64_t n_dofs, int32_t accumulate,
+    int64_t n_strips, int32_t chunk, const int32_t *strip_ptr,
+    const int32_t *steps, const int32_t *steps_e, int64_t n_vertices,
+    void *stream) {
+  return strip_red_entry(delta6, k, layers, coords, mref, mtri, mline, x, y,
+                         n_dofs, accumulate, n_strips, chunk, strip_ptr,
+                         steps, steps_e, n_vertices, nullptr, 0, stream);
+}
+
+extern "C" int pm_column_mass_strip_red_peer(
+    const int32_t *delta6, int32_t k, int32_t layers, const double *coords,
+    const double *mref, const double *mtri, const double *mline,
+    const double *x, double *y, int64_t n_dofs, int32_t accumulate,
+    int64_t n_strips, int32_t chunk, const int32_t *strip_ptr,
+    const int32_t *steps, int64_t n_vertices, double *y_peer,
+    int64_t ghost_vertex_end, void *stream) {
+  return strip_red_entry(delta6, k, layers, coords, mref, mtri, mline, x, y,
+                         n_dofs, accumulate, n_strips, chunk, strip_ptr,
+                         steps, nullptr, n_vertices, y_peer,
+                         ghost_vertex_end, stream);
 }

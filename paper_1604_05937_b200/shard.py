@@ -180,6 +180,84 @@ class HaloExchange:
         return y
 
 
+def fused_halo_plan(fs, shards):
+    """Ghost-vertex bound per rank for the fused halo, or None.
+
+    The fused kernel (``pm_column_mass_strip_red_peer``) sends a vertex's
+    partial columns to the rank below when its id is under a bound, so it
+    applies when (true for RCM-ordered meshes): the layout has
+    DoFs on vertices only; every rank's ghosts are owned by the rank below
+    and lie below its first owned vertex; every touched vertex from there on
+    is owned.  Returns ``[bound_p]`` (0 for rank 0).
+    """
+    layout = fs.layout
+    dims = [d for d in (0, 1, 2) if layout.dofs(d, 0) or layout.dofs(d, 1)]
+    if dims != [0]:
+        return None
+    ends = []
+    for sh in shards:
+        touched, own = sh.dim_entities[0], sh.owned[0]
+        if sh.rank == 0:
+            if sh.send:
+                return None
+            ends.append(0)
+            continue
+        if set(sh.send) - {sh.rank - 1} or own.size == 0:
+            return None
+        lo = int(own[0])
+        if not np.array_equal(np.setdiff1d(touched, own),
+                              touched[touched < lo]):
+            return None
+        ends.append(lo)
+    return ends
+
+
+class PeerWindow:
+    """The y window of the rank below, mapped into this process (CUDA IPC,
+    NVLink peer memory): every rank exports its window; rank p maps rank
+    p-1's.  ``addr`` is shifted like ``_lib.ptr(t, base)`` so that global
+    DoF numbers index it."""
+
+    def __init__(self, y_window, lo, rank, world, group=None):
+        import torch.distributed as dist
+        from . import _lib
+        # every step is collective and failure-consistent: a rank that
+        # cannot export or map makes all ranks raise (no rank is left
+        # waiting in a collective the others skipped)
+        try:
+            mine = (*_lib.ipc_export(y_window), int(lo))
+        except Exception as e:  # noqa: BLE001 - reported on every rank
+            mine = repr(e)
+        infos = [None] * world
+        dist.all_gather_object(infos, mine, group=group)
+        bad = [i for i in infos if isinstance(i, str)]
+        if bad:
+            raise RuntimeError(f"fused halo: IPC export failed: {bad[0]}")
+        self._open = None
+        self.addr = 0
+        err = None
+        if rank > 0:
+            h, o, plo = infos[rank - 1]
+            try:
+                base = _lib.ipc_open(h, o)
+                self._open = (base, o)
+                self.addr = base - 8 * plo
+            except Exception as e:  # noqa: BLE001
+                err = repr(e)
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=group)
+        if any(errs):
+            self.close()
+            raise RuntimeError(
+                f"fused halo: IPC open failed: {next(e for e in errs if e)}")
+
+    def close(self):
+        from . import _lib
+        if self._open is not None:
+            _lib.ipc_close(*self._open)
+            self._open = None
+
+
 class ShardedMassOperator:
     """The column loop over one rank's cell block + the halo exchange.
 
@@ -188,14 +266,28 @@ class ShardedMassOperator:
     window of ``y`` with final values on its owned entity columns.
     """
 
-    def __init__(self, fs, rank, world, quadrature=None, group=None):
+    def __init__(self, fs, rank, world, quadrature=None, group=None,
+                 fused=False):
         import torch
         from . import _lib
         from .kernels import MassOperator
         self.fs = fs
         self.rank, self.world = rank, world
         self.group = group
-        self.shard = partition(fs, world)[rank]
+        shards = partition(fs, world)
+        self.shard = shards[rank]
+        # fused halo: ghost columns are added straight into the owner's
+        # window by the kernel (peer memory) instead of being exchanged
+        self.fused = bool(fused) and world > 1
+        self.ghost_end = 0
+        self._peer = None
+        if self.fused:
+            plan = fused_halo_plan(fs, shards)
+            if plan is None:
+                raise ValueError(
+                    "the fused halo needs a vertex-only layout whose ghosts "
+                    "are owned by the rank below (RCM-ordered blocks)")
+            self.ghost_end = plan[rank]
         self.op = MassOperator(fs, quadrature, schedule="column")
         dev = self.op._dev
         self.d_cells = torch.from_numpy(self.shard.cells).to(dev)
@@ -209,10 +301,48 @@ class ShardedMassOperator:
     def window(self):
         return self.shard.window
 
+    def connect(self, y_window):
+        """Fused halo: map the rank below's ``y_window`` (collective; every
+        rank passes the persistent window it will pass to ``apply``)."""
+        if not self.fused:
+            return
+        if self.strips is None:
+            raise ValueError("the fused halo runs on the strip schedule")
+        if self._peer is not None:
+            self._peer.close()
+        self._peer = PeerWindow(y_window, self.shard.window[0], self.rank,
+                                self.world, group=self.group)
+        self._peer_y = y_window
+
+    def _apply_fused(self, x_window, coords_window, y_window):
+        import torch
+        import torch.distributed as dist
+        if self._peer is None or y_window is not self._peer_y:
+            raise ValueError("fused halo: call connect(y_window) first with "
+                             "the window passed to apply")
+        lo, hi = self.shard.window
+        clo, _chi = self.shard.coord_window
+        op = self.op
+        y_window.zero_()
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)    # every window zeroed
+        strips, W = self.strips
+        self._lib.column_mass_strip_red_peer(
+            op.fs.layout, op.k, op.layers, coords_window, op.mref, x_window,
+            y_window, hi - lo, strips, op.kron, W, self._peer.addr,
+            self.ghost_end if self._peer.addr else 0, accumulate=True,
+            x_base=lo, y_base=lo, coords_base=clo,
+            n_vertices=op.fs.mesh.base.num_vertices)
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)    # every peer addition landed
+        return y_window
+
     def apply(self, x_window, coords_window, y_window=None, exchange=True):
         import torch
         lo, hi = self.shard.window
         clo, _chi = self.shard.coord_window
+        if self.fused and exchange:
+            return self._apply_fused(x_window, coords_window, y_window)
         if y_window is None:
             y_window = torch.empty(hi - lo, dtype=torch.float64,
                                    device=x_window.device)

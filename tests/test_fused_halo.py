@@ -1,0 +1,177 @@
+"""Fused halo: the strip kernel adds ghost vertex columns
+straight into the owning rank's window (peer memory) instead of a
+pack / send / recv / owner-add exchange.
+
+* CPU: the applicability plan (ghosts owned by the rank below and lying
+  under the rank's first owned vertex) on RCM / random meshes, 2–8 ranks.
+* GPU, one process: every rank's window on one device, each rank's kernel
+  given the window of the rank below as its peer — the kernel's ghost
+  redirect and global-index addressing against the oracle.
+* GPU, two processes on one device: the whole product path —
+  ``ShardedMassOperator(fused=True)``: CUDA IPC export / open of the
+  windows, zero → barrier → kernel → barrier (host barriers only: no kernel
+  waits on another).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import LAYOUT_COUNTS, families, quad_degrees
+
+
+def _space(n, layers, lname, ordering="rcm"):
+    from paper_1604_05937_b200 import DofLayout, ExtrudedMesh, number_dofs
+    from paper_1604_05937_b200.configs import base_mesh
+    base, _ = base_mesh(n, ordering)
+    return number_dofs(ExtrudedMesh(base, layers),
+                       DofLayout(lname, LAYOUT_COUNTS[lname]))
+
+
+def _oracle(fs, lname):
+    tri, line, nc = families(lname)
+    return oracle.Problem(fs.mesh.base, fs.mesh.layers, LAYOUT_COUNTS[lname],
+                          tri, line, nc, *quad_degrees(lname))
+
+
+@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1"))
+@pytest.mark.parametrize("world", (2, 3, 4, 8))
+def test_plan_on_rcm_blocks(lname, world):
+    from paper_1604_05937_b200.shard import fused_halo_plan, partition
+    fs = _space(16, 3, lname)
+    shards = partition(fs, world)
+    plan = fused_halo_plan(fs, shards)
+    assert plan is not None and plan[0] == 0
+    for s, end in zip(shards, plan):
+        t, own = s.dim_entities[0], s.owned[0]
+        ghosts = np.setdiff1d(t, own)
+        assert np.all(ghosts < end) and np.all(own >= end)
+        if s.rank:
+            # ghosts belong to the rank below, i.e. inside its window
+            below = shards[s.rank - 1]
+            assert np.isin(ghosts, below.owned[0]).all()
+
+
+@pytest.mark.parametrize("lname", ("P2xP2", "CG1xDG1", "DG1xDG1"))
+def test_plan_refuses_other_layouts(lname):
+    from paper_1604_05937_b200.shard import fused_halo_plan, partition
+    fs = _space(8, 2, lname)
+    if lname == "CG1xDG1":      # vertex-only: applies
+        assert fused_halo_plan(fs, partition(fs, 2)) is not None
+    else:
+        assert fused_halo_plan(fs, partition(fs, 2)) is None
+
+
+def test_plan_refuses_scattered_ownership():
+    """A random vertex order breaks 'ghosts below the first owned vertex'."""
+    from paper_1604_05937_b200.shard import fused_halo_plan, partition
+    fs = _space(16, 2, "CG1xCG1", ordering="random")
+    assert fused_halo_plan(fs, partition(fs, 4)) is None
+
+
+# ------------------------------------------------------------------ GPU
+@pytest.mark.gpu
+@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1", "CG1xDG1"))
+@pytest.mark.parametrize("world", (2, 3, 4))
+def test_fused_kernel_windows_on_one_gpu(lname, world):
+    import torch
+    from paper_1604_05937_b200 import _lib, configs, extrude_coordinates
+    from paper_1604_05937_b200.shard import (ShardedMassOperator,
+                                             fused_halo_plan, ghost_origins,
+                                             partition)
+    w = configs.Workload("c5-fused", 24, 6, lname, quad_degrees(lname))
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    ref = _oracle(fs, lname).assemble(x)
+    xd = torch.from_numpy(x).cuda()
+    plan = fused_halo_plan(fs, partition(fs, world))
+    ops = [ShardedMassOperator(fs, r, world, quad) for r in range(world)]
+    wins = [torch.zeros(op.window[1] - op.window[0], dtype=torch.float64,
+                        device="cuda") for op in ops]
+    for r, op in enumerate(ops):
+        lo, hi = op.window
+        clo, chi = op.shard.coord_window
+        peer = (wins[r - 1].data_ptr() - 8 * ops[r - 1].window[0]) if r else 0
+        strips, W = op.strips
+        _lib.column_mass_strip_red_peer(
+            fs.layout, op.op.k, m.layers, coords[clo:chi].clone(), op.op.mref,
+            xd[lo:hi].clone(), wins[r], hi - lo, strips, op.op.kron, W, peer,
+            plan[r] if r else 0, accumulate=True, x_base=lo, y_base=lo,
+            coords_base=clo, n_vertices=m.base.num_vertices)
+    torch.cuda.synchronize()
+    got = np.zeros_like(ref)
+    for op, win in zip(ops, wins):
+        yw = win.cpu().numpy()
+        for _d, o, c in ghost_origins(fs, op.shard.owned):
+            for org in o:
+                a = org - op.window[0]
+                got[org:org + c] = yw[a:a + c]
+    assert np.abs(got - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _ipc_worker(rank, world, port, lname, q):
+    try:
+        import torch
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_1604_05937_b200 import configs, extrude_coordinates
+        from paper_1604_05937_b200.kernels import mass_action
+        from paper_1604_05937_b200.shard import (ShardedMassOperator,
+                                                 ghost_origins)
+        w = configs.Workload("c5-ipc", 20, 5, lname, quad_degrees(lname))
+        fs, quad, x, _ = configs.build(w)
+        m = fs.mesh
+        coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+        op = ShardedMassOperator(fs, rank, world, quad, fused=True)
+        lo, hi = op.window
+        clo, chi = op.shard.coord_window
+        xd = torch.from_numpy(x[lo:hi].copy()).cuda()
+        yw = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+        op.connect(yw)
+        err = 0.0
+        full = mass_action(fs, x, quadrature=quad)
+        for _rep in range(2):              # the window is reused per step
+            op.apply(xd, coords[clo:chi].clone(), yw)
+            got = yw.cpu().numpy()
+            for _d, o, c in ghost_origins(fs, op.shard.owned):
+                for org in o:
+                    e = np.abs(got[org - lo:org - lo + c] - full[org:org + c])
+                    err = max(err, float(e.max()) / float(np.abs(full).max()))
+        dist.barrier()
+        op._peer.close()
+        dist.destroy_process_group()
+        q.put((rank, err))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, repr(e) + traceback.format_exc()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1"))
+def test_fused_halo_two_processes_ipc(lname):
+    import torch.multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, lname, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert isinstance(res[r], float), res[r]
+        assert res[r] <= 1e-10

@@ -1,6 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_edge_cases.py -m gpu -x -q -k "DG or stream or dg" > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
-: > gpurun_out/dg.jsonl
-for c in C2 C2 C4-DG1xDG1-rcm-L100 C4-DG0xDG0-rcm-L100 C4-DG1xDG0-rcm-L100; do
-timeout 300 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/dg.jsonl
-done
-python tools/summarize.py gpurun_out/dg.jsonl
+for c in C5a C4-CG1xCG1-rcm-L100; do python tools/time_op.py $c new; done
+timeout 600 python -m pytest tests/test_fused_halo.py tests/test_gpu_parity.py -m gpu -q -k "fused or strip or host" > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log

@@ -1,0 +1,29 @@
+"""Time MassOperator.apply for a workload without bench.py (A/B helper)."""
+import sys
+import time
+
+import os
+sys.path.insert(0, os.getcwd())
+import torch
+
+from paper_1604_05937_b200 import configs
+from paper_1604_05937_b200.extrusion import extrude_coordinates
+from paper_1604_05937_b200.kernels import MassOperator
+
+w = configs.workload(sys.argv[1])
+fs, quad, x_np, _ = configs.build(w)
+m = fs.mesh
+coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+op = MassOperator(fs, quad)
+x = torch.from_numpy(x_np).cuda()
+y = torch.zeros_like(x)
+for _ in range(3):
+    op.apply(x, coords, y, accumulate=True)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10):
+    op.apply(x, coords, y, accumulate=True)
+e1.record()
+torch.cuda.synchronize()
+print(sys.argv[2] if len(sys.argv) > 2 else "", sys.argv[1], e0.elapsed_time(e1) / 10)
