@@ -510,16 +510,13 @@ template <class LY, int W> constexpr int sre_entry() {
   return sre_fs0<LY, W>() + 3 * (W + 1) + 2 * sre_fs1<LY, W>();
 }
 
-// CTA size of the P2 kernel (measured: 384 threads at <= 168 registers
-// spill and run 8 % slower)
-#ifndef PM_SRE_THREADS
-#define PM_SRE_THREADS 256
-#endif
-constexpr int kSreThreads = PM_SRE_THREADS;
-constexpr int kSreWarps = kSreThreads / 32;
+// CTA size of the P2 kernel: 384 threads (12 warps at <= 168 registers)
+// with the block-structured triangle factor, 256 with a general one (it
+// spills at 168: measured 8 % slower)
+template <bool SYM> constexpr int sre_threads() { return SYM ? 384 : 256; }
 
 template <class LY, int W, bool SYM, int K = LY::K>
-__global__ void __launch_bounds__(kSreThreads, 1)
+__global__ void __launch_bounds__(sre_threads<SYM>(), 1)
 k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
               const int32_t *__restrict__ steps,
               const int32_t *__restrict__ steps_e, int64_t n_strips,
@@ -532,6 +529,7 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
   static_assert(LY::NH == 6 && LY::NC == 1 && LV0 == 1 && LV1 == 1 &&
                     CH0 == NV - 1 && CH1 == NV - 1,
                 "P2-type layout: level copies + NV-2 connecting functions");
+  constexpr int kSreWarps = sre_threads<SYM>() / 32;
   constexpr int FS0 = sre_fs0<LY, W>(), FS1 = sre_fs1<LY, W>();
   constexpr int ES = sre_entry<LY, W>();
   constexpr int OC = FS0, OE1 = FS0 + 3 * (W + 1), OE2 = OE1 + FS1;
@@ -790,7 +788,6 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
   const int segs = 32 / W;
   const int64_t items = n_strips * ((a.layers + W - 1) / W);
   const int64_t warps = (items + segs - 1) / segs;
-  const unsigned grid = grid_for(warps * 32, kSreThreads, 4);
   const bool sym = kron_sym6(M);
 #define PM_SRE(WW)                                                           \
   do {                                                                       \
@@ -801,14 +798,15 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
   } while (0)
 #define PM_SRE2(WW, SS)                                                      \
   do {                                                                       \
-    const size_t smem = sizeof(double) *                                     \
-                            (kSreWarps * kSrDepth * (32 / WW) + 1) *         \
+    constexpr int T = sre_threads<SS>(), NW = T / 32;                        \
+    const unsigned grid = grid_for(warps * 32, T, 4);                        \
+    const size_t smem = sizeof(double) * (NW * kSrDepth * (32 / WW) + 1) *   \
                             sre_entry<LY, WW>() +                            \
-                        sizeof(int) * kSreWarps * (32 / WW) * 3 * kSrIds;    \
+                        sizeof(int) * NW * (32 / WW) * 3 * kSrIds;           \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
         k_strip_red_e<LY, WW, SS>,                                           \
         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
-    k_strip_red_e<LY, WW, SS><<<grid, kSreThreads, smem, a.s>>>(                         \
+    k_strip_red_e<LY, WW, SS><<<grid, T, smem, a.s>>>(                       \
         M, strip_ptr, steps, steps_e, n_strips, a.layers, e_start, a.coords, \
         a.x, a.y);                                                           \
   } while (0)
