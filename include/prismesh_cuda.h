@@ -303,6 +303,15 @@ int pm_reorder_cells(const int32_t *cell_vertices, int64_t n_cells,
 int pm_stream_triad(double *a, const double *b, const double *c, double alpha,
                     int64_t n, void *stream);
 
+/* Programmatic dependent launch for the DG stream kernel launched by this
+ * host thread (returns the previous setting).  With it on, a stream
+ * kernel starts its prologue, TMA loads and coordinate gathers while the
+ * previous kernel of the stream drains, and waits for it before its first
+ * store: valid only when that previous kernel writes none of this call's
+ * inputs (back-to-back applies to the same fields, e.g. captured by
+ * MassOperator.graph(repeat=K)). */
+int pm_set_launch_overlap(int32_t on);
+
 /* Device properties used to size grids (SM count, L2 bytes). */
 int pm_device_info(int32_t *sm_count, int64_t *l2_bytes);
 

@@ -98,6 +98,7 @@ SIGNATURES = {
     "pm_ipc_export": (ctypes.c_int, [_vp, _vp, _i64p]),
     "pm_ipc_open": (ctypes.c_int, [_vp, _i64, ctypes.POINTER(_vp)]),
     "pm_ipc_close": (ctypes.c_int, [_vp, _i64]),
+    "pm_set_launch_overlap": (ctypes.c_int, [_i32]),
     "pm_stream_triad": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, _i64,
                                        _vp]),
 }
@@ -505,6 +506,12 @@ def stream_triad(a, b, c, alpha, stream=None):
         raise ValueError("triad arrays differ in length")
     check(host_lib().pm_stream_triad(ptr(a), ptr(b), ptr(c), float(alpha),
                                      n, stream_ptr(stream)))
+
+
+def set_launch_overlap(on):
+    """Programmatic dependent launch for this thread's stream kernels
+    (see the header); returns the previous setting."""
+    return bool(host_lib().pm_set_launch_overlap(1 if on else 0))
 
 
 def device_info():

@@ -98,6 +98,17 @@ extern "C" int pm_num_slots(const int32_t *delta6, int32_t *k_out) {
   return PM_OK;
 }
 
+namespace pm {
+static thread_local int g_overlap = 0;
+bool launch_overlap() { return g_overlap != 0; }
+} // namespace pm
+
+extern "C" int pm_set_launch_overlap(int32_t on) {
+  const int prev = pm::g_overlap;
+  pm::g_overlap = on ? 1 : 0;
+  return prev;
+}
+
 extern "C" int pm_device_info(int32_t *sm, int64_t *l2) {
   int dev = 0, n = 0, l2b = 0;
   PM_CUDA_TRY(cudaGetDevice(&dev));

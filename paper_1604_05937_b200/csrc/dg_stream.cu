@@ -44,6 +44,12 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int64_t cl_begin, int layers,
     fence_mbar_init();
   }
   __syncthreads();
+  // programmatic dependent launch (pm_set_launch_overlap): the next
+  // kernel of the stream may start its prologue, loads and gathers while
+  // this grid drains; it waits for this grid before its first store.  A
+  // no-op when the launch carries no programmatic dependency.
+  asm volatile("griddepcontrol.launch_dependents;");
+  bool waited = false;
 
   const int64_t first = blockIdx.x, stride = gridDim.x;
   const int64_t n_mine =
@@ -175,6 +181,10 @@ k_dg_stream(const MassMat<D> M, int64_t n_units, int64_t cl_begin, int layers,
     fence_proxy_async_smem();
     __syncthreads();
     if (t == 0) {
+      if (!waited) { // the previous grid (same y) has finished
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        waited = true;
+      }
       bulk_s2g(y + (cl_begin + u * T) * D, b, BYTES);
       bulk_commit();
       const int64_t nxt = i + S - 1;
@@ -215,8 +225,24 @@ static int dg_stream_launch(const LoopArgs &a, const MassMat<D> &M,
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sm_count() * per_sm;
   if (grid > n_units) grid = n_units;
-  kern<<<(unsigned)grid, T, smem, a.s>>>(M, n_units, cl_begin, a.layers,
-                                         a.xmap, a.xoff, a.coords, a.x, a.y);
+  if (launch_overlap()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = a.s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, M, n_units, cl_begin, a.layers,
+                                   a.xmap, a.xoff, a.coords, a.x, a.y));
+  } else {
+    kern<<<(unsigned)grid, T, smem, a.s>>>(M, n_units, cl_begin, a.layers,
+                                           a.xmap, a.xoff, a.coords, a.x,
+                                           a.y);
+  }
   PM_LAUNCH_CHECK("k_dg_stream");
   return PM_OK;
 }

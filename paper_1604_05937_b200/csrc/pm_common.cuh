@@ -27,6 +27,11 @@ inline unsigned grid_for(int64_t n, int threads, int per_sm = 16) {
   return (unsigned)want;
 }
 
+// Programmatic dependent launch of the DG stream kernel (thread-local,
+// pm_set_launch_overlap): only for back-to-back applies whose inputs no
+// preceding kernel writes.
+bool launch_overlap();
+
 constexpr int kMaxSlots = 64;
 
 // Host-side restatement of the reference slot table (fspace.py:110-131):

@@ -308,17 +308,29 @@ class MassOperator:
             self._coloring = (d_order, ptr)
         return self._coloring
 
-    def graph(self, x, coords, y, accumulate=False, schedule=None):
-        """One ``apply`` on fixed device buffers captured as a CUDA graph
-        (``torch.cuda.CUDAGraph``; ``.replay()`` re-runs it on the current
-        stream): repeated application without per-call host work, for
-        launch-bound sizes and solver loops."""
+    def graph(self, x, coords, y, accumulate=False, schedule=None, repeat=1,
+              overlap=False):
+        """``repeat`` back-to-back ``apply`` calls on fixed device buffers
+        captured as one CUDA graph (``torch.cuda.CUDAGraph``; ``.replay()``
+        re-runs them on the current stream): repeated application without
+        per-call host work, for launch-bound sizes and solver loops.
+
+        ``overlap``: programmatic dependent launch between the captured DG
+        stream kernels — each starts its prologue, loads and gathers while
+        the previous one drains and waits for it only before its first
+        store (the captured calls share their inputs, so this is safe)."""
         import torch
         self.apply(x, coords, y, accumulate=accumulate, schedule=schedule)
         torch.cuda.synchronize()        # plans and kernel attributes ready
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.apply(x, coords, y, accumulate=accumulate, schedule=schedule)
+        prev = _lib.set_launch_overlap(overlap)
+        try:
+            with torch.cuda.graph(g):
+                for _ in range(repeat):
+                    self.apply(x, coords, y, accumulate=accumulate,
+                               schedule=schedule)
+        finally:
+            _lib.set_launch_overlap(prev)
         torch.cuda.synchronize()
         return g
 

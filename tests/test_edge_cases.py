@@ -121,3 +121,31 @@ def test_bad_inputs_rejected_before_iteration():
         op.apply(x, coords, schedule="no-such-schedule")
     with pytest.raises(ValueError):
         op.apply(x, coords, schedule="stream")         # CG is not a DG field
+
+
+@pytest.mark.parametrize("lname", ["DG1xDG1", "DG0xDG1", "CG1xCG1", "P2xP2"])
+@pytest.mark.parametrize("overlap", [False, True])
+def test_graph_of_repeated_applies(lname, overlap):
+    """MassOperator.graph(repeat=K, overlap): K captured applies (DG: with
+    programmatic dependent launch between them) leave exactly the result of
+    one apply (bitwise for the deterministic DG stream)."""
+    from paper_1604_05937_b200.extrusion import extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator
+    from paper_1604_05937_b200.mesh import generate_unit_square_mesh
+    base = generate_unit_square_mesh(48)
+    fs = _space(base, 10, lname)
+    coords = extrude_coordinates(base.coords, 10, 0.1)
+    op = MassOperator(fs)
+    x = torch.from_numpy(
+        np.random.default_rng(5).uniform(-1, 1, fs.total_dofs)).cuda()
+    ref = op.apply(x, coords).clone()
+    y = torch.full_like(x, np.nan)
+    g = op.graph(x, coords, y, repeat=7, overlap=overlap)
+    y.fill_(np.nan)
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    if lname.startswith("DG"):
+        assert torch.equal(y, ref)
+    else:
+        assert _rel(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-12
