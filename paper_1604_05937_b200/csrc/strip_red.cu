@@ -74,14 +74,20 @@ template <class LY> constexpr int sr_min_blocks() {
 template <class LY, int CW> constexpr int sr_fsz() {
   return CW * LY::CH0 + LY::LV0;
 }
+#ifndef PM_SR16
+#define PM_SR16 0
+#endif
+// PM_SR16: 16-byte cp.async.cg rows (L1 bypassed) of the 16-byte aligned
+// superset of each chunk (per-vertex shift 0/1), W lanes x 2 doubles
+constexpr int kSrVec = PM_SR16 ? 2 : 1; // doubles per lane per row
 template <class LY, int W, int L> constexpr int sr_frows() {
-  return (sr_fsz<LY, W * L>() + W - 1) / W;
+  return (sr_fsz<LY, W * L>() + (kSrVec - 1) + kSrVec * W - 1) / (kSrVec * W);
 }
 template <class LY, int W, int L> constexpr int sr_crows() {
-  return (3 * (W * L + 1) + W - 1) / W;
+  return (3 * (W * L + 1) + (kSrVec - 1) + kSrVec * W - 1) / (kSrVec * W);
 }
 template <class LY, int W, int L> constexpr int sr_pentry() {
-  return (sr_frows<LY, W, L>() + sr_crows<LY, W, L>()) * W;
+  return (sr_frows<LY, W, L>() + sr_crows<LY, W, L>()) * kSrVec * W;
 }
 constexpr int kSrIds = 64; // strip vertex ids staged per segment
 #ifndef PM_SR_VTHREADS
@@ -97,6 +103,14 @@ template <class LY, int W, int L> constexpr size_t sr_smem() {
              ((size_t)(sr_threads<LY>() / 32) * kSrDepth * (32 / W) + 1) *
              sr_pentry<LY, W, L>() +
          sizeof(int) * (sr_threads<LY>() / 32) * (32 / W) * kSrIds;
+}
+
+__device__ __forceinline__ void sr_cp16z(double *dst, const double *src,
+                                         int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
 }
 
 __device__ __forceinline__ void sr_cp8z(double *dst, const double *src,
@@ -149,7 +163,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
   static_assert(NH == 3 && NC * NV == CH + LV, "vertex-column layout");
   static_assert(LV == 0 || (LV == NC && NV == 2 && CH == LV), "strip layout");
   constexpr int FR = sr_frows<LY, W, L>(), CR = sr_crows<LY, W, L>();
-  constexpr int FP = FR * W;                 // coordinate part offset
+  constexpr int FP = FR * kSrVec * W;        // coordinate part offset
   constexpr int ES = sr_pentry<LY, W, L>();
   const int lane = threadIdx.x & 31;
   const int sl = lane % W, seg = lane / W;
@@ -242,12 +256,37 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       return ring + (size_t)(slot * SEGS + seg) * ES;
     };
     int rv[kSrDepth];
+#if PM_SR16
+    int rsh[kSrDepth];
+    const int fbytes = 8 * (nl * CH + LV) - 16 * sl;
+    const int cbytes = 8 * 3 * (nl + 1) - 16 * sl;
+    const double *xs = xl - sl, *cs = cl0 - sl;
+#endif
     auto fetch = [&](int k, int slot) {
       if ((k & (kSrIds - 1)) == 0 && k > 0) { // warp-uniform
         __syncwarp();
         load_ids(k);
       }
       const int v = sid[k & (kSrIds - 1)];
+#if PM_SR16
+      const double *fp = col_at(xs, v, colb);
+      const double *cp = col_at(cs, v, ccolb);
+      const int fsh = (int)(reinterpret_cast<uintptr_t>(fp) >> 3) & 1;
+      const int csh = (int)(reinterpret_cast<uintptr_t>(cp) >> 3) & 1;
+      if (k < len) {
+        double *e = entry(slot) + 2 * sl;
+        const double *fa = fp - fsh + 2 * sl, *ca = cp - csh + 2 * sl;
+#pragma unroll
+        for (int r = 0; r < FR; ++r)
+          sr_cp16z(e + 2 * W * r, fa + 2 * W * r,
+                   min(max(fbytes + 8 * fsh - 16 * W * r, 0), 16));
+#pragma unroll
+        for (int r = 0; r < CR; ++r)
+          sr_cp16z(e + FP + 2 * W * r, ca + 2 * W * r,
+                   min(max(cbytes + 8 * csh - 16 * W * r, 0), 16));
+      }
+      rsh[slot] = fsh | (csh << 1);
+#else
       if (k < len) {
         const double *fp = col_at(xl, v, colb);
         const double *cp = col_at(cl0, v, ccolb);
@@ -258,6 +297,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         for (int r = 0; r < CR; ++r)
           sr_cp8z(e + FP + W * r, cp + W * r, cz[r]);
       }
+#endif
       sr_commit(); // one group per step (possibly empty)
       return v;
     };
@@ -326,14 +366,20 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       // (stale, possibly non-finite) ring slot; lanes past the chunk read
       // zero-filled values and are never flushed.
       const double *e = act ? entry(A) : sr_zero;
+#if PM_SR16
+      const int sh = act ? rsh[A] : 0;
+      const double *ef = e + (sh & 1), *ec = e + FP + (sh >> 1);
+#else
+      const double *ef = e, *ec = e + FP;
+#endif
       double f[L + 1][CH], g[L + 1][3];
 #pragma unroll
       for (int j = 0; j <= L; ++j) {
 #pragma unroll
         for (int c = 0; c < CH; ++c)
-          f[j][c] = (j < L || c < LV) ? e[(lb + j) * CH + c] : 0.0;
+          f[j][c] = (j < L || c < LV) ? ef[(lb + j) * CH + c] : 0.0;
 #pragma unroll
-        for (int q = 0; q < 3; ++q) g[j][q] = e[FP + 3 * (lb + j) + q];
+        for (int q = 0; q < 3; ++q) g[j][q] = ec[3 * (lb + j) + q];
       }
 #pragma unroll
       for (int j = 0; j < L; ++j) {
