@@ -149,3 +149,4 @@ def test_graph_of_repeated_applies(lname, overlap):
         assert torch.equal(y, ref)
     else:
         assert _rel(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-12
+

@@ -17,13 +17,14 @@ coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
 op = MassOperator(fs, quad)
 x = torch.from_numpy(x_np).cuda()
 y = torch.zeros_like(x)
+acc = "overwrite" not in sys.argv
 for _ in range(3):
-    op.apply(x, coords, y, accumulate=True)
+    op.apply(x, coords, y, accumulate=acc)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(10):
-    op.apply(x, coords, y, accumulate=True)
+    op.apply(x, coords, y, accumulate=acc)
 e1.record()
 torch.cuda.synchronize()
 print(sys.argv[2] if len(sys.argv) > 2 else "", sys.argv[1], e0.elapsed_time(e1) / 10)
