@@ -38,7 +38,8 @@ FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, only without the file
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=20,
+                   help="timed steps (>= 1)")
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--config", default="C2")
     p.add_argument("--schedule", default="auto")
@@ -46,7 +47,10 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=8.0,
                    help="CPU-baseline sample budget")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    return p.parse_args()
+    args = p.parse_args()
+    if args.steps < 1 or args.warmup < 0:
+        p.error("--steps must be >= 1 and --warmup >= 0")
+    return args
 
 
 def measured_peak():
@@ -439,9 +443,10 @@ def run_ours(args):
     # the K timed steps = K applies captured back to back in one CUDA
     # graph (no per-step host work; the same kernels as op.apply), the DG
     # stream kernels with programmatic dependent launch between steps
-    warm = op.graph(x, coords, y, repeat=args.warmup)
+    warm = op.graph(x, coords, y, repeat=max(1, args.warmup))
     steps = op.graph(x, coords, y, repeat=args.steps, overlap=True)
-    warm.replay()
+    if args.warmup > 0:
+        warm.replay()
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, device events, max over ranks ----------
