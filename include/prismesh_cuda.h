@@ -288,6 +288,15 @@ int pm_derive_edges(const int32_t *cell_vertices, int64_t n_cells,
                     int32_t *cell_edges, int64_t *n_edges, int32_t *status,
                     void *stream);
 
+/* The mesh's vertex graph for RCM (replaces mesh.py vertex_neighbours +
+ * the row lexsort of ordering.py rcm_order): CSR (offsets n_vertices+1
+ * int64, nbr 2*n_edges int32, device) of edge-adjacent vertices, every row
+ * sorted by (degree, index).  n_vertices < 2^24.  Synchronises the
+ * stream. */
+int pm_vertex_graph_sorted(const int32_t *edge_vertices, int64_t n_edges,
+                           int64_t n_vertices, int64_t *offsets, int32_t *nbr,
+                           void *stream);
+
 /* Device cell re-sort of apply_ordering (replaces ordering.py:142-152):
  * cells_out = forward[cell_vertices][perm] with perm the stable lexsort of
  * the rows' sorted new vertex triples; perm_out (optional) receives perm.

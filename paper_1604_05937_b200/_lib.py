@@ -89,6 +89,8 @@ SIGNATURES = {
     "pm_device_info": (ctypes.c_int, [_i32p, _i64p]),
     "pm_derive_edges": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64p,
                                        _i32p, _vp]),
+    "pm_vertex_graph_sorted": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp,
+                                              _vp]),
     "pm_reorder_cells": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _vp,
                                         _vp]),
     "pm_column_mass_strip_red_peer": (ctypes.c_int, [
@@ -483,6 +485,21 @@ def derive_edges_device(cell_vertices, num_vertices=None):
     if st.value:
         return None, None, st.value
     return ev[:n.value].cpu().numpy(), ce.cpu().numpy(), 0
+
+
+def vertex_graph_sorted_device(edge_vertices, n_vertices):
+    """(offsets int64 (n+1,), neighbours int64) of the vertex graph, rows
+    sorted by (degree, index), built on the device."""
+    import numpy as np
+    import torch
+    dev = cuda_device()
+    ev = host_tensor(edge_vertices, np.int32).to(dev)
+    ne = ev.shape[0]
+    off = torch.empty(n_vertices + 1, dtype=torch.int64, device=dev)
+    nb = torch.empty(2 * ne, dtype=torch.int32, device=dev)
+    check(host_lib().pm_vertex_graph_sorted(ptr(ev), ne, n_vertices, ptr(off),
+                                            ptr(nb), stream_ptr(None)))
+    return off.cpu().numpy(), nb.cpu().numpy().astype(np.int64)
 
 
 def reorder_cells_device(cell_vertices, forward):

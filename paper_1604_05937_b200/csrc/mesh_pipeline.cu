@@ -131,6 +131,48 @@ __global__ void k_gather_rows(const int32_t *__restrict__ mapped,
   }
 }
 
+__global__ void k_degree(const int32_t *__restrict__ ev, int64_t ne,
+                         int32_t *__restrict__ deg) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    atomicAdd(deg + ev[2 * e], 1);
+    atomicAdd(deg + ev[2 * e + 1], 1);
+  }
+}
+
+// both directions of every edge, keyed (row, degree(neighbour), neighbour)
+__global__ void k_graph_keys(const int32_t *__restrict__ ev, int64_t ne,
+                             const int32_t *__restrict__ deg,
+                             uint64_t *__restrict__ keys) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = (uint32_t)ev[2 * e], b = (uint32_t)ev[2 * e + 1];
+    keys[2 * e] = (a << 40) | ((uint64_t)deg[b] << 32) | b;
+    keys[2 * e + 1] = (b << 40) | ((uint64_t)deg[a] << 32) | a;
+  }
+}
+
+__global__ void k_graph_unpack(const uint64_t *__restrict__ keys, int64_t n,
+                               int32_t *__restrict__ nbr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    nbr[i] = (int32_t)(keys[i] & 0xffffffffull);
+}
+
+__global__ void k_widen(const int32_t *__restrict__ a, int64_t n,
+                        int64_t *__restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+__global__ void k_offsets(int64_t n, const int64_t *__restrict__ incl,
+                          int64_t *__restrict__ offsets) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    offsets[i] = i == 0 ? 0 : incl[i - 1];
+}
+
 int bits_for(int64_t n) { // bits to hold values < n (n >= 1)
   int b = 0;
   while (b < 63 && ((int64_t)1 << b) < n) ++b;
@@ -223,6 +265,71 @@ extern "C" int pm_derive_edges(const int32_t *cell_vertices, int64_t n_cells,
                               cudaMemcpyDeviceToHost, s));
   PM_CUDA_TRY(cudaStreamSynchronize(s));
   *n_edges = last;
+  return PM_OK;
+}
+
+// The vertex graph of the mesh (edge-adjacent vertices) as CSR with every
+// row sorted by (degree, index): the input of the RCM breadth-first search
+// (reference ordering.py rcm_order: mesh.vertex_neighbours + the row
+// lexsort), which the host then walks (pm_rcm_order).
+extern "C" int pm_vertex_graph_sorted(const int32_t *edge_vertices,
+                                      int64_t n_edges, int64_t n_vertices,
+                                      int64_t *offsets, int32_t *nbr,
+                                      void *stream) {
+  pm::clear_error();
+  if (n_edges < 0 || n_vertices < 0 || n_vertices >= (1 << 24) ||
+      2 * n_edges > INT32_MAX) {
+    pm::set_error("pm_vertex_graph_sorted: sizes out of range (vertices "
+                  "< 2^24, 2*edges < 2^31)");
+    return PM_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_vertices == 0) return PM_OK;
+  Scratch w(s);
+  int32_t *deg;
+  int64_t *deg64, *incl;
+  uint64_t *k0, *k1;
+  const int64_t n2 = 2 * n_edges;
+  PM_CUDA_TRY(w.get(&deg, n_vertices));
+  PM_CUDA_TRY(w.get(&deg64, n_vertices));
+  PM_CUDA_TRY(w.get(&incl, n_vertices));
+  PM_CUDA_TRY(w.get(&k0, n2));
+  PM_CUDA_TRY(w.get(&k1, n2));
+  PM_CUDA_TRY(cudaMemsetAsync(deg, 0, sizeof(int32_t) * n_vertices, s));
+  if (n_edges) {
+    k_degree<<<pm::grid_for(n_edges, 256), 256, 0, s>>>(edge_vertices,
+                                                        n_edges, deg);
+    PM_LAUNCH_CHECK("k_degree");
+  }
+  k_widen<<<pm::grid_for(n_vertices, 256), 256, 0, s>>>(deg, n_vertices,
+                                                        deg64);
+  PM_LAUNCH_CHECK("k_widen");
+  size_t tb = 0, tb2 = 0;
+  PM_CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tb, deg64, incl,
+                                            (int)n_vertices, s));
+  cub::DoubleBuffer<uint64_t> keys(k0, k1);
+  const int end_bit = 40 + bits_for(n_vertices);
+  if (n2)
+    PM_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb2, keys, (int)n2, 0,
+                                               end_bit, s));
+  char *tmp;
+  PM_CUDA_TRY(w.get(&tmp, tb > tb2 ? tb : tb2));
+  PM_CUDA_TRY(cub::DeviceScan::InclusiveSum(tmp, tb, deg64, incl,
+                                            (int)n_vertices, s));
+  k_offsets<<<pm::grid_for(n_vertices + 1, 256), 256, 0, s>>>(
+      n_vertices, incl, offsets);
+  PM_LAUNCH_CHECK("k_offsets");
+  if (n2) {
+    k_graph_keys<<<pm::grid_for(n_edges, 256), 256, 0, s>>>(
+        edge_vertices, n_edges, deg, k0);
+    PM_LAUNCH_CHECK("k_graph_keys");
+    PM_CUDA_TRY(cub::DeviceRadixSort::SortKeys(tmp, tb2, keys, (int)n2, 0,
+                                               end_bit, s));
+    k_graph_unpack<<<pm::grid_for(n2, 256), 256, 0, s>>>(keys.Current(), n2,
+                                                         nbr);
+    PM_LAUNCH_CHECK("k_graph_unpack");
+  }
+  PM_CUDA_TRY(cudaStreamSynchronize(s));
   return PM_OK;
 }
 

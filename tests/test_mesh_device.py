@@ -68,3 +68,44 @@ def test_apply_ordering_device_matches_host(ordering, monkeypatch):
     host = apply_ordering(m, p)
     for a in ("cell_vertices", "coords", "edge_vertices", "cell_edges"):
         assert np.array_equal(getattr(dev, a), getattr(host, a)), a
+
+
+@pytest.mark.parametrize("n,seed", [(200, 0), (257, 3)])
+def test_vertex_graph_sorted_matches_host(n, seed):
+    from paper_1604_05937_b200 import _lib
+    m = _random_mesh(n, seed)
+    off_d, nb_d = _lib.vertex_graph_sorted_device(m.edge_vertices,
+                                                  m.num_vertices)
+    off, nb = m.vertex_neighbours()
+    off = np.asarray(off, dtype=np.int64)
+    deg = np.diff(off)
+    rows = np.repeat(np.arange(m.num_vertices), deg)
+    nb = np.asarray(nb, dtype=np.int64)
+    ref = nb[np.lexsort((nb, deg[nb], rows))]
+    assert np.array_equal(off_d, off)
+    assert np.array_equal(nb_d, ref)
+
+
+@pytest.mark.parametrize("n,seed", [(200, None), (190, 5), (300, 11)])
+def test_rcm_device_graph_matches_host(n, seed, monkeypatch):
+    m = generate_unit_square_mesh(n) if seed is None else _random_mesh(n, seed)
+    assert M.device_mesh_ok(m.num_cells)
+    dev = rcm_vertex_order(m).forward
+    monkeypatch.setenv("PM_DEVICE_MESH", "0")
+    host = rcm_vertex_order(m).forward
+    assert np.array_equal(dev, host)
+
+
+def test_rcm_device_graph_disconnected(monkeypatch):
+    """Two squares side by side, no shared vertex: components in order of
+    their smallest vertex, each from its min-degree vertex."""
+    a = generate_unit_square_mesh(200)
+    cells = np.asarray(a.cell_vertices)
+    coords = np.asarray(a.coords)
+    nv = coords.shape[0]
+    both = BaseMesh(np.vstack([cells, cells + nv]),
+                    np.vstack([coords, coords + [2.0, 0.0]]))
+    dev = rcm_vertex_order(both).forward
+    monkeypatch.setenv("PM_DEVICE_MESH", "0")
+    host = rcm_vertex_order(both).forward
+    assert np.array_equal(dev, host)
