@@ -181,7 +181,6 @@ k_patch(const KronMat M, const PatchDev P, int64_t n_patches, int layers,
 template <class LY>
 static int patch_k(const LoopArgs &a, const PatchDev &P, int64_t n_patches,
                    int W) {
-  constexpr int K = LY::K;
   constexpr int CH = LY::CH0 > LY::CH1 ? LY::CH0 : LY::CH1;
   if (!a.mtri || !a.mline) {
     set_error("the patch kernel needs the Kronecker factors mtri/mline");
