@@ -459,8 +459,10 @@ def strip_chunk_width(layers: int) -> int:
     forced = int(os.environ.get("PM_STRIP_W", "0"))
     if forced in (8, 16, 32):
         return forced
+    # per-chunk charge 0.1 (measured: at λ = 100 W = 32 beats W = 16 on P1
+    # and P2 despite 28 % idle lanes, profiles/README.md)
     return min((8, 16, 32), key=lambda w: (-(-layers // w) * w / layers
-                                           + 0.05 * (-(-layers // w)), -w))
+                                           + 0.1 * (-(-layers // w)), -w))
 
 
 def strip_max_len(n_cells: int, layers: int) -> int:
