@@ -22,25 +22,40 @@ struct MapArgs {
 };
 
 // One thread per (cell, slot); consecutive threads write consecutive map
-// entries, so the int32 map store is fully coalesced.
+// entries, so the int32 map store is fully coalesced.  The per-slot
+// tables live in shared memory (lanes of a warp index different slots:
+// from kernel parameters that would serialise the constant cache) and the
+// (cell, slot) split is 32-bit when the map has < 2^31 entries.
+template <typename I>
 __global__ void __launch_bounds__(256)
 k_build_cell_map(const MapArgs a, const int32_t *__restrict__ cv,
                  const int32_t *__restrict__ ce, int64_t n_cells,
                  int32_t *__restrict__ map) {
-  const int64_t total = n_cells * a.k;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = t / a.k;
-    const int j = (int)(t - c * a.k);
-    const int kind = a.kind[j];
+  __shared__ int8_t s_kind[pm::kMaxSlots], s_local[pm::kMaxSlots];
+  __shared__ int64_t s_base[pm::kMaxSlots], s_col[pm::kMaxSlots];
+  for (int j = threadIdx.x; j < a.k; j += blockDim.x) {
+    const int kd = a.kind[j];
+    s_kind[j] = (int8_t)kd;
+    s_local[j] = a.local[j];
+    s_base[j] = a.start[kd] + a.within[j];
+    s_col[j] = a.column[kd];
+  }
+  __syncthreads();
+  const I k = (I)a.k;
+  const I total = (I)(n_cells * a.k);
+  for (I t = (I)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x); t < total;
+       t += (I)((int64_t)gridDim.x * blockDim.x)) {
+    const I c = t / k;
+    const int j = (int)(t - c * k);
+    const int kind = s_kind[j];
     int64_t ent;
     if (kind == 0)
-      ent = __ldg(cv + 3 * c + a.local[j]);
+      ent = __ldg(cv + 3 * (int64_t)c + s_local[j]);
     else if (kind == 1)
-      ent = __ldg(ce + 3 * c + a.local[j]);
+      ent = __ldg(ce + 3 * (int64_t)c + s_local[j]);
     else
       ent = c;
-    const int64_t v = a.start[kind] + a.column[kind] * ent + a.within[j];
+    const int64_t v = s_base[j] + s_col[j] * ent;
     map[t] = (int32_t)(uint32_t)(uint64_t)v; // numpy int64->int32 store wraps
   }
 }
@@ -54,18 +69,20 @@ __global__ void k_offsets(const OffsetArgs a, int k, int32_t *__restrict__ dst) 
   if (j < k) dst[j] = a.v[j];
 }
 
-// out[3*(i*(L+1)+l)+c]: one thread per output double, coalesced stores.
+// out[3*(i*(L+1)+l)+c]: one thread per output double, coalesced stores
+// (32-bit index split when the field has < 2^31 values).
+template <typename I>
 __global__ void __launch_bounds__(256)
 k_extrude(const double *__restrict__ base, int64_t n_vertices, int layers,
           double h, double *__restrict__ out) {
-  const int64_t per = 3 * (int64_t)(layers + 1);
-  const int64_t total = n_vertices * per;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / per;
+  const I per = 3 * (I)(layers + 1);
+  const I total = (I)(n_vertices * per);
+  for (I t = (I)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x); t < total;
+       t += (I)((int64_t)gridDim.x * blockDim.x)) {
+    const I i = t / per;
     const int r = (int)(t - i * per);
     const int l = r / 3, c = r - 3 * l;
-    out[t] = c < 2 ? __ldg(base + 2 * i + c) : (double)l * h;
+    out[t] = c < 2 ? __ldg(base + 2 * (int64_t)i + c) : (double)l * h;
   }
 }
 
@@ -176,8 +193,12 @@ extern "C" int pm_build_cell_map(const int32_t *cell_vertices,
       return PM_EINVAL;
     }
     const int64_t total = n_cells * st.k;
-    k_build_cell_map<<<pm::grid_for(total, 256), 256, 0, s>>>(
-        a, cell_vertices, cell_edges, n_cells, cell_map);
+    if (total < ((int64_t)1 << 31))
+      k_build_cell_map<uint32_t><<<pm::grid_for(total, 256), 256, 0, s>>>(
+          a, cell_vertices, cell_edges, n_cells, cell_map);
+    else
+      k_build_cell_map<int64_t><<<pm::grid_for(total, 256), 256, 0, s>>>(
+          a, cell_vertices, cell_edges, n_cells, cell_map);
     PM_LAUNCH_CHECK("k_build_cell_map");
   }
   if (offsets) {
@@ -202,8 +223,14 @@ extern "C" int pm_extrude_coordinates(const double *base_coords,
   }
   if (n_vertices == 0) return PM_OK;
   const int64_t total = n_vertices * 3 * (int64_t)(layers + 1);
-  k_extrude<<<pm::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      base_coords, n_vertices, layers, layer_height, out);
+  if (total < ((int64_t)1 << 31))
+    k_extrude<uint32_t><<<pm::grid_for(total, 256), 256, 0,
+                          (cudaStream_t)stream>>>(base_coords, n_vertices,
+                                                  layers, layer_height, out);
+  else
+    k_extrude<int64_t><<<pm::grid_for(total, 256), 256, 0,
+                         (cudaStream_t)stream>>>(base_coords, n_vertices,
+                                                 layers, layer_height, out);
   PM_LAUNCH_CHECK("k_extrude");
   return PM_OK;
 }
