@@ -69,20 +69,31 @@ __global__ void k_offsets(const OffsetArgs a, int k, int32_t *__restrict__ dst) 
   if (j < k) dst[j] = a.v[j];
 }
 
-// out[3*(i*(L+1)+l)+c]: one thread per output double, coalesced stores
-// (32-bit index split when the field has < 2^31 values).
+// out[3*(i*(L+1)+l)+c]: one thread per output pair, one 16-byte store
+// (out is 16-byte aligned), coalesced; 32-bit index split when the field
+// has < 2^31 values.
 template <typename I>
 __global__ void __launch_bounds__(256)
 k_extrude(const double *__restrict__ base, int64_t n_vertices, int layers,
           double h, double *__restrict__ out) {
   const I per = 3 * (I)(layers + 1);
   const I total = (I)(n_vertices * per);
-  for (I t = (I)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x); t < total;
-       t += (I)((int64_t)gridDim.x * blockDim.x)) {
-    const I i = t / per;
-    const int r = (int)(t - i * per);
+  auto value = [&](I i, int r) {
     const int l = r / 3, c = r - 3 * l;
-    out[t] = c < 2 ? __ldg(base + 2 * (int64_t)i + c) : (double)l * h;
+    return c < 2 ? __ldg(base + 2 * (int64_t)i + c) : (double)l * h;
+  };
+  for (I p = (I)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+       2 * p < total; p += (I)((int64_t)gridDim.x * blockDim.x)) {
+    const I t = 2 * p;
+    I i = t / per;
+    int r = (int)(t - i * per);
+    const double v0 = value(i, r);
+    if (t + 1 < total) {
+      if (++r == (int)per) r = 0, ++i;
+      reinterpret_cast<double2 *>(out)[p] = make_double2(v0, value(i, r));
+    } else {
+      out[t] = v0;
+    }
   }
 }
 
@@ -223,12 +234,16 @@ extern "C" int pm_extrude_coordinates(const double *base_coords,
   }
   if (n_vertices == 0) return PM_OK;
   const int64_t total = n_vertices * 3 * (int64_t)(layers + 1);
+  if (reinterpret_cast<uintptr_t>(out) & 15) {
+    pm::set_error("coordinate field must be 16-byte aligned");
+    return PM_EINVAL;
+  }
   if (total < ((int64_t)1 << 31))
-    k_extrude<uint32_t><<<pm::grid_for(total, 256), 256, 0,
+    k_extrude<uint32_t><<<pm::grid_for((total + 1) / 2, 256), 256, 0,
                           (cudaStream_t)stream>>>(base_coords, n_vertices,
                                                   layers, layer_height, out);
   else
-    k_extrude<int64_t><<<pm::grid_for(total, 256), 256, 0,
+    k_extrude<int64_t><<<pm::grid_for((total + 1) / 2, 256), 256, 0,
                          (cudaStream_t)stream>>>(base_coords, n_vertices,
                                                  layers, layer_height, out);
   PM_LAUNCH_CHECK("k_extrude");
