@@ -43,10 +43,7 @@ k_build_cell_map(const MapArgs a, const int32_t *__restrict__ cv,
   __syncthreads();
   const I k = (I)a.k;
   const I total = (I)(n_cells * a.k);
-  for (I t = (I)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x); t < total;
-       t += (I)((int64_t)gridDim.x * blockDim.x)) {
-    const I c = t / k;
-    const int j = (int)(t - c * k);
+  auto entry = [&](I c, int j) {
     const int kind = s_kind[j];
     int64_t ent;
     if (kind == 0)
@@ -56,7 +53,25 @@ k_build_cell_map(const MapArgs a, const int32_t *__restrict__ cv,
     else
       ent = c;
     const int64_t v = s_base[j] + s_col[j] * ent;
-    map[t] = (int32_t)(uint32_t)(uint64_t)v; // numpy int64->int32 store wraps
+    return (int32_t)(uint32_t)(uint64_t)v; // numpy int64->int32 store wraps
+  };
+  // four consecutive entries per thread: one division, one 16-byte store
+  for (I q = (I)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+       4 * q < total; q += (I)((int64_t)gridDim.x * blockDim.x)) {
+    const I t = 4 * q;
+    I c = t / k;
+    int j = (int)(t - c * k);
+    int32_t e[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      e[u] = t + u < total ? entry(c, j) : 0;
+      if (++j == (int)k) j = 0, ++c;
+    }
+    if (t + 3 < total) {
+      reinterpret_cast<int4 *>(map)[q] = make_int4(e[0], e[1], e[2], e[3]);
+    } else {
+      for (int u = 0; t + u < total; ++u) map[t + u] = e[u];
+    }
   }
 }
 
@@ -204,12 +219,19 @@ extern "C" int pm_build_cell_map(const int32_t *cell_vertices,
       return PM_EINVAL;
     }
     const int64_t total = n_cells * st.k;
+    if (reinterpret_cast<uintptr_t>(cell_map) & 15) {
+      pm::set_error("cell map must be 16-byte aligned");
+      return PM_EINVAL;
+    }
+    const unsigned g = pm::grid_for((total + 3) / 4, 256);
     if (total < ((int64_t)1 << 31))
-      k_build_cell_map<uint32_t><<<pm::grid_for(total, 256), 256, 0, s>>>(
-          a, cell_vertices, cell_edges, n_cells, cell_map);
+      k_build_cell_map<uint32_t><<<g, 256, 0, s>>>(a, cell_vertices,
+                                                  cell_edges, n_cells,
+                                                  cell_map);
     else
-      k_build_cell_map<int64_t><<<pm::grid_for(total, 256), 256, 0, s>>>(
-          a, cell_vertices, cell_edges, n_cells, cell_map);
+      k_build_cell_map<int64_t><<<g, 256, 0, s>>>(a, cell_vertices,
+                                                 cell_edges, n_cells,
+                                                 cell_map);
     PM_LAUNCH_CHECK("k_build_cell_map");
   }
   if (offsets) {
