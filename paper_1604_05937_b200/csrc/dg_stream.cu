@@ -250,13 +250,16 @@ static int dg_stream_launch(const LoopArgs &a, const MassMat<D> &M,
 // Stream pipeline shape: 8 stages x 2 CTAs/SM (default; 14 bulk loads of
 // 12 KB in flight per SM, no spills) or PM_STREAM_CFG=0: 6 stages x 3 CTAs
 // (measured 68% vs 76% of HBM on C2, profiles/).
-static int stream_cfg() {
-  static int cfg = -1;
-  if (cfg < 0) {
+// Default by DoFs per cell-layer: 256-cell-layer units, 2 CTAs/SM for
+// DG1 x DG1; 128-cell-layer units, 4 CTAs/SM for the smaller blocks
+// (measured 3-4 % faster for D = 1, 2, 3 at lambda = 100).
+static int stream_cfg(int D) {
+  static int cfg = -2;
+  if (cfg == -2) {
     const char *e = getenv("PM_STREAM_CFG");
-    cfg = e ? atoi(e) : 1;
+    cfg = e ? atoi(e) : -1;
   }
-  return cfg;
+  return cfg >= 0 ? cfg : (D >= 6 ? 1 : 2);
 }
 
 // cell-layers [cl_begin, n_cells*layers) of the DG field (cl_begin must be
@@ -265,7 +268,7 @@ template <int D>
 static int dg_stream_k(const LoopArgs &a, bool *handled, int64_t cl_begin) {
   *handled = false;
   const int64_t n_cl = a.n_cells * (int64_t)a.layers - cl_begin;
-  const int cfg = stream_cfg();
+  const int cfg = stream_cfg(D);
   const int T = cfg == 2 ? 128 : cfg == 3 ? 512 : kStreamT;
   const int64_t n_units = n_cl / T;
   if ((reinterpret_cast<uintptr_t>(a.x) | reinterpret_cast<uintptr_t>(a.y)) &
