@@ -193,6 +193,11 @@ extern "C" int pm_column_mass(const int32_t *delta6, int32_t k,
       rc = pm::launch_dg_stream(a, &handled);
       if (rc || handled) return rc;
     }
+    if (!cells && !a.accumulate) { // vertical-only cell columns
+      bool handled = false;
+      rc = pm::launch_cell_stream(a, delta6, &handled);
+      if (rc || handled) return rc;
+    }
     if (pm::column_supports(delta6)) return pm::launch_column(a, delta6, false);
     return pm::launch_generic(a, !a.dg_only, 0);
   case PM_VARIANT_STREAM: {

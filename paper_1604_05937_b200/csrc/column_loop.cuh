@@ -162,6 +162,8 @@ int launch_generic(const LoopArgs &a, bool atomic, int64_t cl_begin);
 int launch_dg_stream(const LoopArgs &a, bool *handled, int64_t cl_begin = 0);
 constexpr int kStreamT = 256; // cell-layers per DG stream unit (default)
 int launch_column(const LoopArgs &a, const int32_t *delta6, bool colored);
+int launch_cell_stream(const LoopArgs &a, const int32_t *delta6,
+                       bool *handled);
 bool column_supports(const int32_t *delta6);
 int launch_strip_bulk(const LoopArgs &a, const int32_t *delta6,
                       const int32_t *strip_ptr, const int32_t *steps,

@@ -150,3 +150,21 @@ def test_graph_of_repeated_applies(lname, overlap):
     else:
         assert _rel(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-12
 
+
+
+@pytest.mark.parametrize("lname", ["DG0xCG1", "DG1xCG1"])
+@pytest.mark.parametrize("n,layers,ordering", [(6, 16, "rcm"), (12, 20, "rcm"),
+                                               (16, 33, "random"),
+                                               (40, 17, "rcm")])
+def test_cell_stream_vs_oracle(lname, n, layers, ordering):
+    """Vertical-only cell columns through the TMA cell-stream kernel (units
+    overlapping by one cell-layer; column tops and unit boundaries)."""
+    from paper_1604_05937_b200.configs import base_mesh
+    from paper_1604_05937_b200.kernels import mass_action
+    from paper_1604_05937_b200.quadrature import prism_quadrature
+    base, _ = base_mesh(n, ordering)
+    fs = _space(base, layers, lname)
+    assert base.num_cells * layers > 256     # several units
+    f = np.random.default_rng(layers).uniform(-1, 1, fs.total_dofs)
+    got = mass_action(fs, f, quadrature=prism_quadrature(*quad_degrees(lname)))
+    assert _rel(got, _oracle(base, layers, lname, f)) <= 1e-12
