@@ -24,6 +24,8 @@
  *   pm_build_strips          <- host planner of that schedule
  *   pm_column_mass_strip_red <- same, global strips + REDG
  *   pm_build_global_strips   <- host planner of that schedule
+ *   pm_column_mass_patch_strips <- same, store-first strips inside patches
+ *   pm_build_patch_strips    <- host planner of that schedule
  *   pm_column_mass_strip_bulk<- same, TMA bulk-copy prefetch
  *   pm_column_mass_dg_range  <- the DG loop over a cell range (pipelining)
  *   pm_column_probe          <- SPEC.md:338-340 counting / gather kernels
@@ -251,6 +253,48 @@ int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                            int32_t *steps,
                            int32_t *steps_e /* NULL, or 2 edges per step */,
                            int64_t *totals);
+
+/* Store-first patch strips (PM_VARIANT_STRIPRED over patches): the cells
+ * are grouped into compact patches (patch_cells, patch_ptr: e.g. runs of the
+ * Morton order of the centroids) and walked as sequential strips that never
+ * leave their patch; item_ptr[p] .. item_ptr[p+1] are patch p's strips.
+ * A patch's strips are one continuous step stream (no window refill between
+ * strips): a strip's three fill steps flush the previous strip's window,
+ * its first two carry PM_STEP_NOCELL, and their edges (P2) are -1, e01, then
+ * e12, e02 (e_ab joins fill vertices a, b).  Step ids carry PM_STEP_STORE on
+ * the first residency of an entity whose cells all lie in one patch: the
+ * kernel stores that partial column instead of adding it.  zero_list = the other entities (code v, or
+ * n_vertices + e for edge e), cleared by the kernel's zero pass.
+ * Capacities: item_ptr n_patches+1, strip_ptr n_cells+1, steps 3*n_cells,
+ * steps_e 6*n_cells, zero_list n_vertices+n_edges; totals = {strips, steps,
+ * zero entities}.  Entity ids must stay below 2^29. */
+#define PM_STEP_STORE (1 << 30)
+/* ... and on a strip's first two (fill) steps: no cell after the step */
+#define PM_STEP_NOCELL (1 << 29)
+int pm_build_patch_strips(int64_t n_cells, int64_t n_vertices, int64_t n_edges,
+                          const int32_t *cell_vertices,
+                          const int32_t *cell_edges,
+                          const int32_t *patch_cells, const int32_t *patch_ptr,
+                          int64_t n_patches, int32_t max_len,
+                          int32_t *item_ptr, int32_t *strip_ptr,
+                          int32_t *steps,
+                          int32_t *steps_e /* NULL, or 2 edges per step */,
+                          int32_t *zero_list, int64_t *totals);
+
+/* The strip-REDG kernels over store-first patch strips (replaces the
+ * SPEC.md:333-364 coloured par-loop like pm_column_mass_strip_red).  Items
+ * are (patch, layer chunk); a segment walks the patch's strips in order.
+ * accumulate = 0: the zero pass clears the zero_list columns and the
+ * chunk-boundary levels, flagged residencies store; accumulate = 1: every
+ * residency adds (no zero pass). */
+int pm_column_mass_patch_strips(
+    const int32_t *delta6, int32_t k, int32_t layers, const double *coords,
+    const double *mref, const double *mtri, const double *mline,
+    const double *x, double *y, int64_t n_dofs, int32_t accumulate,
+    int64_t n_patches, int32_t chunk, const int32_t *item_ptr,
+    const int32_t *strip_ptr, const int32_t *steps,
+    const int32_t *steps_e /* P2: 2 edges/step */, int64_t n_vertices,
+    int64_t n_zero, const int32_t *zero_list, void *stream);
 
 /* Strip-REDG with the halo exchange fused in (multi-GPU): as
  * pm_column_mass_strip_red for vertex-column layouts, except that the

@@ -81,6 +81,13 @@ SIGNATURES = {
                                                _vp, _vp]),
     "pm_build_global_strips": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp,
                                               _i32, _vp, _vp, _vp, _vp]),
+    "pm_build_patch_strips": (ctypes.c_int, [_i64, _i64, _i64, _vp, _vp, _vp,
+                                             _vp, _i64, _i32, _vp, _vp, _vp,
+                                             _vp, _vp, _vp]),
+    "pm_column_mass_patch_strips": (ctypes.c_int, [
+        _i32p, _i32, _i32, _vp, ctypes.POINTER(_f64), ctypes.POINTER(_f64),
+        ctypes.POINTER(_f64), _vp, _vp, _i64, _i32, _i64, _i32, _vp, _vp,
+        _vp, _vp, _i64, _i64, _vp, _vp]),
     "pm_column_probe": (ctypes.c_int, [_i32, _i32, _i64, _i32, _vp, _vp, _vp,
                                        _vp, _vp]),
     "pm_halo_pack": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
@@ -353,6 +360,66 @@ def build_global_strips(base, max_len=32, cells=None, edges=False):
         return new_sp, st[idx].astype(np.int32), \
             np.ascontiguousarray(se[idx], dtype=np.int32)
     return new_sp, st[idx].astype(np.int32)
+
+
+def build_patch_strips(base, patch_cells, patch_ptr, max_len=1 << 30,
+                       edges=False):
+    """Store-first patch strips (host C++, pm_build_patch_strips): returns
+    (item_ptr, strip_ptr, steps[, steps_e], zero_list), all int32.  Cells
+    ``patch_cells[patch_ptr[p]:patch_ptr[p+1]]`` form patch p; step ids
+    carry ``STEP_STORE`` on the first residency of a patch-interior
+    entity; ``zero_list`` = entities shared by several patches (vertex v,
+    or n_vertices + edge e)."""
+    cv = np.ascontiguousarray(base.cell_vertices, dtype=np.int32)
+    ce = np.ascontiguousarray(base.cell_edges, dtype=np.int32)
+    n = cv.shape[0]
+    pc = np.ascontiguousarray(patch_cells, dtype=np.int32)
+    pp = np.ascontiguousarray(patch_ptr, dtype=np.int32)
+    n_p = pp.shape[0] - 1
+    n0, n1 = base.num_vertices, base.num_edges
+    ip = np.zeros(n_p + 1, dtype=np.int32)
+    sp = np.zeros(n + 1, dtype=np.int32)
+    st = np.zeros(3 * n + 3, dtype=np.int32)
+    se = np.zeros((3 * n + 3, 2), dtype=np.int32) if edges else None
+    zl = np.zeros(n0 + n1 + 1, dtype=np.int32)
+    tot = np.zeros(3, dtype=np.int64)
+    check(host_lib().pm_build_patch_strips(
+        n, n0, n1, cv.ctypes.data_as(_i32p), ce.ctypes.data_as(_i32p),
+        pc.ctypes.data_as(_i32p), pp.ctypes.data_as(_i32p), n_p, max_len,
+        ip.ctypes.data_as(_i32p), sp.ctypes.data_as(_i32p),
+        st.ctypes.data_as(_i32p),
+        None if se is None else se.ctypes.data_as(_i32p),
+        zl.ctypes.data_as(_i32p), tot.ctypes.data_as(_i64p)))
+    out = [ip, sp[:tot[0] + 1].copy(), st[:tot[1]].copy()]
+    if se is not None:
+        out.append(se[:tot[1]].copy())
+    out.append(zl[:tot[2]].copy())
+    return tuple(out)
+
+
+#: flag bits of patch-strip step ids: store-first residency, no cell after
+#: the step (a strip's first two fill steps)
+STEP_STORE = 1 << 30
+STEP_NOCELL = 1 << 29
+
+
+def column_mass_patch_strips(layout, k, layers, coords, mref, x, y, n_dofs,
+                             plan, kron, chunk, accumulate=False, stream=None,
+                             n_vertices=0):
+    """pm_column_mass_patch_strips; ``plan`` = device tensors (item_ptr,
+    strip_ptr, steps, steps_e or None, zero_list)."""
+    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
+    ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
+    d = layout.delta6()
+    ip, sp, st, se, zl = plan
+    rc = host_lib().pm_column_mass_patch_strips(
+        d.ctypes.data_as(_i32p), k, layers, ptr(coords), _f64ptr(m),
+        _f64ptr(mt), _f64ptr(ml), ptr(x), ptr(y), n_dofs,
+        1 if accumulate else 0, ip.shape[0] - 1, chunk, ptr(ip), ptr(sp),
+        ptr(st), ptr(se), n_vertices, zl.shape[0], ptr(zl),
+        stream_ptr(stream))
+    check(rc)
 
 
 def column_mass_strip_red(layout, k, layers, coords, mref, x, y, n_dofs,

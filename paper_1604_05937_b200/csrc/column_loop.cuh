@@ -123,6 +123,11 @@ struct LoopArgs {
   // peer whose y (global-index window, peer memory) is y_peer
   double *y_peer = nullptr;
   int64_t ghost_end = 0;
+  // store-first patch strips (pm_column_mass_patch_strips): the strips of
+  // group p are item_ptr[p] .. item_ptr[p+1] (NULL: one strip per group);
+  // store = flagged residencies store instead of adding
+  const int32_t *item_ptr = nullptr;
+  int store = 0;
 };
 
 // y = det * (Mtri (x) Mline) x by sum factorisation over a layout's

@@ -433,3 +433,190 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
   totals[1] = n_steps;
   return PM_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Patch strips for the store-first strip schedule (csrc/strip_red.cu).
+// Cells come grouped into compact patches (patch_cells[patch_ptr[p] ..
+// patch_ptr[p+1]), e.g. runs of the Morton order of the centroids).  Inside
+// a patch the cells are walked as sequential strips exactly like
+// pm_build_global_strips (start at the patch's lowest unused cell, one new
+// vertex per cell), but a strip never leaves its patch.  One warp segment
+// walks all strips of a patch in order, so every partial column of an
+// entity whose cells all lie in one patch comes from that segment: the
+// first residency of such an entity in the patch's walk is flagged
+// (PM_STEP_STORE, bit 30 of its step id) and the kernel STORES that partial
+// column instead of adding it — the entity needs no zeroing and its output
+// lines no L2 fill from HBM.  Entities touched by more than one patch are
+// listed in zero_list (code v for vertex v, n_vertices + e for edge e); the
+// kernel's zero pass clears them and every residency of theirs adds.
+// item_ptr[p] .. item_ptr[p+1] = the strips of patch p.
+// totals = {strips, steps, entities in zero_list}.
+// ---------------------------------------------------------------------------
+extern "C" int pm_build_patch_strips(
+    int64_t n_cells, int64_t n_vertices, int64_t n_edges,
+    const int32_t *cell_vertices, const int32_t *cell_edges,
+    const int32_t *patch_cells, const int32_t *patch_ptr, int64_t n_patches,
+    int32_t max_len, int32_t *item_ptr, int32_t *strip_ptr, int32_t *steps,
+    int32_t *steps_e, int32_t *zero_list, int64_t *totals) {
+  pm::clear_error();
+  if (n_cells < 0 || n_vertices < 0 || n_edges < 0 || n_patches < 0 ||
+      max_len < 1 || n_vertices + n_edges >= PM_STEP_NOCELL) {
+    pm::set_error("pm_build_patch_strips: bad arguments (entity ids must "
+                  "stay below 2^29)");
+    return PM_EINVAL;
+  }
+  if (n_patches > 0 && patch_ptr[n_patches] != n_cells) {
+    pm::set_error("pm_build_patch_strips: patches must cover every cell once");
+    return PM_EINVAL;
+  }
+  std::vector<int32_t> patch_of(n_cells, -1);
+  for (int64_t p = 0; p < n_patches; ++p)
+    for (int32_t i = patch_ptr[p]; i < patch_ptr[p + 1]; ++i) {
+      const int32_t c = patch_cells[i];
+      if (c < 0 || c >= n_cells || patch_of[c] >= 0) {
+        pm::set_error("pm_build_patch_strips: patch_cells is not a "
+                      "permutation of the cells");
+        return PM_EINVAL;
+      }
+      patch_of[c] = (int32_t)p;
+    }
+  // owner patch per entity, -2 = touched by several patches
+  std::vector<int32_t> vown(n_vertices, -1), eown(steps_e ? n_edges : 0, -1);
+  auto claim = [](std::vector<int32_t> &own, int64_t i, int32_t p) {
+    if (own[i] == -1)
+      own[i] = p;
+    else if (own[i] != p)
+      own[i] = -2;
+  };
+  for (int64_t c = 0; c < n_cells; ++c)
+    for (int k = 0; k < 3; ++k) {
+      claim(vown, cell_vertices[3 * c + k], patch_of[c]);
+      if (steps_e) claim(eown, cell_edges[3 * c + k], patch_of[c]);
+    }
+  std::vector<int32_t> ec(2 * (size_t)n_edges, -1);
+  for (int64_t c = 0; c < n_cells; ++c)
+    for (int k = 0; k < 3; ++k) {
+      const int64_t e = cell_edges[3 * c + k];
+      if (ec[2 * e] < 0)
+        ec[2 * e] = (int32_t)c;
+      else
+        ec[2 * e + 1] = (int32_t)c;
+    }
+  auto vid = [&](int64_t c, int k) { return cell_vertices[3 * c + k]; };
+  auto across = [&](int64_t c, int32_t u, int32_t w) -> int64_t {
+    for (int k = 0; k < 3; ++k) {
+      const int32_t a = vid(c, (k + 1) % 3), b = vid(c, (k + 2) % 3);
+      if ((a == u && b == w) || (a == w && b == u)) {
+        const int64_t e = cell_edges[3 * c + k];
+        return ec[2 * e] == c ? ec[2 * e + 1] : ec[2 * e];
+      }
+    }
+    return -1;
+  };
+  auto third = [&](int64_t c, int32_t u, int32_t w) -> int32_t {
+    for (int q = 0; q < 3; ++q)
+      if (vid(c, q) != u && vid(c, q) != w) return vid(c, q);
+    return -1;
+  };
+  auto opp = [&](int64_t c, int32_t v) -> int32_t {
+    for (int q = 0; q < 3; ++q)
+      if (vid(c, q) == v) return cell_edges[3 * c + q];
+    return -1;
+  };
+  std::vector<uint8_t> used(n_cells, 0);
+  std::vector<int32_t> vseen(n_vertices, -1), eseen(steps_e ? n_edges : 0, -1);
+  std::vector<int32_t> order;
+  int64_t n_strips = 0, n_steps = 0;
+  strip_ptr[0] = 0;
+  // a residency of entity i in patch p: flagged if it is the entity's first
+  // in the patch and no other patch touches the entity
+  auto flag = [&](std::vector<int32_t> &own, std::vector<int32_t> &seen,
+                  int32_t i, int32_t p) -> int32_t {
+    if (i < 0) return i;
+    if (seen[i] == p) return i;
+    seen[i] = p;
+    return own[i] == p ? (i | PM_STEP_STORE) : i;
+  };
+  for (int64_t p = 0; p < n_patches; ++p) {
+    item_ptr[p] = (int32_t)n_strips;
+    order.assign(patch_cells + patch_ptr[p], patch_cells + patch_ptr[p + 1]);
+    std::sort(order.begin(), order.end());
+    const int32_t pp = (int32_t)p;
+    auto ok = [&](int64_t j) { return j >= 0 && patch_of[j] == pp && !used[j]; };
+    for (const int32_t start : order) {
+      if (used[start]) continue;
+      int64_t cur = start;
+      used[cur] = 1;
+      int32_t win[3] = {vid(cur, 0), vid(cur, 1), vid(cur, 2)};
+      int64_t next = -1;
+      int best = -1;
+      for (int e = 0; e < 3; ++e) {
+        const int32_t a0 = vid(cur, e), a1 = vid(cur, (e + 1) % 3),
+                      a2 = vid(cur, (e + 2) % 3);
+        const int64_t j = across(cur, a1, a2);
+        if (!ok(j)) continue;
+        for (int dir = 0; dir < 2; ++dir) {
+          const int32_t u = dir ? a2 : a1, w = dir ? a1 : a2;
+          const int32_t nv = third(j, u, w);
+          const int64_t j2 = across(j, w, nv);
+          const int score = (ok(j2) && j2 != cur) ? 2 : 1;
+          if (score > best) {
+            best = score;
+            next = j;
+            win[0] = a0, win[1] = u, win[2] = w;
+          }
+        }
+      }
+      // fill: one continuous stream per patch, every step in normal form
+      // (slot s flushes / loads edge slots s+1, s+2): the first cell's
+      // edges arrive as (-1, -1), (e01, -1), (e12, e02) so each lands in the
+      // slot opposite its vertex and none is flushed before its cells ran
+      const int32_t fe[3][2] = {{-1, -1},
+                                {opp(cur, win[2]), -1},
+                                {opp(cur, win[0]), opp(cur, win[1])}};
+      for (int k = 0; k < 3; ++k) {
+        if (steps_e) {
+          steps_e[2 * n_steps] = flag(eown, eseen, fe[k][0], pp);
+          steps_e[2 * n_steps + 1] = flag(eown, eseen, fe[k][1], pp);
+        }
+        steps[n_steps++] =
+            flag(vown, vseen, win[k], pp) | (k < 2 ? PM_STEP_NOCELL : 0);
+      }
+      int32_t len = 1, slot = 0;
+      while (next >= 0 && len < max_len) {
+        const int32_t nv =
+            third(next, win[(slot + 1) % 3], win[(slot + 2) % 3]);
+        if (nv < 0) {
+          pm::set_error("pm_build_patch_strips: broken strip");
+          return PM_EINVAL;
+        }
+        used[next] = 1;
+        if (steps_e) {
+          steps_e[2 * n_steps] =
+              flag(eown, eseen, opp(next, win[(slot + 1) % 3]), pp);
+          steps_e[2 * n_steps + 1] =
+              flag(eown, eseen, opp(next, win[(slot + 2) % 3]), pp);
+        }
+        win[slot] = nv;
+        steps[n_steps++] = flag(vown, vseen, nv, pp);
+        cur = next;
+        slot = (slot + 1) % 3;
+        ++len;
+        const int64_t j = across(cur, win[(slot + 1) % 3], win[(slot + 2) % 3]);
+        next = ok(j) ? j : -1;
+      }
+      ++n_strips;
+      strip_ptr[n_strips] = (int32_t)n_steps;
+    }
+  }
+  item_ptr[n_patches] = (int32_t)n_strips;
+  int64_t nz = 0;
+  for (int64_t v = 0; v < n_vertices; ++v)
+    if (vown[v] < 0) zero_list[nz++] = (int32_t)v; // shared, or in no cell
+  for (int64_t e = 0; e < (int64_t)eown.size(); ++e)
+    if (eown[e] < 0) zero_list[nz++] = (int32_t)(n_vertices + e);
+  totals[0] = n_strips;
+  totals[1] = n_steps;
+  totals[2] = nz;
+  return PM_OK;
+}

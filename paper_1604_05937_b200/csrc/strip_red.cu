@@ -121,6 +121,20 @@ __device__ __forceinline__ void sr_cp8z(double *dst, const double *src,
                : "memory");
 }
 
+// Flush of a partial column element: mode 0 = nothing, 1 = add (REDG),
+// 2 = store (the first residency of a patch-interior entity, pm_build_patch_
+// strips); predicated, no branch
+__device__ __forceinline__ void sr_put(double *p, double v, int mode) {
+  asm volatile("{\n\t.reg .pred ps, pr;\n\t"
+               "setp.eq.s32 ps, %2, 2;\n\t"
+               "setp.eq.s32 pr, %2, 1;\n\t"
+               "@ps st.global.f64 [%0], %1;\n\t"
+               "@pr red.global.add.f64 [%0], %1;\n\t}" ::"l"(p),
+               "d"(v), "r"(mode)
+               : "memory");
+}
+constexpr int kIdMask = PM_STEP_NOCELL - 1; // entity id of a step record
+
 // element `v` of a column family with a stride in bytes (one IMAD.WIDE)
 template <class T>
 __device__ __forceinline__ T *col_at(T *base, int v, int stride_bytes) {
@@ -143,13 +157,14 @@ template <class LY, int L> constexpr int sr_blocks() {
 // the level between two of them is read once, and the per-step overhead
 // (ids, ring wait, addressing, loop) is paid once per L cell-layers.
 template <class LY, int W, bool SYM, int L, bool PEER = false,
-          int K = LY::K>
+          bool STREAM = false, int K = LY::K>
 __global__ void __launch_bounds__(sr_threads<LY>(), sr_blocks<LY, L>())
-k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
-            const int32_t *__restrict__ steps, int64_t n_strips, int layers,
+k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
+            const int32_t *__restrict__ strip_ptr,
+            const int32_t *__restrict__ steps, int64_t n_groups, int layers,
             const double *__restrict__ coords, const double *__restrict__ x,
             double *__restrict__ y, double *__restrict__ y_peer,
-            int ghost_end) {
+            int ghost_end, int store) {
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int SEGS = 32 / W;
   constexpr int CW = W * L; // levels per chunk
@@ -185,23 +200,36 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
     sr_ring[(size_t)NWARP * kSrDepth * SEGS * ES + i] = 0.0;
   __syncthreads();
 
-  // work item = (strip, layer chunk), chunk fastest: the chunks of a strip
+  // work item = (group, layer chunk), chunk fastest: the chunks of a group
   // run side by side, so the sectors two chunks of a vertex column share
-  // are fetched once (neighbouring strips are still close in time)
+  // are fetched once (neighbouring groups are still close in time).  A
+  // group is one global strip (item_ptr == NULL) or the strips of a patch
+  // (item_ptr[p] .. item_ptr[p+1]), walked one after the other.
   const int n_chunks = (layers + CW - 1) / CW;
-  const int64_t n_items = n_strips * n_chunks;
+  const int64_t n_items = n_groups * n_chunks;
   for (int64_t i0 = warp * SEGS; i0 < n_items; i0 += n_warps * SEGS) {
     const int64_t item = i0 + seg;
     const bool has = item < n_items;
-    const int64_t si = has ? item / n_chunks : 0;
+    const int64_t gi = has ? item / n_chunks : 0;
     const int l0 = has ? (int)(item % n_chunks) * CW : 0;
-    const int k0 = has ? __ldg(strip_ptr + si) : 0;
-    const int len = has ? __ldg(strip_ptr + si + 1) - k0 : 0;
+    // the group's steps are one contiguous range; in STREAM mode (patch
+    // strips) its strips follow each other without a window refill: the
+    // three fill steps of a strip flush the previous strip's vertices
+    const int64_t gs = item_ptr ? __ldg(item_ptr + gi) : gi;
+    const int64_t ge = item_ptr ? __ldg(item_ptr + gi + 1) : gi + 1;
+    const int k0 = has ? __ldg(strip_ptr + gs) : 0;
+    const int len = has ? __ldg(strip_ptr + ge) - k0 : 0;
     int maxlen = len;
 #pragma unroll
     for (int o = W; o < 32; o <<= 1)
       maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
     const int nl = has ? min(CW, layers - l0) : 0;
+    // store-first flushes: the chunk's bottom level is shared with the
+    // chunk below (its top), so lane 0 of an upper chunk always adds, and
+    // so does the top lane unless the chunk ends the column (the zero pass
+    // clears those levels)
+    const bool bot_st = L == 1 && (sl > 0 || l0 == 0);
+    const bool top_st = L == 1 && l0 + nl == layers;
     const int lb = L * sl; // the lane's first level in the chunk
     // source sizes of the lane's copies (8 inside the chunk, else 0)
     int fz[FR], cz[CR];
@@ -223,7 +251,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
     // xm, ym (mid-layer), dz; per-vertex accumulators acc[j][c][v]
     double zv[3][L][NC][NV], gm[3][L][3], acc[3][L][NC][NV];
     double *yc[3] = {yl, yl, yl}; // lane's first element of the column
-    bool live[3] = {false, false, false};
+    bool live[3] = {false, false, false}, st[3] = {false, false, false};
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -269,8 +297,8 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       }
       const int v = sid[k & (kSrIds - 1)];
 #if PM_SR16
-      const double *fp = col_at(xs, v, colb);
-      const double *cp = col_at(cs, v, ccolb);
+      const double *fp = col_at(xs, v & kIdMask, colb);
+      const double *cp = col_at(cs, v & kIdMask, ccolb);
       const int fsh = (int)(reinterpret_cast<uintptr_t>(fp) >> 3) & 1;
       const int csh = (int)(reinterpret_cast<uintptr_t>(cp) >> 3) & 1;
       if (k < len) {
@@ -288,8 +316,8 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
       rsh[slot] = fsh | (csh << 1);
 #else
       if (k < len) {
-        const double *fp = col_at(xl, v, colb);
-        const double *cp = col_at(cl0, v, ccolb);
+        const double *fp = col_at(xl, v & kIdMask, colb);
+        const double *cp = col_at(cl0, v & kIdMask, ccolb);
         double *e = entry(slot) + sl;
 #pragma unroll
         for (int r = 0; r < FR; ++r) sr_cp8z(e + W * r, fp + W * r, fz[r]);
@@ -334,12 +362,18 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
           const double below = __shfl_up_sync(FULL, vt[c < LV ? c : 0], 1, W);
           if (sl > 0) v0 += below;
         }
-        if (live[A]) {
+        const int add = live[A] ? 1 : 0;
+        const int put = live[A] ? (st[A] ? 2 : 1) : 0;
 #pragma unroll
-          for (int j = 0; j < L; ++j)
-            if (lb + j < nl) atomicAdd(yc[A] + j * CH + c, j ? vb[j][c] : v0);
-          if (c < LV && lb + L - 1 == nl - 1)
-            atomicAdd(yc[A] + L * CH + c, vt[c < LV ? c : 0]);
+        for (int j = 0; j < L; ++j)
+          sr_put(yc[A] + j * CH + c, j ? vb[j][c] : v0,
+                 lb + j >= nl                      ? 0
+                 : (j > 0 || c >= LV || bot_st) ? put
+                                                 : add);
+        if (c < LV)
+          sr_put(yc[A] + L * CH + c, vt[c < LV ? c : 0],
+                 lb + L - 1 != nl - 1 ? 0 : top_st ? put : add);
+        if (live[A]) {
           if (c < LV && L > 1 && lb < nl && lb + L - 1 > nl - 1) {
             // partial chunk ending inside this lane: its top is the level
             // after the last valid one
@@ -388,8 +422,11 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         gm[A][j][2] = g[j + 1][2] - g[j][2];
       }
       __syncwarp(); // reads done before the slot is refilled
-      yc[A] = col_at(PEER && rv[A] < ghost_end ? ylg : yl, rv[A], colb);
+      const int va = rv[A] & kIdMask;
+      const int rv_cell = rv[A]; // before the slot is refilled
+      yc[A] = col_at(PEER && va < ghost_end ? ylg : yl, va, colb);
       live[A] = act;
+      st[A] = L == 1 && store && (rv[A] & PM_STEP_STORE);
       // interval stage of the entering vertex
 #pragma unroll
       for (int j = 0; j < L; ++j)
@@ -420,7 +457,10 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
         // (with L > 1 a lane's upper level may lie past a partial chunk;
         // its accumulator feeds the chunk's top level, so it must stay 0)
         const double det =
-            (act && (L == 1 || lb + j < nl)) ? dj : 0.0;
+            (act && !(STREAM && (rv_cell & PM_STEP_NOCELL)) &&
+             (L == 1 || lb + j < nl))
+                ? dj
+                : 0.0;
         // triangle stage, det folded into the accumulation
         if constexpr (SYM) { // Mtri = ta I + tb J
           const double dta = det * M.ta, dtb = det * M.tb;
@@ -456,10 +496,14 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ strip_ptr,
     using S2 = std::integral_constant<int, 2>;
     using TF = std::true_type;
     using FF = std::false_type;
-    step(S0{}, TF{}, 0);
-    step(S1{}, TF{}, 1);
-    step(S2{}, TF{}, 2);
-    for (int k = 3; k < maxlen; k += 3) {
+    int kb = 0;
+    if constexpr (!STREAM) {
+      step(S0{}, TF{}, 0);
+      step(S1{}, TF{}, 1);
+      step(S2{}, TF{}, 2);
+      kb = 3;
+    }
+    for (int k = kb; k < maxlen; k += 3) {
       step(S0{}, FF{}, k);
       step(S1{}, FF{}, k + 1);
       step(S2{}, FF{}, k + 2);
@@ -478,7 +522,8 @@ static int strip_levels() {
   return e && atoi(e) == 2 ? 2 : 1;
 }
 
-template <class LY, int W, bool SYM, int L, bool PEER = false>
+template <class LY, int W, bool SYM, int L, bool PEER = false,
+          bool STREAM = false>
 static int strip_red_launch(const LoopArgs &a, const KronMat &M,
                             const int32_t *strip_ptr, const int32_t *steps,
                             int64_t n_strips) {
@@ -488,12 +533,12 @@ static int strip_red_launch(const LoopArgs &a, const KronMat &M,
   constexpr int T = sr_threads<LY>();
   const unsigned grid = grid_for(warps * 32, T, 8);
   const size_t smem = sr_smem<LY, W, L>();
-  PM_CUDA_TRY(cudaFuncSetAttribute(k_strip_red<LY, W, SYM, L, PEER>,
+  PM_CUDA_TRY(cudaFuncSetAttribute(k_strip_red<LY, W, SYM, L, PEER, STREAM>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-  k_strip_red<LY, W, SYM, L, PEER><<<grid, T, smem, a.s>>>(
-      M, strip_ptr, steps, n_strips, a.layers, a.coords, a.x, a.y, a.y_peer,
-      (int)a.ghost_end);
+  k_strip_red<LY, W, SYM, L, PEER, STREAM><<<grid, T, smem, a.s>>>(
+      M, a.item_ptr, strip_ptr, steps, n_strips, a.layers, a.coords, a.x, a.y,
+      a.y_peer, (int)a.ghost_end, a.store);
   PM_LAUNCH_CHECK("k_strip_red");
   return PM_OK;
 }
@@ -508,6 +553,13 @@ static int strip_red_w(const LoopArgs &a, const KronMat &M, bool sym,
                                                     n_strips);
     return strip_red_launch<LY, W, false, 1, true>(a, M, strip_ptr, steps,
                                                    n_strips);
+  }
+  if (a.item_ptr) { // store-first patch strips: one level per lane
+    if (sym)
+      return strip_red_launch<LY, W, true, 1, false, true>(a, M, strip_ptr,
+                                                           steps, n_strips);
+    return strip_red_launch<LY, W, false, 1, false, true>(a, M, strip_ptr,
+                                                          steps, n_strips);
   }
   if constexpr (LY::CH0 <= 2 && W <= 16) {
     if (L == 2 && sym)
@@ -561,13 +613,15 @@ template <class LY, int W> constexpr int sre_entry() {
 // spills at 168: measured 8 % slower)
 template <bool SYM> constexpr int sre_threads() { return SYM ? 384 : 256; }
 
-template <class LY, int W, bool SYM, int K = LY::K>
+template <class LY, int W, bool SYM, bool STREAM = false, int K = LY::K>
 __global__ void __launch_bounds__(sre_threads<SYM>(), 1)
-k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
+k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
+              const int32_t *__restrict__ strip_ptr,
               const int32_t *__restrict__ steps,
-              const int32_t *__restrict__ steps_e, int64_t n_strips,
+              const int32_t *__restrict__ steps_e, int64_t n_groups,
               int layers, int64_t e_start, const double *__restrict__ coords,
-              const double *__restrict__ x, double *__restrict__ y) {
+              const double *__restrict__ x, double *__restrict__ y,
+              int store) {
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int SEGS = 32 / W;
   constexpr int LV0 = LY::LV0, CH0 = LY::CH0, LV1 = LY::LV1, CH1 = LY::CH1;
@@ -600,20 +654,31 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
     sr_ring[(size_t)kSreWarps * kSrDepth * SEGS * ES + i] = 0.0;
   __syncthreads();
 
+  // items = (group, chunk) as in k_strip_red: a group is one global strip
+  // or the strips of a patch
   const int n_chunks = (layers + W - 1) / W;
-  const int64_t n_items = n_strips * n_chunks;
+  const int64_t n_items = n_groups * n_chunks;
   for (int64_t i0 = warp * SEGS; i0 < n_items; i0 += n_warps * SEGS) {
     const int64_t item = i0 + seg;
     const bool has = item < n_items;
-    const int64_t si = has ? item / n_chunks : 0;
+    const int64_t gi = has ? item / n_chunks : 0;
     const int l0 = has ? (int)(item % n_chunks) * W : 0;
-    const int k0 = has ? __ldg(strip_ptr + si) : 0;
-    const int len = has ? __ldg(strip_ptr + si + 1) - k0 : 0;
+    // one contiguous step range per group; STREAM (patch strips): strips
+    // follow each other, every step in normal form (fill steps bring the
+    // first cell's edges with -1 = none, see pm_build_patch_strips)
+    const int64_t gs = item_ptr ? __ldg(item_ptr + gi) : gi;
+    const int64_t ge = item_ptr ? __ldg(item_ptr + gi + 1) : gi + 1;
+    const int k0 = has ? __ldg(strip_ptr + gs) : 0;
+    const int len = has ? __ldg(strip_ptr + ge) - k0 : 0;
     int maxlen = len;
 #pragma unroll
     for (int o = W; o < 32; o <<= 1)
       maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
     const int nl = has ? min(W, layers - l0) : 0;
+    // store-first: the chunk's bottom level copy is shared with the chunk
+    // below, its top with the chunk above (both cleared by the zero pass)
+    const bool bot_st = sl > 0 || l0 == 0;
+    const bool top_st = l0 + nl == layers;
     const bool lane_ok = sl < nl;
     const int fl0 = nl * CH0 + LV0, fl1 = nl * CH1 + LV1, cl = 3 * (nl + 1);
     // the segment's chunk of every column (copies) and the lane's element
@@ -629,7 +694,11 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
     // accumulators per entity and interval function
     double zv[3][NV], ze[3][NV], gm[3][3], av[3][NV], ae[3][NV];
     double *yvc[3] = {yv0, yv0, yv0}, *yec[3] = {ye0, ye0, ye0};
-    bool vlive[3] = {false, false, false}, elive[3] = {false, false, false};
+    // per window slot a: bit a vertex live, 3+a edge live, 6+a vertex
+    // store-first, 9+a edge store-first (one register)
+    unsigned wf = 0;
+    auto setb = [&](int b, bool on) { wf = on ? (wf | (1u << b)) : (wf & ~(1u << b)); };
+    auto getb = [&](int b) { return ((wf >> b) & 1u) != 0; };
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
 #pragma unroll
@@ -672,10 +741,12 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
       const int e1 = sid[kSrIds + 2 * j], e2 = sid[kSrIds + 2 * j + 1];
       if (k < len) {
         double *en = entry(slot);
-        seg_copy(en, col_at(xv0, v, col0), fl0, FS0);
-        seg_copy(en + OC, col_at(cc0, v, ccol), cl, 3 * (W + 1));
-        seg_copy(en + OE1, col_at(xe0, e1, col1), fl1, FS1);
-        if (k >= 3) seg_copy(en + OE2, col_at(xe0, e2, col1), fl1, FS1);
+        seg_copy(en, col_at(xv0, v & kIdMask, col0), fl0, FS0);
+        seg_copy(en + OC, col_at(cc0, v & kIdMask, ccol), cl, 3 * (W + 1));
+        if (!STREAM || e1 >= 0)
+          seg_copy(en + OE1, col_at(xe0, e1 & kIdMask, col1), fl1, FS1);
+        if (STREAM ? e2 >= 0 : k >= 3)
+          seg_copy(en + OE2, col_at(xe0, e2 & kIdMask, col1), fl1, FS1);
       }
       sr_commit();
       rv[slot] = v, re1[slot] = e1, re2[slot] = e2;
@@ -686,14 +757,15 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
     // flush an entity residency: accumulators back to the layer block
     // (bottom copy v = 0, connecting v = 1..NV-2, top copy v = NV-1 added
     // one lane up; the chunk's top level by the last lane)
-    auto flush = [&](double (&acc)[NV], double *yp, bool live) {
+    auto flush = [&](double (&acc)[NV], double *yp, bool live, bool st) {
       const double below = __shfl_up_sync(FULL, acc[NV - 1], 1, W);
-      if (live && lane_ok) {
-        atomicAdd(yp, sl > 0 ? acc[0] + below : acc[0]);
+      const int add = live && lane_ok ? 1 : 0;
+      const int put = add ? (st ? 2 : 1) : 0;
+      sr_put(yp, sl > 0 ? acc[0] + below : acc[0], bot_st ? put : add);
 #pragma unroll
-        for (int v = 1; v < NV - 1; ++v) atomicAdd(yp + v, acc[v]);
-        if (sl == nl - 1) atomicAdd(yp + (NV - 1), acc[NV - 1]);
-      }
+      for (int v = 1; v < NV - 1; ++v) sr_put(yp + v, acc[v], put);
+      sr_put(yp + (NV - 1), acc[NV - 1],
+             sl != nl - 1 ? 0 : top_st ? put : add);
 #pragma unroll
       for (int v = 0; v < NV; ++v) acc[v] = 0.0;
     };
@@ -717,12 +789,12 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
       constexpr int A = decltype(A_)::value;
       constexpr bool FILL = decltype(FILL_)::value;
       constexpr int B1 = (A + 1) % 3, B2 = (A + 2) % 3;
-      flush(av[A], yvc[A], vlive[A]);
+      flush(av[A], yvc[A], getb(A), getb(6 + A));
       if (FILL) {
-        flush(ae[A], yec[A], elive[A]);
+        flush(ae[A], yec[A], getb(3 + A), getb(9 + A));
       } else {
-        flush(ae[B1], yec[B1], elive[B1]);
-        flush(ae[B2], yec[B2], elive[B2]);
+        flush(ae[B1], yec[B1], getb(3 + B1), getb(9 + B1));
+        flush(ae[B2], yec[B2], getb(3 + B2), getb(9 + B2));
       }
       const bool act = k < len;
       sr_wait<kSrDepth - 1>();
@@ -736,20 +808,29 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
         gm[A][1] = 0.5 * (g[1] + g[4]); // prism_abs_detj
         gm[A][2] = g[5] - g[2];
       }
-      yvc[A] = col_at(yv0, rv[A], col0);
-      vlive[A] = act;
+      yvc[A] = col_at(yv0, rv[A] & kIdMask, col0);
+      setb(A, act);
+      setb(6 + A, store && (rv[A] & PM_STEP_STORE));
       if (FILL) {
         enter(ze[A], en + OE1);
-        yec[A] = col_at(ye0, re1[A], col1);
-        elive[A] = act;
+        yec[A] = col_at(ye0, re1[A] & kIdMask, col1);
+        setb(3 + A, act);
+        setb(9 + A, store && (re1[A] & PM_STEP_STORE));
       } else {
-        enter(ze[B1], en + OE1);
-        yec[B1] = col_at(ye0, re1[A], col1);
-        elive[B1] = act;
-        enter(ze[B2], en + OE2);
-        yec[B2] = col_at(ye0, re2[A], col1);
-        elive[B2] = act;
+        // STREAM: an edge id -1 (fill steps) leaves the slot dead: zero
+        // block in, nothing flushed
+        const bool l1 = act && (!STREAM || re1[A] >= 0);
+        const bool l2 = act && (!STREAM || re2[A] >= 0);
+        enter(ze[B1], l1 ? en + OE1 : sr_zero);
+        yec[B1] = col_at(ye0, re1[A] & kIdMask, col1);
+        setb(3 + B1, l1);
+        setb(9 + B1, store && (re1[A] & PM_STEP_STORE));
+        enter(ze[B2], l2 ? en + OE2 : sr_zero);
+        yec[B2] = col_at(ye0, re2[A] & kIdMask, col1);
+        setb(3 + B2, l2);
+        setb(9 + B2, store && (re2[A] & PM_STEP_STORE));
       }
+      const int rv_cell = rv[A]; // before the slot is refilled
       __syncwarp();
       fetch(k + kSrDepth, A);
       if (FILL && A < 2) return; // window not full yet
@@ -758,7 +839,8 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
       const double dj = prism_abs_detj_mid(gm[0][0], gm[0][1], gm[0][2],
                                            gm[1][0], gm[1][1], gm[1][2],
                                            gm[2][0], gm[2][1], gm[2][2]);
-      const double det = act ? dj : 0.0;
+      const double det =
+          (act && !(STREAM && (rv_cell & PM_STEP_NOCELL))) ? dj : 0.0;
       // triangle stage (h: vertices 0-2, edges 3-5), det folded into the
       // accumulation
       if constexpr (SYM) { // block form a I + b J (KronMat::p)
@@ -800,19 +882,24 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ strip_ptr,
     using S2 = std::integral_constant<int, 2>;
     using TF = std::true_type;
     using FF = std::false_type;
-    step(S0{}, TF{}, 0);
-    step(S1{}, TF{}, 1);
-    step(S2{}, TF{}, 2);
-    for (int k = 3; k < maxlen; k += 3) {
+    int kb = 0;
+    if constexpr (!STREAM) {
+      step(S0{}, TF{}, 0);
+      step(S1{}, TF{}, 1);
+      step(S2{}, TF{}, 2);
+      kb = 3;
+    }
+    for (int k = kb; k < maxlen; k += 3) {
       step(S0{}, FF{}, k);
       step(S1{}, FF{}, k + 1);
       step(S2{}, FF{}, k + 2);
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      flush(av[a], yvc[a], vlive[a]);
-      flush(ae[a], yec[a], elive[a]);
+      flush(av[a], yvc[a], getb(a), getb(6 + a));
+      flush(ae[a], yec[a], getb(3 + a), getb(9 + a));
     }
+    sr_wait<0>(); // no copy in flight into the ring across items
   }
 }
 
@@ -844,17 +931,24 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
   } while (0)
 #define PM_SRE2(WW, SS)                                                      \
   do {                                                                       \
+    if (a.item_ptr)                                                          \
+      PM_SRE3(WW, SS, true);                                                 \
+    else                                                                     \
+      PM_SRE3(WW, SS, false);                                                \
+  } while (0)
+#define PM_SRE3(WW, SS, ST)                                                  \
+  do {                                                                       \
     constexpr int T = sre_threads<SS>(), NW = T / 32;                        \
     const unsigned grid = grid_for(warps * 32, T, 4);                        \
     const size_t smem = sizeof(double) * (NW * kSrDepth * (32 / WW) + 1) *   \
                             sre_entry<LY, WW>() +                            \
                         sizeof(int) * NW * (32 / WW) * 3 * kSrIds;           \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
-        k_strip_red_e<LY, WW, SS>,                                           \
+        k_strip_red_e<LY, WW, SS, ST>,                                       \
         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
-    k_strip_red_e<LY, WW, SS><<<grid, T, smem, a.s>>>(                       \
-        M, strip_ptr, steps, steps_e, n_strips, a.layers, e_start, a.coords, \
-        a.x, a.y);                                                           \
+    k_strip_red_e<LY, WW, SS, ST><<<grid, T, smem, a.s>>>(                   \
+        M, a.item_ptr, strip_ptr, steps, steps_e, n_strips, a.layers,        \
+        e_start, a.coords, a.x, a.y, a.store);                               \
   } while (0)
   if (W == 32)
     PM_SRE(32);
@@ -868,6 +962,7 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
   }
 #undef PM_SRE
 #undef PM_SRE2
+#undef PM_SRE3
   PM_LAUNCH_CHECK("k_strip_red_e");
   return PM_OK;
 }
@@ -878,6 +973,46 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
   X(0, 2, 0, 0, 0, 0)                                                        \
   X(3, 0, 0, 0, 0, 0)
 
+// Zero pass of the store-first patch strips: the columns of the entities
+// several patches touch (warp per entity, coalesced) ...
+__global__ void k_zero_entities(double *__restrict__ y,
+                                const int32_t *__restrict__ zero_list,
+                                int64_t n_zero, int64_t n_vertices, int colv,
+                                int cole, int64_t e_start) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n_zero; i += n_warps) {
+    const int64_t e = __ldg(zero_list + i);
+    double *col = e < n_vertices ? y + e * colv
+                                 : y + e_start + (e - n_vertices) * cole;
+    const int n = e < n_vertices ? colv : cole;
+    for (int j = lane; j < n; j += 32) col[j] = 0.0;
+  }
+}
+
+// ... and every column's level copies on the layer-chunk boundaries (the
+// top of one chunk item, the bottom of the next: both add)
+__global__ void k_zero_chunk_levels(double *__restrict__ y, int64_t n_vertices,
+                                    int64_t n_edges, int colv, int cole,
+                                    int64_t e_start, int ch0, int lv0, int ch1,
+                                    int lv1, int cw, int nb) {
+  const int64_t nv = n_vertices * nb * lv0, ne = n_edges * nb * lv1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nv + ne;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < nv) {
+      const int64_t ent = t / (nb * lv0);
+      const int r = (int)(t - ent * nb * lv0);
+      y[ent * colv + (int64_t)(r / lv0 + 1) * cw * ch0 + r % lv0] = 0.0;
+    } else {
+      const int64_t u = t - nv, ent = u / (nb * lv1);
+      const int r = (int)(u - ent * nb * lv1);
+      y[e_start + ent * cole + (int64_t)(r / lv1 + 1) * cw * ch1 + r % lv1] =
+          0.0;
+    }
+  }
+}
+
 } // namespace pm
 
 static int strip_red_entry(
@@ -886,9 +1021,12 @@ static int strip_red_entry(
     const double *x, double *y, int64_t n_dofs, int32_t accumulate,
     int64_t n_strips, int32_t chunk, const int32_t *strip_ptr,
     const int32_t *steps, const int32_t *steps_e, int64_t n_vertices,
-    double *y_peer, int64_t ghost_end, void *stream) {
+    double *y_peer, int64_t ghost_end, void *stream,
+    const int32_t *item_ptr = nullptr, int64_t n_zero = 0,
+    const int32_t *zero_list = nullptr) {
   pm::clear_error();
   pm::LoopArgs a;
+  a.item_ptr = item_ptr;
   a.y_peer = y_peer;
   a.ghost_end = y_peer ? ghost_end : 0;
   if (y_peer && (ghost_end < 0 || ghost_end > INT32_MAX ||
@@ -912,8 +1050,36 @@ static int strip_red_entry(
   a.x = x;
   a.y = y;
   a.s = (cudaStream_t)stream;
-  if (!accumulate && n_dofs > 0)
+  if (item_ptr && !accumulate && n_dofs > 0 && chunk > 0) {
+    // store-first patch strips: only the shared columns and the chunk
+    // boundary levels need zeroing
+    const int ch0 = delta6[0] + delta6[1], lv0 = delta6[0];
+    const int ch1 = delta6[2] + delta6[3], lv1 = delta6[2];
+    const int colv = layers * ch0 + lv0, cole = layers * ch1 + lv1;
+    const int64_t e_start = (int64_t)colv * n_vertices;
+    const int64_t n_edges = cole > 0 ? (n_dofs - e_start) / cole : 0;
+    if (n_zero < 0 || (n_zero > 0 && !zero_list) || e_start > n_dofs ||
+        e_start + n_edges * cole != n_dofs) {
+      pm::set_error("pm_column_mass_patch_strips: bad zero list / sizes");
+      return PM_EINVAL;
+    }
+    if (n_zero > 0) {
+      pm::k_zero_entities<<<pm::grid_for(n_zero * 32, 256, 4), 256, 0, a.s>>>(
+          y, zero_list, n_zero, n_vertices, colv, cole, e_start);
+      PM_LAUNCH_CHECK("k_zero_entities");
+    }
+    const int nb = (layers + chunk - 1) / chunk - 1;
+    const int64_t nlev = (n_vertices * lv0 + n_edges * lv1) * nb;
+    if (nlev > 0) {
+      pm::k_zero_chunk_levels<<<pm::grid_for(nlev, 256, 4), 256, 0, a.s>>>(
+          y, n_vertices, n_edges, colv, cole, e_start, ch0, lv0, ch1, lv1,
+          chunk, nb);
+      PM_LAUNCH_CHECK("k_zero_chunk_levels");
+    }
+    a.store = 1;
+  } else if (!accumulate && n_dofs > 0) {
     PM_CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)n_dofs * sizeof(double), a.s));
+  }
   if (n_strips == 0) return PM_OK;
   if (!coords || !x || !y || !strip_ptr || !steps) {
     pm::set_error("NULL device pointer");
@@ -957,4 +1123,29 @@ extern "C" int pm_column_mass_strip_red_peer(
                          n_dofs, accumulate, n_strips, chunk, strip_ptr,
                          steps, nullptr, n_vertices, y_peer,
                          ghost_vertex_end, stream);
+}
+
+extern "C" int pm_column_mass_patch_strips(
+    const int32_t *delta6, int32_t k, int32_t layers, const double *coords,
+    const double *mref, const double *mtri, const double *mline,
+    const double *x, double *y, int64_t n_dofs, int32_t accumulate,
+    int64_t n_patches, int32_t chunk, const int32_t *item_ptr,
+    const int32_t *strip_ptr, const int32_t *steps, const int32_t *steps_e,
+    int64_t n_vertices, int64_t n_zero, const int32_t *zero_list,
+    void *stream) {
+  if (!item_ptr && n_patches > 0) {
+    pm::clear_error();
+    pm::set_error("pm_column_mass_patch_strips: NULL item_ptr");
+    return PM_EINVAL;
+  }
+  if (pm::strip_levels() != 1) {
+    pm::clear_error();
+    pm::set_error("store-first patch strips run one level per lane "
+                  "(unset PM_STRIP_L)");
+    return PM_EINVAL;
+  }
+  return strip_red_entry(delta6, k, layers, coords, mref, mtri, mline, x, y,
+                         n_dofs, accumulate, n_patches, chunk, strip_ptr,
+                         steps, steps_e, n_vertices, nullptr, 0, stream,
+                         item_ptr, n_zero, zero_list);
 }

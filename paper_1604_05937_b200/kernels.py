@@ -154,6 +154,7 @@ class MassOperator:
         self._patch = None
         self._strip = None
         self._gstrips = None
+        self._pstrips = None
         self._strip_inv = None
         self._hbuf = None
         self._dev = _lib.cuda_device()
@@ -167,7 +168,8 @@ class MassOperator:
         """Column-loop kernel launches one ``apply`` issues."""
         if self.schedule in ("colored", "sequential") and self.share == 2:
             return self._color_lists()[1].shape[0] - 1
-        if self.schedule in ("auto", "patch", "stripred", "strip") and \
+        if self.schedule in ("auto", "patch", "stripred", "strip",
+                             "pstrip") and \
                 self.share == 2:
             return 1
         return 1
@@ -279,6 +281,44 @@ class MassOperator:
             self._gstrips = g
         return self._gstrips
 
+    def _patch_strips(self):
+        """Store-first patch strips (cached): Morton patches of the cells,
+        sequential strips inside each (pm_build_patch_strips)."""
+        if self._pstrips is None:
+            import torch
+            from .schedule import morton_order
+            base = self.fs.mesh.base
+            cv = np.asarray(base.cell_vertices)
+            cent = np.asarray(base.coords)[cv].mean(axis=1)
+            order = morton_order(cent).astype(np.int32)
+            W = strip_chunk_width(self.layers)
+            P = patch_strip_size(self.n_cells, self.layers)
+            ptr = np.arange(0, self.n_cells + P, P, dtype=np.int64)
+            ptr[-1] = self.n_cells
+            ptr = np.unique(ptr).astype(np.int32)
+            import os
+            if os.environ.get("PM_PATCH_ORDER", "rcm") == "rcm":
+                # patches in order of their mean vertex id: on RCM-ordered
+                # meshes the running patches sweep the mesh along the RCM
+                # front, like the global strips
+                key = np.add.reduceat(cv[order].astype(np.float64).sum(1),
+                                      ptr[:-1]) / np.diff(ptr)
+                porder = np.argsort(key, kind="stable")
+                lens = np.diff(ptr)[porder]
+                order = np.concatenate([order[ptr[p]:ptr[p + 1]]
+                                        for p in porder]).astype(np.int32)
+                ptr = np.zeros(len(lens) + 1, dtype=np.int32)
+                np.cumsum(lens, out=ptr[1:])
+            edges = bool(self.fs.layout.dofs(1, 0) or
+                         self.fs.layout.dofs(1, 1))
+            res = _lib.build_patch_strips(base, order, ptr, edges=edges)
+            if not edges:
+                res = res[:3] + (None,) + res[3:]
+            dev = tuple(None if a is None else torch.from_numpy(a).to(self._dev)
+                        for a in res)
+            self._pstrips = (dev, W)
+        return self._pstrips
+
     def _strip_plan(self):
         if self._strip is None:
             from .schedule import build_strip_plan
@@ -374,6 +414,18 @@ class MassOperator:
                                        stream=stream,
                                        n_vertices=self.fs.mesh.base.num_vertices)
             return y
+        if sched == "pstrip":
+            if not self.stripred_ok:
+                raise ValueError(
+                    f"the patch-strip schedule needs a vertex-column layout "
+                    f"and a vertex-permutation invariant triangle factor, got "
+                    f"{self.fs.layout.name}")
+            plan, W = self._patch_strips()
+            _lib.column_mass_patch_strips(
+                self.fs.layout, self.k, self.layers, coords, self.mref, x, y,
+                n, plan, self.kron, W, accumulate=accumulate, stream=stream,
+                n_vertices=self.fs.mesh.base.num_vertices)
+            return y
         if sched == "strip":
             if not self.strip_ok:
                 raise ValueError(
@@ -463,6 +515,18 @@ def strip_chunk_width(layers: int) -> int:
     # and P2 despite 28 % idle lanes, profiles/README.md)
     return min((8, 16, 32), key=lambda w: (-(-layers // w) * w / layers
                                            + 0.1 * (-(-layers // w)), -w))
+
+
+def patch_strip_size(n_cells: int, layers: int) -> int:
+    """Cells per patch of the store-first patch strips: large patches share
+    fewer entities (zeroed, added), small ones give enough (patch, chunk)
+    items to fill 148 SMs; PM_PATCH_CELLS overrides (tuning knob)."""
+    import os
+    forced = int(os.environ.get("PM_PATCH_CELLS", "0"))
+    if forced > 0:
+        return forced
+    chunks = -(-layers // strip_chunk_width(layers))
+    return int(max(32, min(512, n_cells * chunks // (148 * 64))))
 
 
 def strip_max_len(n_cells: int, layers: int) -> int:

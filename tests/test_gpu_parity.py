@@ -127,7 +127,7 @@ def test_arity_and_mesh_mismatch_rejected(gmesh):
 
 
 SCHEDULES = ("auto", "atomic", "colored", "column", "patch", "strip",
-             "stripred")
+             "stripred", "pstrip")
 
 
 def _schedule_applies(lname, schedule):
@@ -135,7 +135,7 @@ def _schedule_applies(lname, schedule):
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "P2xP2", "VP1")
     if schedule == "strip":
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1")
-    if schedule == "stripred":
+    if schedule in ("stripred", "pstrip"):
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1", "P2xP2")
     return True
 
@@ -403,6 +403,34 @@ def test_stripred_layers(lname, layers):
     ref = _oracle_for(w, fs).assemble(x)
     assert _rel(y, ref) <= 1e-10
     y2 = op.apply(xd, coords, torch.from_numpy(y).cuda(), accumulate=True)
+    assert _rel(y2.cpu().numpy(), 2 * ref) <= 1e-10
+
+
+@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1", "CG1xDG1", "CG1xDG0",
+                                   "P2xP2"))
+@pytest.mark.parametrize("layers", (1, 5, 16, 33, 64, 100))
+@pytest.mark.parametrize("patch", (1, 8, 64, 100000))
+def test_patch_strips_layers(lname, layers, patch, monkeypatch):
+    """Store-first patch strips: every DoF written (y starts as NaN), equal
+    to the oracle, for one-cell patches (everything shared), small and
+    whole-mesh patches and every chunk-boundary case; accumulate adds."""
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator
+    monkeypatch.setenv("PM_PATCH_CELLS", str(patch))
+    w = configs.Workload("psl", 12, layers, lname, quad_degrees(lname),
+                         ordering="random", jitter=0.2)
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    op = MassOperator(fs, quad, schedule="pstrip")
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    xd = torch.from_numpy(x).cuda()
+    y = torch.full_like(xd, float("nan"))
+    op.apply(xd, coords, y)
+    ref = _oracle_for(w, fs).assemble(x)
+    yh = y.cpu().numpy()
+    assert np.isfinite(yh).all()
+    assert _rel(yh, ref) <= 1e-10
+    y2 = op.apply(xd, coords, y, accumulate=True)
     assert _rel(y2.cpu().numpy(), 2 * ref) <= 1e-10
 
 

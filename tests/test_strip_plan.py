@@ -170,3 +170,83 @@ def test_global_strip_edges(n, ordering, max_len):
                 for b in range(3):
                     others = {win[(b + 1) % 3], win[(b + 2) % 3]}
                     assert set(ev[ewin[b]].tolist()) == others
+
+
+@pytest.mark.parametrize("n,ordering", ((7, "rcm"), (12, "random"),
+                                        (16, "rcm")))
+@pytest.mark.parametrize("patch", (1, 5, 40, 10000))
+def test_patch_strips_plan(n, ordering, patch):
+    """pm_build_patch_strips, emulated the way k_strip_red(_e) STREAM walks
+    it: one continuous step stream per patch, step K flushes and refills
+    vertex slot K % 3 and edge slots K+1, K+2 (-1 = none).  Every cell is
+    visited once with a consistent window (edge slot a opposite vertex slot
+    a), and the store-first flags make each entity's first flushed write in
+    a patch a store that no other patch races with."""
+    from paper_1604_05937_b200 import _lib
+    from paper_1604_05937_b200.configs import base_mesh
+    from paper_1604_05937_b200.schedule import morton_order
+    base, _ = base_mesh(n, ordering, 0.2)
+    cv = np.asarray(base.cell_vertices)
+    ce = np.asarray(base.cell_edges)
+    nc, n0 = cv.shape[0], base.num_vertices
+    order = morton_order(np.asarray(base.coords)[cv].mean(axis=1))
+    ptr = np.unique(np.append(np.arange(0, nc, patch), nc))
+    patch_of = np.empty(nc, dtype=np.int64)
+    for p in range(len(ptr) - 1):
+        patch_of[order[ptr[p]:ptr[p + 1]]] = p
+    ip, sp, st, se, zl = _lib.build_patch_strips(base, order, ptr, edges=True)
+    S, NOCELL = _lib.STEP_STORE, _lib.STEP_NOCELL
+    mask = NOCELL - 1
+    zero = set(zl.tolist())
+    owners = {}
+    edge_of = {}
+    for c in range(nc):
+        for q in range(3):
+            owners.setdefault(int(cv[c, q]), set()).add(patch_of[c])
+            owners.setdefault(n0 + int(ce[c, q]), set()).add(patch_of[c])
+            a, b = sorted((int(cv[c, (q + 1) % 3]), int(cv[c, (q + 2) % 3])))
+            edge_of[(a, b)] = int(ce[c, q])
+    shared = {e for e, o in owners.items() if len(o) > 1}
+    assert zero == shared
+    stored = set()
+    cells_seen = []
+    sorted_cells = {tuple(sorted(r)): i for i, r in enumerate(cv.tolist())}
+    for p in range(len(ptr) - 1):
+        touched = set()
+
+        def flush(res):
+            if res is None:
+                return
+            code, flag = res
+            if flag:
+                assert code not in zero and code not in stored
+                stored.add(code)
+            else:
+                assert code in zero or code in touched
+            touched.add(code)
+
+        vs, es = [None] * 3, [None] * 3
+        k0, k1 = sp[ip[p]], sp[ip[p + 1]]
+        for K in range(k1 - k0):
+            A = K % 3
+            raw = int(st[k0 + K])
+            flush(vs[A])
+            vs[A] = (raw & mask, raw & S)
+            for q, B in enumerate(((A + 1) % 3, (A + 2) % 3)):
+                flush(es[B])
+                e = int(se[k0 + K, q])
+                es[B] = None if e < 0 else (n0 + (e & mask), e & S)
+            if raw & NOCELL:
+                continue
+            win = [v[0] for v in vs]
+            c = sorted_cells[tuple(sorted(win))]
+            assert patch_of[c] == p
+            cells_seen.append(c)
+            for a in range(3):
+                u, w = sorted((win[(a + 1) % 3], win[(a + 2) % 3]))
+                assert es[a] is not None and es[a][0] == n0 + edge_of[(u, w)]
+        for r in vs + es:
+            flush(r)
+    assert sorted(cells_seen) == list(range(nc))
+    # every entity of some cell is zeroed or stored exactly once
+    assert stored | zero == set(owners)
