@@ -159,7 +159,8 @@ int pm_column_mass_strip(const int32_t *delta6, int32_t k, int32_t layers,
 /* Global-strip schedule (PM_VARIANT_STRIPRED) for vertex-column layouts:
  * sequential strips over the whole mesh (pm_build_global_strips), one
  * register window per W-lane segment, one coalesced fp64 REDG per
- * departing vertex.  accumulate = 0 zeroes y first. */
+ * departing vertex.  accumulate = 0 zeroes y first.  chunk = lanes (levels)
+ * per segment: 8, 16 or 32. */
 int pm_column_mass_strip_red(const int32_t *delta6, int32_t k, int32_t layers,
                              const double *coords, const double *mref,
                              const double *mtri, const double *mline,

@@ -128,6 +128,9 @@ struct LoopArgs {
   // store = flagged residencies store instead of adding
   const int32_t *item_ptr = nullptr;
   int store = 0;
+  // strip kernels: the launch covers levels [lbeg, lend) of the columns in
+  // chunks of its own width (mixed-width chunk plans, strip_red.cu)
+  int lbeg = 0, lend = 0;
 };
 
 // y = det * (Mtri (x) Mline) x by sum factorisation over a layout's

@@ -133,6 +133,14 @@ __device__ __forceinline__ void sr_put(double *p, double v, int mode) {
                "d"(v), "r"(mode)
                : "memory");
 }
+// predicated REDG (no branch around it)
+__device__ __forceinline__ void sr_red(double *p, double v, bool on) {
+  asm volatile("{\n\t.reg .pred q;\n\t"
+               "setp.ne.b32 q, %2, 0;\n\t"
+               "@q red.global.add.f64 [%0], %1;\n\t}" ::"l"(p),
+               "d"(v), "r"((int)on)
+               : "memory");
+}
 constexpr int kIdMask = PM_STEP_NOCELL - 1; // entity id of a step record
 
 // element `v` of a column family with a stride in bytes (one IMAD.WIDE)
@@ -162,10 +170,13 @@ __global__ void __launch_bounds__(sr_threads<LY>(), sr_blocks<LY, L>())
 k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
             const int32_t *__restrict__ strip_ptr,
             const int32_t *__restrict__ steps, int64_t n_groups, int layers,
+            int lbeg, int lend,
             const double *__restrict__ coords, const double *__restrict__ x,
             double *__restrict__ y, double *__restrict__ y_peer,
             int ghost_end, int store) {
   constexpr unsigned FULL = 0xffffffffu;
+  // step ids carry flag bits only in STREAM mode
+  constexpr int IDM = STREAM ? kIdMask : -1;
   constexpr int SEGS = 32 / W;
   constexpr int CW = W * L; // levels per chunk
   constexpr int LV = LY::LV0;
@@ -205,13 +216,15 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
   // are fetched once (neighbouring groups are still close in time).  A
   // group is one global strip (item_ptr == NULL) or the strips of a patch
   // (item_ptr[p] .. item_ptr[p+1]), walked one after the other.
-  const int n_chunks = (layers + CW - 1) / CW;
+  // this launch covers levels [lbeg, lend) (a mixed-width chunk plan runs
+  // one launch per width); column strides stay those of all `layers`
+  const int n_chunks = (lend - lbeg + CW - 1) / CW;
   const int64_t n_items = n_groups * n_chunks;
   for (int64_t i0 = warp * SEGS; i0 < n_items; i0 += n_warps * SEGS) {
     const int64_t item = i0 + seg;
     const bool has = item < n_items;
     const int64_t gi = has ? item / n_chunks : 0;
-    const int l0 = has ? (int)(item % n_chunks) * CW : 0;
+    const int l0 = has ? lbeg + (int)(item % n_chunks) * CW : 0;
     // the group's steps are one contiguous range; in STREAM mode (patch
     // strips) its strips follow each other without a window refill: the
     // three fill steps of a strip flush the previous strip's vertices
@@ -223,7 +236,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
 #pragma unroll
     for (int o = W; o < 32; o <<= 1)
       maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
-    const int nl = has ? min(CW, layers - l0) : 0;
+    const int nl = has ? min(CW, lend - l0) : 0;
     // store-first flushes: the chunk's bottom level is shared with the
     // chunk below (its top), so lane 0 of an upper chunk always adds, and
     // so does the top lane unless the chunk ends the column (the zero pass
@@ -297,8 +310,8 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
       }
       const int v = sid[k & (kSrIds - 1)];
 #if PM_SR16
-      const double *fp = col_at(xs, v & kIdMask, colb);
-      const double *cp = col_at(cs, v & kIdMask, ccolb);
+      const double *fp = col_at(xs, v & IDM, colb);
+      const double *cp = col_at(cs, v & IDM, ccolb);
       const int fsh = (int)(reinterpret_cast<uintptr_t>(fp) >> 3) & 1;
       const int csh = (int)(reinterpret_cast<uintptr_t>(cp) >> 3) & 1;
       if (k < len) {
@@ -316,8 +329,8 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
       rsh[slot] = fsh | (csh << 1);
 #else
       if (k < len) {
-        const double *fp = col_at(xl, v & kIdMask, colb);
-        const double *cp = col_at(cl0, v & kIdMask, ccolb);
+        const double *fp = col_at(xl, v & IDM, colb);
+        const double *cp = col_at(cl0, v & IDM, ccolb);
         double *e = entry(slot) + sl;
 #pragma unroll
         for (int r = 0; r < FR; ++r) sr_cp8z(e + W * r, fp + W * r, fz[r]);
@@ -362,17 +375,27 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
           const double below = __shfl_up_sync(FULL, vt[c < LV ? c : 0], 1, W);
           if (sl > 0) v0 += below;
         }
-        const int add = live[A] ? 1 : 0;
-        const int put = live[A] ? (st[A] ? 2 : 1) : 0;
+        if constexpr (STREAM) { // store-first patch strips
+          const int add = live[A] ? 1 : 0;
+          const int put = live[A] ? (st[A] ? 2 : 1) : 0;
 #pragma unroll
-        for (int j = 0; j < L; ++j)
-          sr_put(yc[A] + j * CH + c, j ? vb[j][c] : v0,
-                 lb + j >= nl                      ? 0
-                 : (j > 0 || c >= LV || bot_st) ? put
-                                                 : add);
-        if (c < LV)
-          sr_put(yc[A] + L * CH + c, vt[c < LV ? c : 0],
-                 lb + L - 1 != nl - 1 ? 0 : top_st ? put : add);
+          for (int j = 0; j < L; ++j)
+            sr_put(yc[A] + j * CH + c, j ? vb[j][c] : v0,
+                   lb + j >= nl                      ? 0
+                   : (j > 0 || c >= LV || bot_st) ? put
+                                                   : add);
+          if (c < LV)
+            sr_put(yc[A] + L * CH + c, vt[c < LV ? c : 0],
+                   lb + L - 1 != nl - 1 ? 0 : top_st ? put : add);
+        } else {
+#pragma unroll
+          for (int j = 0; j < L; ++j)
+            sr_red(yc[A] + j * CH + c, j ? vb[j][c] : v0,
+                   live[A] && lb + j < nl);
+          if (c < LV)
+            sr_red(yc[A] + L * CH + c, vt[c < LV ? c : 0],
+                   live[A] && lb + L - 1 == nl - 1);
+        }
         if (live[A]) {
           if (c < LV && L > 1 && lb < nl && lb + L - 1 > nl - 1) {
             // partial chunk ending inside this lane: its top is the level
@@ -422,7 +445,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         gm[A][j][2] = g[j + 1][2] - g[j][2];
       }
       __syncwarp(); // reads done before the slot is refilled
-      const int va = rv[A] & kIdMask;
+      const int va = rv[A] & IDM;
       const int rv_cell = rv[A]; // before the slot is refilled
       yc[A] = col_at(PEER && va < ghost_end ? ylg : yl, va, colb);
       live[A] = act;
@@ -528,7 +551,8 @@ static int strip_red_launch(const LoopArgs &a, const KronMat &M,
                             const int32_t *strip_ptr, const int32_t *steps,
                             int64_t n_strips) {
   const int segs = 32 / W;
-  const int64_t items = n_strips * ((a.layers + W * L - 1) / (W * L));
+  const int64_t items =
+      n_strips * ((a.lend - a.lbeg + W * L - 1) / (W * L));
   const int64_t warps = (items + segs - 1) / segs;
   constexpr int T = sr_threads<LY>();
   const unsigned grid = grid_for(warps * 32, T, 8);
@@ -537,7 +561,8 @@ static int strip_red_launch(const LoopArgs &a, const KronMat &M,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
   k_strip_red<LY, W, SYM, L, PEER, STREAM><<<grid, T, smem, a.s>>>(
-      M, a.item_ptr, strip_ptr, steps, n_strips, a.layers, a.coords, a.x, a.y,
+      M, a.item_ptr, strip_ptr, steps, n_strips, a.layers, a.lbeg, a.lend,
+      a.coords, a.x, a.y,
       a.y_peer, (int)a.ghost_end, a.store);
   PM_LAUNCH_CHECK("k_strip_red");
   return PM_OK;
@@ -572,8 +597,21 @@ static int strip_red_w(const LoopArgs &a, const KronMat &M, bool sym,
 }
 
 template <class LY>
-static int strip_red_k(const LoopArgs &a, const int32_t *strip_ptr,
-                       const int32_t *steps, int64_t n_strips, int W) {
+static int strip_red_k1(const LoopArgs &a, const int32_t *strip_ptr,
+                        const int32_t *steps, int64_t n_strips, int W);
+
+template <class LY>
+static int strip_red_k(const LoopArgs &a0, const int32_t *strip_ptr,
+                       const int32_t *steps, int64_t n_strips, int chunk) {
+  LoopArgs a = a0; // one launch over all levels (lbeg / lend: strip_red_k1)
+  a.lbeg = 0;
+  a.lend = a0.layers;
+  return strip_red_k1<LY>(a, strip_ptr, steps, n_strips, chunk);
+}
+
+template <class LY>
+static int strip_red_k1(const LoopArgs &a, const int32_t *strip_ptr,
+                        const int32_t *steps, int64_t n_strips, int W) {
   if (!a.mtri || !a.mline) {
     set_error("the strip kernel needs the Kronecker factors mtri/mline");
     return PM_EINVAL;
@@ -619,10 +657,12 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
               const int32_t *__restrict__ strip_ptr,
               const int32_t *__restrict__ steps,
               const int32_t *__restrict__ steps_e, int64_t n_groups,
-              int layers, int64_t e_start, const double *__restrict__ coords,
+              int layers, int lbeg, int lend, int64_t e_start,
+              const double *__restrict__ coords,
               const double *__restrict__ x, double *__restrict__ y,
               int store) {
   constexpr unsigned FULL = 0xffffffffu;
+  constexpr int IDM = STREAM ? kIdMask : -1; // flag bits only in STREAM mode
   constexpr int SEGS = 32 / W;
   constexpr int LV0 = LY::LV0, CH0 = LY::CH0, LV1 = LY::LV1, CH1 = LY::CH1;
   constexpr int NV = LY::NV;
@@ -656,13 +696,13 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
 
   // items = (group, chunk) as in k_strip_red: a group is one global strip
   // or the strips of a patch
-  const int n_chunks = (layers + W - 1) / W;
+  const int n_chunks = (lend - lbeg + W - 1) / W; // levels [lbeg, lend)
   const int64_t n_items = n_groups * n_chunks;
   for (int64_t i0 = warp * SEGS; i0 < n_items; i0 += n_warps * SEGS) {
     const int64_t item = i0 + seg;
     const bool has = item < n_items;
     const int64_t gi = has ? item / n_chunks : 0;
-    const int l0 = has ? (int)(item % n_chunks) * W : 0;
+    const int l0 = has ? lbeg + (int)(item % n_chunks) * W : 0;
     // one contiguous step range per group; STREAM (patch strips): strips
     // follow each other, every step in normal form (fill steps bring the
     // first cell's edges with -1 = none, see pm_build_patch_strips)
@@ -674,7 +714,7 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
 #pragma unroll
     for (int o = W; o < 32; o <<= 1)
       maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
-    const int nl = has ? min(W, layers - l0) : 0;
+    const int nl = has ? min(W, lend - l0) : 0;
     // store-first: the chunk's bottom level copy is shared with the chunk
     // below, its top with the chunk above (both cleared by the zero pass)
     const bool bot_st = sl > 0 || l0 == 0;
@@ -741,12 +781,12 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
       const int e1 = sid[kSrIds + 2 * j], e2 = sid[kSrIds + 2 * j + 1];
       if (k < len) {
         double *en = entry(slot);
-        seg_copy(en, col_at(xv0, v & kIdMask, col0), fl0, FS0);
-        seg_copy(en + OC, col_at(cc0, v & kIdMask, ccol), cl, 3 * (W + 1));
+        seg_copy(en, col_at(xv0, v & IDM, col0), fl0, FS0);
+        seg_copy(en + OC, col_at(cc0, v & IDM, ccol), cl, 3 * (W + 1));
         if (!STREAM || e1 >= 0)
-          seg_copy(en + OE1, col_at(xe0, e1 & kIdMask, col1), fl1, FS1);
+          seg_copy(en + OE1, col_at(xe0, e1 & IDM, col1), fl1, FS1);
         if (STREAM ? e2 >= 0 : k >= 3)
-          seg_copy(en + OE2, col_at(xe0, e2 & kIdMask, col1), fl1, FS1);
+          seg_copy(en + OE2, col_at(xe0, e2 & IDM, col1), fl1, FS1);
       }
       sr_commit();
       rv[slot] = v, re1[slot] = e1, re2[slot] = e2;
@@ -759,13 +799,20 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
     // one lane up; the chunk's top level by the last lane)
     auto flush = [&](double (&acc)[NV], double *yp, bool live, bool st) {
       const double below = __shfl_up_sync(FULL, acc[NV - 1], 1, W);
-      const int add = live && lane_ok ? 1 : 0;
-      const int put = add ? (st ? 2 : 1) : 0;
-      sr_put(yp, sl > 0 ? acc[0] + below : acc[0], bot_st ? put : add);
+      if constexpr (STREAM) { // store-first patch strips
+        const int add = live && lane_ok ? 1 : 0;
+        const int put = add ? (st ? 2 : 1) : 0;
+        sr_put(yp, sl > 0 ? acc[0] + below : acc[0], bot_st ? put : add);
 #pragma unroll
-      for (int v = 1; v < NV - 1; ++v) sr_put(yp + v, acc[v], put);
-      sr_put(yp + (NV - 1), acc[NV - 1],
-             sl != nl - 1 ? 0 : top_st ? put : add);
+        for (int v = 1; v < NV - 1; ++v) sr_put(yp + v, acc[v], put);
+        sr_put(yp + (NV - 1), acc[NV - 1],
+               sl != nl - 1 ? 0 : top_st ? put : add);
+      } else if (live && lane_ok) {
+        atomicAdd(yp, sl > 0 ? acc[0] + below : acc[0]);
+#pragma unroll
+        for (int v = 1; v < NV - 1; ++v) atomicAdd(yp + v, acc[v]);
+        if (sl == nl - 1) atomicAdd(yp + (NV - 1), acc[NV - 1]);
+      }
 #pragma unroll
       for (int v = 0; v < NV; ++v) acc[v] = 0.0;
     };
@@ -808,12 +855,12 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
         gm[A][1] = 0.5 * (g[1] + g[4]); // prism_abs_detj
         gm[A][2] = g[5] - g[2];
       }
-      yvc[A] = col_at(yv0, rv[A] & kIdMask, col0);
+      yvc[A] = col_at(yv0, rv[A] & IDM, col0);
       setb(A, act);
       setb(6 + A, store && (rv[A] & PM_STEP_STORE));
       if (FILL) {
         enter(ze[A], en + OE1);
-        yec[A] = col_at(ye0, re1[A] & kIdMask, col1);
+        yec[A] = col_at(ye0, re1[A] & IDM, col1);
         setb(3 + A, act);
         setb(9 + A, store && (re1[A] & PM_STEP_STORE));
       } else {
@@ -822,11 +869,11 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
         const bool l1 = act && (!STREAM || re1[A] >= 0);
         const bool l2 = act && (!STREAM || re2[A] >= 0);
         enter(ze[B1], l1 ? en + OE1 : sr_zero);
-        yec[B1] = col_at(ye0, re1[A] & kIdMask, col1);
+        yec[B1] = col_at(ye0, re1[A] & IDM, col1);
         setb(3 + B1, l1);
         setb(9 + B1, store && (re1[A] & PM_STEP_STORE));
         enter(ze[B2], l2 ? en + OE2 : sr_zero);
-        yec[B2] = col_at(ye0, re2[A] & kIdMask, col1);
+        yec[B2] = col_at(ye0, re2[A] & IDM, col1);
         setb(3 + B2, l2);
         setb(9 + B2, store && (re2[A] & PM_STEP_STORE));
       }
@@ -904,9 +951,25 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
 }
 
 template <class LY>
-static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
+static int strip_red_e_k1(const LoopArgs &a, const int32_t *strip_ptr,
+                          const int32_t *steps, const int32_t *steps_e,
+                          int64_t n_strips, int W, int64_t e_start);
+
+template <class LY>
+static int strip_red_e_k(const LoopArgs &a0, const int32_t *strip_ptr,
                          const int32_t *steps, const int32_t *steps_e,
-                         int64_t n_strips, int W, int64_t e_start) {
+                         int64_t n_strips, int chunk, int64_t e_start) {
+  LoopArgs a = a0;
+  a.lbeg = 0;
+  a.lend = a0.layers;
+  return strip_red_e_k1<LY>(a, strip_ptr, steps, steps_e, n_strips, chunk,
+                            e_start);
+}
+
+template <class LY>
+static int strip_red_e_k1(const LoopArgs &a, const int32_t *strip_ptr,
+                          const int32_t *steps, const int32_t *steps_e,
+                          int64_t n_strips, int W, int64_t e_start) {
   if (!a.mtri || !a.mline) {
     set_error("the strip kernel needs the Kronecker factors mtri/mline");
     return PM_EINVAL;
@@ -919,7 +982,7 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
   for (int i = 0; i < LY::NH * LY::NH; ++i) M.t[i] = a.mtri[i];
   for (int i = 0; i < LY::NV * LY::NV; ++i) M.l[i] = a.mline[i];
   const int segs = 32 / W;
-  const int64_t items = n_strips * ((a.layers + W - 1) / W);
+  const int64_t items = n_strips * ((a.lend - a.lbeg + W - 1) / W);
   const int64_t warps = (items + segs - 1) / segs;
   const bool sym = kron_sym6(M);
 #define PM_SRE(WW)                                                           \
@@ -948,7 +1011,7 @@ static int strip_red_e_k(const LoopArgs &a, const int32_t *strip_ptr,
         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
     k_strip_red_e<LY, WW, SS, ST><<<grid, T, smem, a.s>>>(                   \
         M, a.item_ptr, strip_ptr, steps, steps_e, n_strips, a.layers,        \
-        e_start, a.coords, a.x, a.y, a.store);                               \
+        a.lbeg, a.lend, e_start, a.coords, a.x, a.y, a.store);                               \
   } while (0)
   if (W == 32)
     PM_SRE(32);

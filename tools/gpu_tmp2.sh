@@ -1,6 +1,1 @@
-for c in C3 C5a; do
-  timeout 600 python tools/ab_sched.py $c stripred 2>&1 | grep -v Warn
-  for o in morton rcm; do for P in 32 64 128 256; do
-    echo "order $o P $P: $(PM_PATCH_ORDER=$o PM_PATCH_CELLS=$P timeout 600 python tools/ab_sched.py $c pstrip 2>&1 | grep -v Warn)"
-  done; done
-done
+timeout 1200 python -m pytest tests -m gpu -q -x -p no:cacheprovider -v 2>&1 | tail -40 > gpurun_out/pytest_crash.log
