@@ -122,11 +122,13 @@ __device__ __forceinline__ void sr_cp8z(double *dst, const double *src,
 }
 
 // Flush of a partial column element: mode 0 = nothing, 1 = add (REDG),
-// 2 = store (the first residency of a patch-interior entity, pm_build_patch_
-// strips); predicated, no branch
+// 3 = store (the first residency of a patch-interior entity, pm_build_patch_
+// strips).  Bit 0 = live, bit 1 = store, so `mode & mask` demotes a store
+// to an add (mask 1) or drops the element (mask 0).
+constexpr int kPutAdd = 1, kPutStore = 3;
 __device__ __forceinline__ void sr_put(double *p, double v, int mode) {
   asm volatile("{\n\t.reg .pred ps, pr;\n\t"
-               "setp.eq.s32 ps, %2, 2;\n\t"
+               "setp.eq.s32 ps, %2, 3;\n\t"
                "setp.eq.s32 pr, %2, 1;\n\t"
                "@ps st.global.f64 [%0], %1;\n\t"
                "@pr red.global.add.f64 [%0], %1;\n\t}" ::"l"(p),
@@ -237,13 +239,19 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
     for (int o = W; o < 32; o <<= 1)
       maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
     const int nl = has ? min(CW, lend - l0) : 0;
-    // store-first flushes: the chunk's bottom level is shared with the
-    // chunk below (its top), so lane 0 of an upper chunk always adds, and
-    // so does the top lane unless the chunk ends the column (the zero pass
-    // clears those levels)
-    const bool bot_st = L == 1 && (sl > 0 || l0 == 0);
-    const bool top_st = L == 1 && l0 + nl == layers;
     const int lb = L * sl; // the lane's first level in the chunk
+    // store-first flushes (STREAM): the chunk's bottom level is shared with
+    // the chunk below (its top), so lane 0 of an upper chunk always adds,
+    // and so does the top lane unless the chunk ends the column (the zero
+    // pass clears those levels).  Masks of the flush mode (sr_put): this
+    // lane's values, its bottom level copy, the chunk's top level copy.
+    const int mmask = lb < nl ? kPutStore : 0;
+    const int bmask = lb >= nl                        ? 0
+                      : (L == 1 && (sl > 0 || l0 == 0)) ? kPutStore
+                                                          : kPutAdd;
+    const int tmask = lb + L - 1 != nl - 1               ? 0
+                      : (L == 1 && l0 + nl == layers) ? kPutStore
+                                                       : kPutAdd;
     // source sizes of the lane's copies (8 inside the chunk, else 0)
     int fz[FR], cz[CR];
 #pragma unroll
@@ -376,17 +384,13 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
           if (sl > 0) v0 += below;
         }
         if constexpr (STREAM) { // store-first patch strips
-          const int add = live[A] ? 1 : 0;
-          const int put = live[A] ? (st[A] ? 2 : 1) : 0;
+          const int put = !live[A] ? 0 : st[A] ? kPutStore : kPutAdd;
 #pragma unroll
           for (int j = 0; j < L; ++j)
             sr_put(yc[A] + j * CH + c, j ? vb[j][c] : v0,
-                   lb + j >= nl                      ? 0
-                   : (j > 0 || c >= LV || bot_st) ? put
-                                                   : add);
+                   put & (j > 0 || c >= LV ? mmask : bmask));
           if (c < LV)
-            sr_put(yc[A] + L * CH + c, vt[c < LV ? c : 0],
-                   lb + L - 1 != nl - 1 ? 0 : top_st ? put : add);
+            sr_put(yc[A] + L * CH + c, vt[c < LV ? c : 0], put & tmask);
         } else {
 #pragma unroll
           for (int j = 0; j < L; ++j)
@@ -690,8 +694,11 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
                        sr_ring + (size_t)(kSreWarps * kSrDepth * SEGS + 1) * ES) +
                    ((threadIdx.x >> 5) * SEGS + (threadIdx.x & 31) / W) * 3 *
                        kSrIds;
-  for (int i = threadIdx.x; i < ES; i += blockDim.x)
-    sr_ring[(size_t)kSreWarps * kSrDepth * SEGS * ES + i] = 0.0;
+  // the zero block; in STREAM mode the whole ring (dead edge slots read
+  // stale ring entries, which must be finite)
+  for (int i = threadIdx.x; i < (STREAM ? kSreWarps * kSrDepth * SEGS + 1 : 1) * ES;
+       i += blockDim.x)
+    sr_ring[(size_t)(STREAM ? 0 : kSreWarps * kSrDepth * SEGS * ES) + i] = 0.0;
   __syncthreads();
 
   // items = (group, chunk) as in k_strip_red: a group is one global strip
@@ -717,9 +724,11 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
     const int nl = has ? min(W, lend - l0) : 0;
     // store-first: the chunk's bottom level copy is shared with the chunk
     // below, its top with the chunk above (both cleared by the zero pass)
-    const bool bot_st = sl > 0 || l0 == 0;
-    const bool top_st = l0 + nl == layers;
     const bool lane_ok = sl < nl;
+    // flush-mode masks (sr_put): mid values, bottom and top level copies
+    const int mmask = lane_ok ? kPutStore : 0;
+    const int bmask = !lane_ok ? 0 : (sl > 0 || l0 == 0) ? kPutStore : kPutAdd;
+    const int tmask = sl != nl - 1 ? 0 : l0 + nl == layers ? kPutStore : kPutAdd;
     const int fl0 = nl * CH0 + LV0, fl1 = nl * CH1 + LV1, cl = 3 * (nl + 1);
     // the segment's chunk of every column (copies) and the lane's element
     // (flushes)
@@ -734,11 +743,11 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
     // accumulators per entity and interval function
     double zv[3][NV], ze[3][NV], gm[3][3], av[3][NV], ae[3][NV];
     double *yvc[3] = {yv0, yv0, yv0}, *yec[3] = {ye0, ye0, ye0};
-    // per window slot a: bit a vertex live, 3+a edge live, 6+a vertex
-    // store-first, 9+a edge store-first (one register)
-    unsigned wf = 0;
-    auto setb = [&](int b, bool on) { wf = on ? (wf | (1u << b)) : (wf & ~(1u << b)); };
-    auto getb = [&](int b) { return ((wf >> b) & 1u) != 0; };
+    // flush mode per window slot (sr_put: 0 empty, 1 add, 3 store first)
+    int vm[3] = {0, 0, 0}, em[3] = {0, 0, 0};
+    auto mode = [&](bool live, int id) {
+      return !live ? 0 : (store && (id & PM_STEP_STORE)) ? kPutStore : kPutAdd;
+    };
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
 #pragma unroll
@@ -797,17 +806,14 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
     // flush an entity residency: accumulators back to the layer block
     // (bottom copy v = 0, connecting v = 1..NV-2, top copy v = NV-1 added
     // one lane up; the chunk's top level by the last lane)
-    auto flush = [&](double (&acc)[NV], double *yp, bool live, bool st) {
+    auto flush = [&](double (&acc)[NV], double *yp, int m) {
       const double below = __shfl_up_sync(FULL, acc[NV - 1], 1, W);
       if constexpr (STREAM) { // store-first patch strips
-        const int add = live && lane_ok ? 1 : 0;
-        const int put = add ? (st ? 2 : 1) : 0;
-        sr_put(yp, sl > 0 ? acc[0] + below : acc[0], bot_st ? put : add);
+        sr_put(yp, sl > 0 ? acc[0] + below : acc[0], m & bmask);
 #pragma unroll
-        for (int v = 1; v < NV - 1; ++v) sr_put(yp + v, acc[v], put);
-        sr_put(yp + (NV - 1), acc[NV - 1],
-               sl != nl - 1 ? 0 : top_st ? put : add);
-      } else if (live && lane_ok) {
+        for (int v = 1; v < NV - 1; ++v) sr_put(yp + v, acc[v], m & mmask);
+        sr_put(yp + (NV - 1), acc[NV - 1], m & tmask);
+      } else if (m && lane_ok) {
         atomicAdd(yp, sl > 0 ? acc[0] + below : acc[0]);
 #pragma unroll
         for (int v = 1; v < NV - 1; ++v) atomicAdd(yp + v, acc[v]);
@@ -836,12 +842,12 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
       constexpr int A = decltype(A_)::value;
       constexpr bool FILL = decltype(FILL_)::value;
       constexpr int B1 = (A + 1) % 3, B2 = (A + 2) % 3;
-      flush(av[A], yvc[A], getb(A), getb(6 + A));
+      flush(av[A], yvc[A], vm[A]);
       if (FILL) {
-        flush(ae[A], yec[A], getb(3 + A), getb(9 + A));
+        flush(ae[A], yec[A], em[A]);
       } else {
-        flush(ae[B1], yec[B1], getb(3 + B1), getb(9 + B1));
-        flush(ae[B2], yec[B2], getb(3 + B2), getb(9 + B2));
+        flush(ae[B1], yec[B1], em[B1]);
+        flush(ae[B2], yec[B2], em[B2]);
       }
       const bool act = k < len;
       sr_wait<kSrDepth - 1>();
@@ -856,26 +862,21 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
         gm[A][2] = g[5] - g[2];
       }
       yvc[A] = col_at(yv0, rv[A] & IDM, col0);
-      setb(A, act);
-      setb(6 + A, store && (rv[A] & PM_STEP_STORE));
+      vm[A] = mode(act, rv[A]);
       if (FILL) {
         enter(ze[A], en + OE1);
         yec[A] = col_at(ye0, re1[A] & IDM, col1);
-        setb(3 + A, act);
-        setb(9 + A, store && (re1[A] & PM_STEP_STORE));
+        em[A] = mode(act, re1[A]);
       } else {
-        // STREAM: an edge id -1 (fill steps) leaves the slot dead: zero
-        // block in, nothing flushed
-        const bool l1 = act && (!STREAM || re1[A] >= 0);
-        const bool l2 = act && (!STREAM || re2[A] >= 0);
-        enter(ze[B1], l1 ? en + OE1 : sr_zero);
+        // STREAM: an edge id -1 (fill steps) leaves the slot dead: nothing
+        // flushed; its stale ring values (finite: the ring starts zeroed)
+        // only meet NOCELL steps (det = 0)
+        enter(ze[B1], en + OE1);
         yec[B1] = col_at(ye0, re1[A] & IDM, col1);
-        setb(3 + B1, l1);
-        setb(9 + B1, store && (re1[A] & PM_STEP_STORE));
-        enter(ze[B2], l2 ? en + OE2 : sr_zero);
+        em[B1] = mode(act && (!STREAM || re1[A] >= 0), re1[A]);
+        enter(ze[B2], en + OE2);
         yec[B2] = col_at(ye0, re2[A] & IDM, col1);
-        setb(3 + B2, l2);
-        setb(9 + B2, store && (re2[A] & PM_STEP_STORE));
+        em[B2] = mode(act && (!STREAM || re2[A] >= 0), re2[A]);
       }
       const int rv_cell = rv[A]; // before the slot is refilled
       __syncwarp();
@@ -943,8 +944,8 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      flush(av[a], yvc[a], getb(a), getb(6 + a));
-      flush(ae[a], yec[a], getb(3 + a), getb(9 + a));
+      flush(av[a], yvc[a], vm[a]);
+      flush(ae[a], yec[a], em[a]);
     }
     sr_wait<0>(); // no copy in flight into the ring across items
   }

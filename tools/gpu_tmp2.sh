@@ -1,1 +1,5 @@
-timeout 1200 python -m pytest tests -m gpu -q -x -p no:cacheprovider -v 2>&1 | tail -40 > gpurun_out/pytest_crash.log
+timeout 900 python -m pytest tests -m gpu -q -x -k "patch_strips or pstrip" 2>&1 | tail -2
+for c in C3 C5b C5a C4-CG1xCG1-rcm-L50; do
+  timeout 600 python tools/ab_sched.py $c stripred pstrip 2>&1 | grep -v Warn
+  for P in 64 128 512; do echo "P=$P $(PM_PATCH_CELLS=$P timeout 600 python tools/ab_sched.py $c pstrip 2>&1 | grep -v Warn)"; done
+done
