@@ -21,9 +21,12 @@ ncu --set full --clock-control none --import-source on -k regex:k_dg_stream -s 4
     -o gpurun_out/prof_C2_stream -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_c2.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_strip_red_e -s 1 -c 1 \
     -o gpurun_out/prof_C3_stripred_e -f python bench.py --config C3 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_c3.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_strip_red -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k k_strip_red -s 1 -c 1 \
     -o gpurun_out/prof_C5a_stripred -f python bench.py --config C5a --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_c5a.log 2>&1
 for r in gpurun_out/prof_C2_stream gpurun_out/prof_C3_stripred_e gpurun_out/prof_C5a_stripred; do
   python tools/ncu_summary.py $r.ncu-rep > $r.txt 2>&1
 done
 tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log | tail -2; cat gpurun_out/all.txt | head -60
+ncu --set full --clock-control none --import-source on -k k_strip_red -s 1 -c 1 \
+    -o gpurun_out/prof_C5b_stripred -f python bench.py --config C5b --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_c5b.log 2>&1
+python tools/ncu_summary.py gpurun_out/prof_C5b_stripred.ncu-rep > gpurun_out/prof_C5b_stripred.txt 2>&1
