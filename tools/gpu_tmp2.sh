@@ -1,6 +1,7 @@
-for c in C5a C5b; do
-ncu --set full --clock-control none --import-source on -k k_strip_red -s 1 -c 1 \
-    -o gpurun_out/prof_${c}_stripred -f python bench.py --config $c --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_$c.log 2>&1
-python tools/ncu_summary.py gpurun_out/prof_${c}_stripred.ncu-rep > gpurun_out/prof_${c}_stripred.txt 2>&1
+PM_DG_RING=1 timeout 900 python -m pytest tests -m gpu -q -x -k "DG or dg or stream or smoke" 2>&1 | tail -2
+for r in 0 1 2 3 4; do
+  echo "ring $r: $(PM_DG_RING=$r timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["roofline"]["kernel_ms"], d["value"], d["roofline"]["frac"])')"
 done
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_strip_red -s 1 -c 1 python bench.py --config C3 --steps 2 --warmup 1 --no-cpu-baseline 2>&1 | grep -E "__" > gpurun_out/traffic_C3.txt
+for c in C4-DG1xDG1-rcm-L20 C4-DG1xDG1-rcm-L256 C4-DG1xDG1-random-L100; do for r in 0 1; do
+  echo "$c ring $r: $(PM_DG_RING=$r timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["roofline"]["kernel_ms"], d["value"], d["roofline"]["frac"])')"
+done; done
