@@ -250,3 +250,27 @@ def test_patch_strips_plan(n, ordering, patch):
     assert sorted(cells_seen) == list(range(nc))
     # every entity of some cell is zeroed or stored exactly once
     assert stored | zero == set(owners)
+
+
+def test_integration_patch_strips_snippet():
+    """INTEGRATION.md's ctypes binding of pm_build_patch_strips, executed
+    verbatim (host planner: no GPU), equals the package's wrapper."""
+    import ctypes
+    import re
+    from paper_1604_05937_b200 import _lib
+    from paper_1604_05937_b200.configs import base_mesh
+    from paper_1604_05937_b200.schedule import morton_order
+    text = open("INTEGRATION.md").read()
+    code = next(b for b in re.findall(r"```python\n(.*?)```", text, re.S)
+                if "def patch_strips" in b)
+    lib = _lib.host_lib()
+    ns = {"ctypes": ctypes, "np": np, "lib": lib,
+          "i32p": ctypes.POINTER(ctypes.c_int32)}
+    exec(code, ns)                                  # noqa: S102
+    base, _ = base_mesh(9, "rcm", 0.1)
+    cv = np.asarray(base.cell_vertices)
+    order = morton_order(np.asarray(base.coords)[cv].mean(axis=1))
+    ptr = np.unique(np.append(np.arange(0, cv.shape[0], 16), cv.shape[0]))
+    got = ns["patch_strips"](base, order, ptr, edges=True)
+    want = _lib.build_patch_strips(base, order, ptr, edges=True)
+    assert all(np.array_equal(a, b) for a, b in zip(got, want))
