@@ -530,10 +530,15 @@ def patch_strip_size(n_cells: int, layers: int) -> int:
 
 
 def strip_max_len(n_cells: int, layers: int) -> int:
-    """Strip length cap: long strips amortise the 3-vertex fill, but small
-    meshes need enough (strip, chunk) items to fill 148 SMs."""
+    """Strip length cap: long strips amortise the 3-vertex fill, the final
+    flushes and the per-strip setup, but small meshes need enough (strip,
+    chunk) items to fill 148 SMs.  Measured (profiles/README.md): cap 512
+    vs 32 takes C5a 3.78 -> 3.35 ms, C5b 9.41 -> 8.66, C3 1.66 -> 1.60;
+    4096 is slower again (too few items).  PM_STRIP_MAXLEN overrides."""
+    import os
+    cap = int(os.environ.get("PM_STRIP_MAXLEN", "512"))
     chunks = -(-layers // strip_chunk_width(layers))
-    return int(max(4, min(32, n_cells * chunks // 12000)))
+    return int(max(4, min(cap, n_cells * chunks // 12000)))
 
 
 _COLORINGS = {}

@@ -1,7 +1,3 @@
-PM_DG_RING=1 timeout 900 python -m pytest tests -m gpu -q -x -k "DG or dg or stream or smoke" 2>&1 | tail -2
-for r in 0 1 2 3 4; do
-  echo "ring $r: $(PM_DG_RING=$r timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["roofline"]["kernel_ms"], d["value"], d["roofline"]["frac"])')"
+for c in C3 C5a C5b; do
+  for m in 128 256 512 4096; do echo "maxlen $m $(PM_STRIP_MAXLEN=$m timeout 600 python tools/ab_sched.py $c stripred 2>&1 | grep -v Warn)"; done
 done
-for c in C4-DG1xDG1-rcm-L20 C4-DG1xDG1-rcm-L256 C4-DG1xDG1-random-L100; do for r in 0 1; do
-  echo "$c ring $r: $(PM_DG_RING=$r timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["roofline"]["kernel_ms"], d["value"], d["roofline"]["frac"])')"
-done; done
