@@ -53,7 +53,9 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
         objs.append(obj)
         if not _stale(obj, [src] + headers):
             continue
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        # PM_NVCC_EXTRA: extra -D tuning flags (experiments, e.g. -DPM_SR_DEPTH=6)
+        cmd = [NVCC, *ARCH, *FLAGS, *os.environ.get("PM_NVCC_EXTRA", "").split(),
+               "-c", src, "-o", obj]
         if ptxas_verbose and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
         if src.endswith(".cpp"):

@@ -59,7 +59,13 @@ template <class LY, int W> constexpr int srb_fpart() {
 template <class LY, int W> constexpr int srb_entry() {
   return srb_fpart<LY, W>() + ((3 * (W + 1) + 3) / 2) * 2;
 }
-constexpr int kSrDepth = 3; // steps in flight per segment
+// steps in flight per segment: 3 (ring slot = window slot) or 6 (ring slot
+// k % 6, window slot k % 3; compile-time PM_SR_DEPTH)
+#ifndef PM_SR_DEPTH
+#define PM_SR_DEPTH 3
+#endif
+constexpr int kSrDepth = PM_SR_DEPTH;
+static_assert(kSrDepth == 3 || kSrDepth == 6, "ring depth 3 or 6");
 
 // 3-vector windows need more registers: one CTA per SM there
 template <class LY> constexpr int sr_min_blocks() {
@@ -415,8 +421,9 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
 
     // one strip step into window slot A; FILL: the first three steps (the
     // window fills, nothing to flush, no cell before the third vertex)
-    auto step = [&](auto A_, auto FILL_, int k) {
-      constexpr int A = decltype(A_)::value;
+    auto step = [&](auto A_, auto R_, auto FILL_, int k) {
+      constexpr int A = decltype(A_)::value; // window slot (k % 3)
+      constexpr int R = decltype(R_)::value; // ring slot (k % kSrDepth)
       constexpr bool FILL = decltype(FILL_)::value;
       if (!FILL) flush(A_);
       const bool act = k < len;
@@ -426,9 +433,9 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
       // steps past this segment's strip read a zero block instead of the
       // (stale, possibly non-finite) ring slot; lanes past the chunk read
       // zero-filled values and are never flushed.
-      const double *e = act ? entry(A) : sr_zero;
+      const double *e = act ? entry(R) : sr_zero;
 #if PM_SR16
-      const int sh = act ? rsh[A] : 0;
+      const int sh = act ? rsh[R] : 0;
       const double *ef = e + (sh & 1), *ec = e + FP + (sh >> 1);
 #else
       const double *ef = e, *ec = e + FP;
@@ -449,11 +456,11 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         gm[A][j][2] = g[j + 1][2] - g[j][2];
       }
       __syncwarp(); // reads done before the slot is refilled
-      const int va = rv[A] & IDM;
-      const int rv_cell = rv[A]; // before the slot is refilled
+      const int va = rv[R] & IDM;
+      const int rv_cell = rv[R]; // before the slot is refilled
       yc[A] = col_at(PEER && va < ghost_end ? ylg : yl, va, colb);
       live[A] = act;
-      st[A] = L == 1 && store && (rv[A] & PM_STEP_STORE);
+      st[A] = L == 1 && store && (rv[R] & PM_STEP_STORE);
       // interval stage of the entering vertex
 #pragma unroll
       for (int j = 0; j < L; ++j)
@@ -472,7 +479,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
             zv[A][j][c][v] = s;
           }
       // refill ring slot A with the step kSrDepth ahead
-      rv[A] = fetch(k + kSrDepth, A);
+      rv[R] = fetch(k + kSrDepth, R);
       if (FILL && A < 2) return; // window not full yet
 #pragma unroll
       for (int j = 0; j < L; ++j) {
@@ -523,17 +530,40 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
     using S2 = std::integral_constant<int, 2>;
     using TF = std::true_type;
     using FF = std::false_type;
+    using S3 = std::integral_constant<int, 3>;
+    using S4 = std::integral_constant<int, 4>;
+    using S5 = std::integral_constant<int, 5>;
     int kb = 0;
     if constexpr (!STREAM) {
-      step(S0{}, TF{}, 0);
-      step(S1{}, TF{}, 1);
-      step(S2{}, TF{}, 2);
+      step(S0{}, S0{}, TF{}, 0);
+      step(S1{}, S1{}, TF{}, 1);
+      step(S2{}, S2{}, TF{}, 2);
       kb = 3;
     }
-    for (int k = kb; k < maxlen; k += 3) {
-      step(S0{}, FF{}, k);
-      step(S1{}, FF{}, k + 1);
-      step(S2{}, FF{}, k + 2);
+    if constexpr (kSrDepth == 3) {
+      for (int k = kb; k < maxlen; k += 3) {
+        step(S0{}, S0{}, FF{}, k);
+        step(S1{}, S1{}, FF{}, k + 1);
+        step(S2{}, S2{}, FF{}, k + 2);
+      }
+    } else if constexpr (!STREAM) { // ring slots 3,4,5,0,1,2 from k = 3
+      for (int k = kb; k < maxlen; k += 6) {
+        step(S0{}, S3{}, FF{}, k);
+        step(S1{}, S4{}, FF{}, k + 1);
+        step(S2{}, S5{}, FF{}, k + 2);
+        step(S0{}, S0{}, FF{}, k + 3);
+        step(S1{}, S1{}, FF{}, k + 4);
+        step(S2{}, S2{}, FF{}, k + 5);
+      }
+    } else {
+      for (int k = kb; k < maxlen; k += 6) {
+        step(S0{}, S0{}, FF{}, k);
+        step(S1{}, S1{}, FF{}, k + 1);
+        step(S2{}, S2{}, FF{}, k + 2);
+        step(S0{}, S3{}, FF{}, k + 3);
+        step(S1{}, S4{}, FF{}, k + 4);
+        step(S2{}, S5{}, FF{}, k + 5);
+      }
     }
     flush(S0{});
     flush(S1{});
@@ -541,6 +571,14 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
     sr_wait<0>(); // no copy in flight into the ring across items
   }
   if constexpr (PEER) __threadfence_system(); // peer REDs land before exit
+}
+
+// CTAs per SM in the strip kernels' grid-stride grid (PM_STRIP_GRID tuning
+// knob; default `def`)
+static int strip_grid_cap(int def) {
+  const char *e = getenv("PM_STRIP_GRID");
+  const int v = e ? atoi(e) : 0;
+  return v > 0 ? v : def;
 }
 
 // levels per lane (PM_STRIP_L tuning knob: 1 or 2)
@@ -559,7 +597,7 @@ static int strip_red_launch(const LoopArgs &a, const KronMat &M,
       n_strips * ((a.lend - a.lbeg + W * L - 1) / (W * L));
   const int64_t warps = (items + segs - 1) / segs;
   constexpr int T = sr_threads<LY>();
-  const unsigned grid = grid_for(warps * 32, T, 8);
+  const unsigned grid = grid_for(warps * 32, T, strip_grid_cap(8));
   const size_t smem = sr_smem<LY, W, L>();
   PM_CUDA_TRY(cudaFuncSetAttribute(k_strip_red<LY, W, SYM, L, PEER, STREAM>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -838,8 +876,9 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
     };
     // one strip step into vertex slot A; FILL: edge slot A, else the edge
     // slots A+1, A+2
-    auto step = [&](auto A_, auto FILL_, int k) {
-      constexpr int A = decltype(A_)::value;
+    auto step = [&](auto A_, auto R_, auto FILL_, int k) {
+      constexpr int A = decltype(A_)::value; // window slot (k % 3)
+      constexpr int R = decltype(R_)::value; // ring slot (k % kSrDepth)
       constexpr bool FILL = decltype(FILL_)::value;
       constexpr int B1 = (A + 1) % 3, B2 = (A + 2) % 3;
       flush(av[A], yvc[A], vm[A]);
@@ -853,7 +892,7 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
       sr_wait<kSrDepth - 1>();
       __syncwarp();
       // past the strip's end: read the zero block (contribution exactly 0)
-      const double *en = act ? entry(A) : sr_zero;
+      const double *en = act ? entry(R) : sr_zero;
       enter(zv[A], en);
       {
         const double *g = en + OC + 3 * sl;
@@ -861,26 +900,26 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
         gm[A][1] = 0.5 * (g[1] + g[4]); // prism_abs_detj
         gm[A][2] = g[5] - g[2];
       }
-      yvc[A] = col_at(yv0, rv[A] & IDM, col0);
-      vm[A] = mode(act, rv[A]);
+      yvc[A] = col_at(yv0, rv[R] & IDM, col0);
+      vm[A] = mode(act, rv[R]);
       if (FILL) {
         enter(ze[A], en + OE1);
-        yec[A] = col_at(ye0, re1[A] & IDM, col1);
-        em[A] = mode(act, re1[A]);
+        yec[A] = col_at(ye0, re1[R] & IDM, col1);
+        em[A] = mode(act, re1[R]);
       } else {
         // STREAM: an edge id -1 (fill steps) leaves the slot dead: nothing
         // flushed; its stale ring values (finite: the ring starts zeroed)
         // only meet NOCELL steps (det = 0)
         enter(ze[B1], en + OE1);
-        yec[B1] = col_at(ye0, re1[A] & IDM, col1);
-        em[B1] = mode(act && (!STREAM || re1[A] >= 0), re1[A]);
+        yec[B1] = col_at(ye0, re1[R] & IDM, col1);
+        em[B1] = mode(act && (!STREAM || re1[R] >= 0), re1[R]);
         enter(ze[B2], en + OE2);
-        yec[B2] = col_at(ye0, re2[A] & IDM, col1);
-        em[B2] = mode(act && (!STREAM || re2[A] >= 0), re2[A]);
+        yec[B2] = col_at(ye0, re2[R] & IDM, col1);
+        em[B2] = mode(act && (!STREAM || re2[R] >= 0), re2[R]);
       }
-      const int rv_cell = rv[A]; // before the slot is refilled
+      const int rv_cell = rv[R]; // before the slot is refilled
       __syncwarp();
-      fetch(k + kSrDepth, A);
+      fetch(k + kSrDepth, R);
       if (FILL && A < 2) return; // window not full yet
       // lanes past the chunk are never flushed; past the strip's end the
       // window still holds live entities: no contribution
@@ -930,17 +969,40 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
     using S2 = std::integral_constant<int, 2>;
     using TF = std::true_type;
     using FF = std::false_type;
+    using S3 = std::integral_constant<int, 3>;
+    using S4 = std::integral_constant<int, 4>;
+    using S5 = std::integral_constant<int, 5>;
     int kb = 0;
     if constexpr (!STREAM) {
-      step(S0{}, TF{}, 0);
-      step(S1{}, TF{}, 1);
-      step(S2{}, TF{}, 2);
+      step(S0{}, S0{}, TF{}, 0);
+      step(S1{}, S1{}, TF{}, 1);
+      step(S2{}, S2{}, TF{}, 2);
       kb = 3;
     }
-    for (int k = kb; k < maxlen; k += 3) {
-      step(S0{}, FF{}, k);
-      step(S1{}, FF{}, k + 1);
-      step(S2{}, FF{}, k + 2);
+    if constexpr (kSrDepth == 3) {
+      for (int k = kb; k < maxlen; k += 3) {
+        step(S0{}, S0{}, FF{}, k);
+        step(S1{}, S1{}, FF{}, k + 1);
+        step(S2{}, S2{}, FF{}, k + 2);
+      }
+    } else if constexpr (!STREAM) { // ring slots 3,4,5,0,1,2 from k = 3
+      for (int k = kb; k < maxlen; k += 6) {
+        step(S0{}, S3{}, FF{}, k);
+        step(S1{}, S4{}, FF{}, k + 1);
+        step(S2{}, S5{}, FF{}, k + 2);
+        step(S0{}, S0{}, FF{}, k + 3);
+        step(S1{}, S1{}, FF{}, k + 4);
+        step(S2{}, S2{}, FF{}, k + 5);
+      }
+    } else {
+      for (int k = kb; k < maxlen; k += 6) {
+        step(S0{}, S0{}, FF{}, k);
+        step(S1{}, S1{}, FF{}, k + 1);
+        step(S2{}, S2{}, FF{}, k + 2);
+        step(S0{}, S3{}, FF{}, k + 3);
+        step(S1{}, S4{}, FF{}, k + 4);
+        step(S2{}, S5{}, FF{}, k + 5);
+      }
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -1003,7 +1065,7 @@ static int strip_red_e_k1(const LoopArgs &a, const int32_t *strip_ptr,
 #define PM_SRE3(WW, SS, ST)                                                  \
   do {                                                                       \
     constexpr int T = sre_threads<SS>(), NW = T / 32;                        \
-    const unsigned grid = grid_for(warps * 32, T, 4);                        \
+    const unsigned grid = grid_for(warps * 32, T, strip_grid_cap(4));        \
     const size_t smem = sizeof(double) * (NW * kSrDepth * (32 / WW) + 1) *   \
                             sre_entry<LY, WW>() +                            \
                         sizeof(int) * NW * (32 / WW) * 3 * kSrIds;           \
