@@ -511,10 +511,13 @@ def strip_chunk_width(layers: int) -> int:
     forced = int(os.environ.get("PM_STRIP_W", "0"))
     if forced in (8, 16, 32):
         return forced
-    # per-chunk charge 0.1 (measured: at λ = 100 W = 32 beats W = 16 on P1
-    # and P2 despite 28 % idle lanes, profiles/README.md)
-    return min((8, 16, 32), key=lambda w: (-(-layers // w) * w / layers
-                                           + 0.1 * (-(-layers // w)), -w))
+    # lane slots (chunks x W) weighted by a per-slot cost that grows as the
+    # segments narrow (more lines touched per warp instruction): fitted to
+    # the config-4 P1 sweep over W in {8, 16, 32} and λ in {1 .. 256}
+    # (e.g. λ = 256: 0.458 / 0.272 / 0.249 ms) and C3 (P2, λ = 100: W = 32
+    # 5 % faster than 16), profiles/README.md
+    cost = {8: 1.6, 16: 1.15, 32: 1.0}
+    return min((8, 16, 32), key=lambda w: (-(-layers // w) * w * cost[w], -w))
 
 
 def patch_strip_size(n_cells: int, layers: int) -> int:
