@@ -104,11 +104,23 @@ constexpr int kSrIds = 64; // strip vertex ids staged per segment
 template <class LY> constexpr int sr_threads() {
   return LY::CH0 > 2 ? PM_SR_VTHREADS : 256;
 }
+// Multi-channel layouts (3-vector P1: CH = 3) flush through a per-segment
+// staging row of the chunk's (W + 1) * CH values, so the REDs run over
+// consecutive addresses (lane-contiguous) instead of at a CH * 8-byte
+// stride: a third of the L2 reduction sector operations
+#ifndef PM_SR_TROW
+#define PM_SR_TROW 1
+#endif
+template <class LY, int W, int L> constexpr int sr_trow() {
+  return (PM_SR_TROW && L == 1 && LY::CH0 > 1) ? (W + 1) * LY::CH0 : 0;
+}
 template <class LY, int W, int L> constexpr size_t sr_smem() {
   return sizeof(double) *
              ((size_t)(sr_threads<LY>() / 32) * kSrDepth * (32 / W) + 1) *
              sr_pentry<LY, W, L>() +
-         sizeof(int) * (sr_threads<LY>() / 32) * (32 / W) * kSrIds;
+         sizeof(int) * (sr_threads<LY>() / 32) * (32 / W) * kSrIds +
+         sizeof(double) * (sr_threads<LY>() / 32) * (32 / W) *
+             sr_trow<LY, W, L>();
 }
 
 __device__ __forceinline__ void sr_cp16z(double *dst, const double *src,
@@ -215,6 +227,12 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
   int *const sid = reinterpret_cast<int *>(sr_ring + (size_t)(NWARP * kSrDepth *
                                                               SEGS + 1) * ES) +
                    ((threadIdx.x >> 5) * SEGS + seg) * kSrIds;
+  constexpr int TR = STREAM ? 0 : sr_trow<LY, W, L>();
+  double *const trow =
+      reinterpret_cast<double *>(reinterpret_cast<int *>(
+          sr_ring + (size_t)(NWARP * kSrDepth * SEGS + 1) * ES) +
+                                 NWARP * SEGS * kSrIds) +
+      ((threadIdx.x >> 5) * SEGS + seg) * TR;
   for (int i = threadIdx.x; i < ES; i += blockDim.x)
     sr_ring[(size_t)NWARP * kSrDepth * SEGS * ES + i] = 0.0;
   __syncthreads();
@@ -397,6 +415,11 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
                    put & (j > 0 || c >= LV ? mmask : bmask));
           if (c < LV)
             sr_put(yc[A] + L * CH + c, vt[c < LV ? c : 0], put & tmask);
+        } else if constexpr (TR > 0) { // staged, added below
+          // (lanes past the chunk stay out: their slot is the chunk top)
+          if (sl < nl) trow[sl * CH + c] = v0;
+          if (c < LV && sl == nl - 1)
+            trow[(sl + 1) * CH + c] = vt[c < LV ? c : 0];
         } else {
 #pragma unroll
           for (int j = 0; j < L; ++j)
@@ -416,6 +439,17 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
                 atomicAdd(yc[A] + (j + 1) * CH + c, vb[j + 1][c]);
           }
         }
+      }
+      if constexpr (TR > 0) { // the staged chunk, lane-contiguous REDs
+        __syncwarp();
+        double *const base = yc[A] - sl * CH; // the chunk's first value
+        const int n = nl * CH + LV;
+#pragma unroll
+        for (int r = 0; r < (TR + W - 1) / W; ++r) {
+          const int i = sl + W * r;
+          sr_red(base + i, trow[i < TR ? i : 0], live[A] && i < n);
+        }
+        __syncwarp(); // row reads done before the next flush stages
       }
     };
 
@@ -684,6 +718,9 @@ static int strip_red_k1(const LoopArgs &a, const int32_t *strip_ptr,
 // ---------------------------------------------------------------------------
 template <class LY, int W> constexpr int sre_fs0() { return W * LY::CH0 + LY::LV0; }
 template <class LY, int W> constexpr int sre_fs1() { return W * LY::CH1 + LY::LV1; }
+template <class LY, int W> constexpr int sre_trow() {
+  return PM_SR_TROW ? (W + 1) * (LY::NV - 1) : 0;
+}
 template <class LY, int W> constexpr int sre_entry() {
   return sre_fs0<LY, W>() + 3 * (W + 1) + 2 * sre_fs1<LY, W>();
 }
@@ -732,6 +769,16 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
                        sr_ring + (size_t)(kSreWarps * kSrDepth * SEGS + 1) * ES) +
                    ((threadIdx.x >> 5) * SEGS + (threadIdx.x & 31) / W) * 3 *
                        kSrIds;
+  // flush staging row (see sr_trow): the entity chunk's (W + 1) * (NV - 1)
+  // values, added with lane-contiguous REDs (level copies and mid values
+  // alternate in the column: per-lane REDs run at a 16-byte stride)
+  constexpr int TR = STREAM ? 0 : sre_trow<LY, W>();
+  double *const trow =
+      reinterpret_cast<double *>(
+          reinterpret_cast<int *>(sr_ring + (size_t)(kSreWarps * kSrDepth *
+                                                         SEGS + 1) * ES) +
+          kSreWarps * SEGS * 3 * kSrIds) +
+      ((threadIdx.x >> 5) * SEGS + (threadIdx.x & 31) / W) * TR;
   // the zero block; in STREAM mode the whole ring (dead edge slots read
   // stale ring entries, which must be finite)
   for (int i = threadIdx.x; i < (STREAM ? kSreWarps * kSrDepth * SEGS + 1 : 1) * ES;
@@ -851,6 +898,23 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
 #pragma unroll
         for (int v = 1; v < NV - 1; ++v) sr_put(yp + v, acc[v], m & mmask);
         sr_put(yp + (NV - 1), acc[NV - 1], m & tmask);
+      } else if constexpr (TR > 0) {
+        // (lanes past the chunk stay out: their first slot is the top)
+        if (lane_ok) {
+          trow[sl * (NV - 1)] = sl > 0 ? acc[0] + below : acc[0];
+#pragma unroll
+          for (int v = 1; v < NV - 1; ++v) trow[sl * (NV - 1) + v] = acc[v];
+        }
+        if (sl == nl - 1) trow[(sl + 1) * (NV - 1)] = acc[NV - 1];
+        __syncwarp();
+        double *const base = yp - sl * (NV - 1); // the chunk's first value
+        const int n = nl * (NV - 1) + 1;
+#pragma unroll
+        for (int r = 0; r < (TR + W - 1) / W; ++r) {
+          const int i = sl + W * r;
+          sr_red(base + i, trow[i < TR ? i : 0], m && i < n);
+        }
+        __syncwarp(); // row reads done before the next flush stages
       } else if (m && lane_ok) {
         atomicAdd(yp, sl > 0 ? acc[0] + below : acc[0]);
 #pragma unroll
@@ -1068,7 +1132,8 @@ static int strip_red_e_k1(const LoopArgs &a, const int32_t *strip_ptr,
     const unsigned grid = grid_for(warps * 32, T, strip_grid_cap(4));        \
     const size_t smem = sizeof(double) * (NW * kSrDepth * (32 / WW) + 1) *   \
                             sre_entry<LY, WW>() +                            \
-                        sizeof(int) * NW * (32 / WW) * 3 * kSrIds;           \
+                        sizeof(int) * NW * (32 / WW) * 3 * kSrIds +          \
+                        sizeof(double) * NW * (32 / WW) * sre_trow<LY, WW>(); \
     PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
         k_strip_red_e<LY, WW, SS, ST>,                                       \
         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
