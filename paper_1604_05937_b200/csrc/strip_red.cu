@@ -227,7 +227,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
   int *const sid = reinterpret_cast<int *>(sr_ring + (size_t)(NWARP * kSrDepth *
                                                               SEGS + 1) * ES) +
                    ((threadIdx.x >> 5) * SEGS + seg) * kSrIds;
-  constexpr int TR = STREAM ? 0 : sr_trow<LY, W, L>();
+  constexpr int TR = sr_trow<LY, W, L>();
   double *const trow =
       reinterpret_cast<double *>(reinterpret_cast<int *>(
           sr_ring + (size_t)(NWARP * kSrDepth * SEGS + 1) * ES) +
@@ -407,7 +407,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
           const double below = __shfl_up_sync(FULL, vt[c < LV ? c : 0], 1, W);
           if (sl > 0) v0 += below;
         }
-        if constexpr (STREAM) { // store-first patch strips
+        if constexpr (STREAM && TR == 0) { // store-first patch strips
           const int put = !live[A] ? 0 : st[A] ? kPutStore : kPutAdd;
 #pragma unroll
           for (int j = 0; j < L; ++j)
@@ -415,7 +415,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
                    put & (j > 0 || c >= LV ? mmask : bmask));
           if (c < LV)
             sr_put(yc[A] + L * CH + c, vt[c < LV ? c : 0], put & tmask);
-        } else if constexpr (TR > 0) { // staged, added below
+        } else if constexpr (TR > 0) { // staged, added / stored below
           // (lanes past the chunk stay out: their slot is the chunk top)
           if (sl < nl) trow[sl * CH + c] = v0;
           if (c < LV && sl == nl - 1)
@@ -444,10 +444,23 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         __syncwarp();
         double *const base = yc[A] - sl * CH; // the chunk's first value
         const int n = nl * CH + LV;
+        if constexpr (STREAM) {
+          // store-first: the chunk's bottom / top level copies are shared
+          // with the chunks below / above (zeroed, always added)
+          const int put = !live[A] ? 0 : st[A] ? kPutStore : kPutAdd;
+          const int lo = l0 > 0 ? LV : 0, hi = l0 + nl < layers ? n - LV : n;
 #pragma unroll
-        for (int r = 0; r < (TR + W - 1) / W; ++r) {
-          const int i = sl + W * r;
-          sr_red(base + i, trow[i < TR ? i : 0], live[A] && i < n);
+          for (int r = 0; r < (TR + W - 1) / W; ++r) {
+            const int i = sl + W * r;
+            sr_put(base + i, trow[i < TR ? i : 0],
+                   i >= n ? 0 : (i < lo || i >= hi) ? (put & kPutAdd) : put);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < (TR + W - 1) / W; ++r) {
+            const int i = sl + W * r;
+            sr_red(base + i, trow[i < TR ? i : 0], live[A] && i < n);
+          }
         }
         __syncwarp(); // row reads done before the next flush stages
       }
@@ -772,7 +785,7 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
   // flush staging row (see sr_trow): the entity chunk's (W + 1) * (NV - 1)
   // values, added with lane-contiguous REDs (level copies and mid values
   // alternate in the column: per-lane REDs run at a 16-byte stride)
-  constexpr int TR = STREAM ? 0 : sre_trow<LY, W>();
+  constexpr int TR = sre_trow<LY, W>();
   double *const trow =
       reinterpret_cast<double *>(
           reinterpret_cast<int *>(sr_ring + (size_t)(kSreWarps * kSrDepth *
@@ -893,7 +906,7 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
     // one lane up; the chunk's top level by the last lane)
     auto flush = [&](double (&acc)[NV], double *yp, int m) {
       const double below = __shfl_up_sync(FULL, acc[NV - 1], 1, W);
-      if constexpr (STREAM) { // store-first patch strips
+      if constexpr (STREAM && TR == 0) { // store-first patch strips
         sr_put(yp, sl > 0 ? acc[0] + below : acc[0], m & bmask);
 #pragma unroll
         for (int v = 1; v < NV - 1; ++v) sr_put(yp + v, acc[v], m & mmask);
@@ -909,10 +922,20 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
         __syncwarp();
         double *const base = yp - sl * (NV - 1); // the chunk's first value
         const int n = nl * (NV - 1) + 1;
+        if constexpr (STREAM) { // store-first (m = 3): shared level copies add
+          const int lo = l0 > 0 ? 1 : 0, hi = l0 + nl < layers ? n - 1 : n;
 #pragma unroll
-        for (int r = 0; r < (TR + W - 1) / W; ++r) {
-          const int i = sl + W * r;
-          sr_red(base + i, trow[i < TR ? i : 0], m && i < n);
+          for (int r = 0; r < (TR + W - 1) / W; ++r) {
+            const int i = sl + W * r;
+            sr_put(base + i, trow[i < TR ? i : 0],
+                   i >= n ? 0 : (i < lo || i >= hi) ? (m & kPutAdd) : m);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < (TR + W - 1) / W; ++r) {
+            const int i = sl + W * r;
+            sr_red(base + i, trow[i < TR ? i : 0], m && i < n);
+          }
         }
         __syncwarp(); // row reads done before the next flush stages
       } else if (m && lane_ok) {
