@@ -111,6 +111,12 @@ template <class LY> constexpr int sr_threads() {
 #ifndef PM_SR_TROW
 #define PM_SR_TROW 1
 #endif
+// 1: ring copies zero-fill the unused tail of each row (every lane writes);
+// 0: lanes past the chunk copy nothing (measured: C5a -1 %, C4 P1 -3 %,
+// C5b +2 %: kept at 1)
+#ifndef PM_SR_ZFILL
+#define PM_SR_ZFILL 1
+#endif
 template <class LY, int W, int L> constexpr int sr_trow() {
   return (PM_SR_TROW && L == 1 && LY::CH0 > 1) ? (W + 1) * LY::CH0 : 0;
 }
@@ -233,8 +239,10 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
           sr_ring + (size_t)(NWARP * kSrDepth * SEGS + 1) * ES) +
                                  NWARP * SEGS * kSrIds) +
       ((threadIdx.x >> 5) * SEGS + seg) * TR;
-  for (int i = threadIdx.x; i < ES; i += blockDim.x)
-    sr_ring[(size_t)NWARP * kSrDepth * SEGS * ES + i] = 0.0;
+  // the zero block (and, without zero-filling copies, the whole ring)
+  for (int i = threadIdx.x; i < (PM_SR_ZFILL ? 1 : NWARP * kSrDepth * SEGS + 1) * ES;
+       i += blockDim.x)
+    sr_ring[(size_t)(PM_SR_ZFILL ? NWARP * kSrDepth * SEGS * ES : 0) + i] = 0.0;
   __syncthreads();
 
   // work item = (group, layer chunk), chunk fastest: the chunks of a group
@@ -364,11 +372,24 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         const double *fp = col_at(xl, v & IDM, colb);
         const double *cp = col_at(cl0, v & IDM, ccolb);
         double *e = entry(slot) + sl;
+#if PM_SR_ZFILL
 #pragma unroll
         for (int r = 0; r < FR; ++r) sr_cp8z(e + W * r, fp + W * r, fz[r]);
 #pragma unroll
         for (int r = 0; r < CR; ++r)
           sr_cp8z(e + FP + W * r, cp + W * r, cz[r]);
+#else
+        // lanes past the chunk copy nothing (the last row of each part is
+        // mostly empty: 1 of 33 field / 3 of 99 coordinate values at W =
+        // 32); they read stale ring values, finite since the ring starts
+        // zeroed, and are never flushed
+#pragma unroll
+        for (int r = 0; r < FR; ++r)
+          if (fz[r]) sr_cp8(e + W * r, fp + W * r);
+#pragma unroll
+        for (int r = 0; r < CR; ++r)
+          if (cz[r]) sr_cp8(e + FP + W * r, cp + W * r);
+#endif
       }
 #endif
       sr_commit(); // one group per step (possibly empty)

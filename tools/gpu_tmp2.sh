@@ -1,5 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q -x -k "patch_strips or pstrip" 2>&1 | tail -1
-for c in C5b C3; do
-  timeout 600 python tools/ab_sched.py $c stripred pstrip 2>&1 | grep -v Warn
-  for P in 64 128 256 1024; do echo "P=$P $(PM_PATCH_CELLS=$P timeout 600 python tools/ab_sched.py $c pstrip 2>&1 | grep -v Warn)"; done
-done
+timeout 900 python -m pytest tests -m gpu -q -x -k "stripred or strip_red or VP1 or CG1xCG1 or halo" 2>&1 | tail -1
+for c in C5a C5b C4-CG1xCG1-rcm-L50 C4-CG1xCG1-rcm-L20; do timeout 600 python tools/ab_sched.py $c stripred 2>&1 | grep -v Warn; done
