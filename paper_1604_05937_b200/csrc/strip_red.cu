@@ -92,8 +92,24 @@ template <class LY, int W, int L> constexpr int sr_frows() {
 template <class LY, int W, int L> constexpr int sr_crows() {
   return (3 * (W * L + 1) + (kSrVec - 1) + kSrVec * W - 1) / (kSrVec * W);
 }
+// PM_SR_PACK: the coordinate chunk follows the field chunk directly in the
+// ring entry (one row straddles both), so a step copies
+// ceil((fsz + 3 (CW + 1)) / W) rows instead of a row-rounded field part
+// plus a row-rounded coordinate part (P1 at W = 32: 5 copies instead of 6;
+// measured C5a -3 %, config-4 P1 -2..3 %; 3-vector P1 +1.5 %, so scalar
+// vertex columns only)
+#ifndef PM_SR_PACK
+#define PM_SR_PACK 1
+#endif
+template <class LY> constexpr bool sr_pack() {
+  return PM_SR_PACK && !PM_SR16 && LY::CH0 == 1;
+}
+template <class LY, int W, int L> constexpr int sr_prows() {
+  return (sr_fsz<LY, W * L>() + 3 * (W * L + 1) + W - 1) / W;
+}
 template <class LY, int W, int L> constexpr int sr_pentry() {
-  return (sr_frows<LY, W, L>() + sr_crows<LY, W, L>()) * kSrVec * W;
+  return sr_pack<LY>() ? sr_prows<LY, W, L>() * W
+                 : (sr_frows<LY, W, L>() + sr_crows<LY, W, L>()) * kSrVec * W;
 }
 constexpr int kSrIds = 64; // strip vertex ids staged per segment
 #ifndef PM_SR_VTHREADS
@@ -215,7 +231,10 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
   static_assert(NH == 3 && NC * NV == CH + LV, "vertex-column layout");
   static_assert(LV == 0 || (LV == NC && NV == 2 && CH == LV), "strip layout");
   constexpr int FR = sr_frows<LY, W, L>(), CR = sr_crows<LY, W, L>();
-  constexpr int FP = FR * kSrVec * W;        // coordinate part offset
+  // coordinate part offset in a ring entry
+  constexpr bool kSrPack = sr_pack<LY>();
+  constexpr int FP = kSrPack ? sr_fsz<LY, CW>() : FR * kSrVec * W;
+  constexpr int PR = sr_prows<LY, W, L>(); // rows of a packed entry
   constexpr int ES = sr_pentry<LY, W, L>();
   const int lane = threadIdx.x & 31;
   const int sl = lane % W, seg = lane / W;
@@ -285,7 +304,13 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
                       : (L == 1 && l0 + nl == layers) ? kPutStore
                                                        : kPutAdd;
     // source sizes of the lane's copies (8 inside the chunk, else 0)
-    int fz[FR], cz[CR];
+    int fz[FR], cz[CR], pz[PR];
+#pragma unroll
+    for (int r = 0; r < PR; ++r) { // packed rows: field, then coordinates
+      const int i = sl + W * r;
+      pz[r] = i < FP ? (i < nl * CH + LV ? 8 : 0)
+                     : (i - FP < 3 * (nl + 1) ? 8 : 0);
+    }
 #pragma unroll
     for (int r = 0; r < FR; ++r) fz[r] = sl + W * r < nl * CH + LV ? 8 : 0;
 #pragma unroll
@@ -372,6 +397,19 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         const double *fp = col_at(xl, v & IDM, colb);
         const double *cp = col_at(cl0, v & IDM, ccolb);
         double *e = entry(slot) + sl;
+        if constexpr (kSrPack) {
+#pragma unroll
+          for (int r = 0; r < PR; ++r) {
+            if (W * (r + 1) <= FP) // field row
+              sr_cp8z(e + W * r, fp + W * r, pz[r]);
+            else if (W * r >= FP) // coordinate row
+              sr_cp8z(e + W * r, cp + (W * r - FP), pz[r]);
+            else // the row that straddles both parts
+              sr_cp8z(e + W * r,
+                      sl + W * r < FP ? fp + W * r : cp + (W * r - FP),
+                      pz[r]);
+          }
+        } else {
 #if PM_SR_ZFILL
 #pragma unroll
         for (int r = 0; r < FR; ++r) sr_cp8z(e + W * r, fp + W * r, fz[r]);
@@ -390,6 +428,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         for (int r = 0; r < CR; ++r)
           if (cz[r]) sr_cp8(e + FP + W * r, cp + W * r);
 #endif
+        }
       }
 #endif
       sr_commit(); // one group per step (possibly empty)

@@ -1,7 +1,7 @@
-PM_STREAM_WS=1 timeout 900 python -m pytest tests -m gpu -q -x -k "DG1xDG1 or stream or host_pipelined" 2>&1 | tail -1
-for r in 0 1 2 3 0; do
-  echo "ws $r: $(PM_STREAM_WS=$r timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["roofline"]["kernel_ms"], d["value"], d["roofline"]["frac"])')"
+L=paper_1604_05937_b200/_native/libprismesh_cuda.so
+cp build/exp/pack.so $L
+timeout 900 python -m pytest tests -m gpu -q -k "stripred or strip_red or VP1 or CG1xCG1 or CG1xDG or halo or pstrip or patch_strips" 2>&1 | tail -1
+for v in nopack pack nopack pack; do
+  cp build/exp/$v.so $L
+  for c in C5a C5b C4-CG1xCG1-rcm-L50 C4-CG1xCG1-rcm-L20; do echo "$v $(timeout 600 python tools/ab_sched.py $c stripred 2>&1 | grep -v Warn | awk '{print $1, $3}')"; done
 done
-for c in C4-DG1xDG1-rcm-L20 C4-DG1xDG1-rcm-L256; do for r in 0 1; do
-  echo "$c ws $r: $(PM_STREAM_WS=$r timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["roofline"]["kernel_ms"], d["value"], d["roofline"]["frac"])')"
-done; done
