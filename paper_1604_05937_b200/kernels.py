@@ -540,8 +540,9 @@ def strip_max_len(n_cells: int, layers: int) -> int:
     4096 is slower again (too few items).  PM_STRIP_MAXLEN overrides."""
     import os
     cap = int(os.environ.get("PM_STRIP_MAXLEN", "512"))
+    items = int(os.environ.get("PM_STRIP_ITEMS", "12000"))  # tuning knob
     chunks = -(-layers // strip_chunk_width(layers))
-    return int(max(4, min(cap, n_cells * chunks // 12000)))
+    return int(max(4, min(cap, n_cells * chunks // items)))
 
 
 _COLORINGS = {}
