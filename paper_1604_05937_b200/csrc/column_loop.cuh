@@ -23,6 +23,16 @@ prism_abs_detj_mid(double xm0, double ym0, double dz0, double xm1, double ym1,
   return fabs(a2 * h);
 }
 
+// The same with the constant factors left out (12 |det J| from per-vertex
+// bottom+top sums of x, y and heights); callers fold 1/12 into their
+// Kronecker factors (kron_fold12).
+__device__ __forceinline__ double
+prism_abs_detj_12(double xs0, double ys0, double dz0, double xs1, double ys1,
+                  double dz1, double xs2, double ys2, double dz2) {
+  const double a2 = (xs1 - xs0) * (ys2 - ys0) - (xs2 - xs0) * (ys1 - ys0);
+  return fabs(a2 * (dz0 + dz1 + dz2));
+}
+
 // Reference-prism mass matrix as the tensor product of its triangle and
 // interval factors: Mref[(c,h,v),(c,h',v')] = Mtri[h][h'] * Mline[v][v'].
 struct KronMat {
@@ -66,6 +76,16 @@ inline bool kron_sym6(KronMat &M) {
          block_sym(M.t, 6, 3, 0, big, &q[0], &q[1]) &&
          fabs(q[0] - M.p[4]) <= 8 * 2.220446049250313e-16 * big &&
          fabs(q[1] - M.p[5]) <= 8 * 2.220446049250313e-16 * big;
+}
+
+// Scale the triangle-stage factors by 1/12 (the strip kernels accumulate
+// with 12 |det J|, prism_abs_detj_12)
+inline void kron_fold12(KronMat &M) {
+  constexpr double k = 1.0 / 12.0;
+  for (double &t : M.t) t *= k;
+  M.ta *= k;
+  M.tb *= k;
+  for (double &q : M.p) q *= k;
 }
 
 // Does the 3 x 3 triangle factor have the form ta I + tb J (to a relative

@@ -558,8 +558,10 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
       }
 #pragma unroll
       for (int j = 0; j < L; ++j) {
-        gm[A][j][0] = 0.5 * (g[j][0] + g[j + 1][0]); // same operations as
-        gm[A][j][1] = 0.5 * (g[j][1] + g[j + 1][1]); // prism_abs_detj
+        // bottom + top sums (2 xm, 2 ym) and the height; the factors 1/4
+        // and 1/3 of |det J| live in the Kronecker factors (kron_fold12)
+        gm[A][j][0] = g[j][0] + g[j + 1][0];
+        gm[A][j][1] = g[j][1] + g[j + 1][1];
         gm[A][j][2] = g[j + 1][2] - g[j][2];
       }
       __syncwarp(); // reads done before the slot is refilled
@@ -592,7 +594,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
       for (int j = 0; j < L; ++j) {
         // past the strip's end the window still holds two live vertices:
         // the step contributes nothing
-        const double dj = prism_abs_detj_mid(
+        const double dj = prism_abs_detj_12(
             gm[0][j][0], gm[0][j][1], gm[0][j][2], gm[1][j][0], gm[1][j][1],
             gm[1][j][2], gm[2][j][0], gm[2][j][1], gm[2][j][2]);
         // (with L > 1 a lane's upper level may lie past a partial chunk;
@@ -769,6 +771,7 @@ static int strip_red_k1(const LoopArgs &a, const int32_t *strip_ptr,
   for (int i = 0; i < LY::NH * LY::NH; ++i) M.t[i] = a.mtri[i];
   for (int i = 0; i < LY::NV * LY::NV; ++i) M.l[i] = a.mline[i];
   const bool sym = kron_sym3(M);
+  kron_fold12(M);
   const int L = strip_levels();
   switch (W) {
   case 32: return strip_red_w<LY, 32>(a, M, sym, L, strip_ptr, steps, n_strips);
@@ -1043,8 +1046,8 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
       enter(zv[A], en);
       {
         const double *g = en + OC + 3 * sl;
-        gm[A][0] = 0.5 * (g[0] + g[3]); // same operations as
-        gm[A][1] = 0.5 * (g[1] + g[4]); // prism_abs_detj
+        gm[A][0] = g[0] + g[3]; // bottom + top sums and the height:
+        gm[A][1] = g[1] + g[4]; // 12 |det J| (prism_abs_detj_12)
         gm[A][2] = g[5] - g[2];
       }
       yvc[A] = col_at(yv0, rv[R] & IDM, col0);
@@ -1070,7 +1073,7 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
       if (FILL && A < 2) return; // window not full yet
       // lanes past the chunk are never flushed; past the strip's end the
       // window still holds live entities: no contribution
-      const double dj = prism_abs_detj_mid(gm[0][0], gm[0][1], gm[0][2],
+      const double dj = prism_abs_detj_12(gm[0][0], gm[0][1], gm[0][2],
                                            gm[1][0], gm[1][1], gm[1][2],
                                            gm[2][0], gm[2][1], gm[2][2]);
       const double det =
@@ -1195,6 +1198,7 @@ static int strip_red_e_k1(const LoopArgs &a, const int32_t *strip_ptr,
   const int64_t items = n_strips * ((a.lend - a.lbeg + W - 1) / W);
   const int64_t warps = (items + segs - 1) / segs;
   const bool sym = kron_sym6(M);
+  kron_fold12(M);
 #define PM_SRE(WW)                                                           \
   do {                                                                       \
     if (sym)                                                                 \

@@ -1,4 +1,7 @@
-for L in 10 20 50 100; do for it in 3000 6000 12000; do for w in 16 32; do
-  echo "L=$L items=$it W=$w $(PM_STRIP_ITEMS=$it PM_STRIP_W=$w timeout 600 python tools/ab_sched.py C4-CG1xCG1-rcm-L$L stripred 2>&1 | grep -v Warn | awk '{print $3}')"
-done; done; done
-for it in 3000 6000 12000; do echo "C3 items=$it $(PM_STRIP_ITEMS=$it timeout 600 python tools/ab_sched.py C3 stripred 2>&1 | grep -v Warn | awk '{print $3}')"; done
+L=paper_1604_05937_b200/_native/libprismesh_cuda.so
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -1
+for v in pack fold pack fold; do
+  cp build/exp/$v.so $L
+  for c in C3 C5a C5b; do echo "$v $(timeout 600 python tools/ab_sched.py $c stripred 2>&1 | grep -v Warn | awk '{print $1, $3}')"; done
+done
+cp build/exp/fold.so $L
