@@ -1,1 +1,4 @@
-for c in C5b C5a C3; do for w in 16 32; do echo "W=$w $(PM_STRIP_W=$w timeout 600 python tools/ab_sched.py $c stripred 2>&1 | grep -v Warn | awk '{print $1, $3}')"; done; done
+for r in 1 4 5 6 1 4 5 6; do
+  echo "cfg $r: $(PM_STREAM_CFG=$r timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["ms_per_step"],5), round(d["roofline"]["kernel_ms"],5), round(d["value"]), round(d["roofline"]["frac"],4))')"
+done
+PM_STREAM_CFG=5 timeout 600 python -m pytest tests -m gpu -q -k "DG1xDG1 or stream" 2>&1 | tail -1
