@@ -117,8 +117,11 @@ constexpr int kSrIds = 64; // strip vertex ids staged per segment
 #endif
 // CTA size: 256 threads, 384 for the 3-vector layouts (12 warps at <= 168
 // registers instead of 8 at 182)
+#ifndef PM_SR_STHREADS
+#define PM_SR_STHREADS 256 // CTA size of the scalar / 2-channel strip kernel
+#endif
 template <class LY> constexpr int sr_threads() {
-  return LY::CH0 > 2 ? PM_SR_VTHREADS : 256;
+  return LY::CH0 > 2 ? PM_SR_VTHREADS : PM_SR_STHREADS;
 }
 // Multi-channel layouts (3-vector P1: CH = 3) flush through a per-segment
 // staging row of the chunk's (W + 1) * CH values, so the REDs run over
@@ -195,7 +198,7 @@ __device__ __forceinline__ T *col_at(T *base, int v, int stride_bytes) {
 }
 
 template <class LY, int L> constexpr int sr_blocks() {
-  return (LY::CH0 > 2 || L > 1) ? 1 : 2;
+  return (LY::CH0 > 2 || L > 1) ? 1 : 512 / PM_SR_STHREADS;
 }
 
 // The element kernel split along the window: y = det (Mtri (x) Mline) x.

@@ -1,4 +1,6 @@
-PM_STREAM_CFG=7 timeout 600 python -m pytest tests -m gpu -q -k "DG1xDG1 or stream or host_pipelined" 2>&1 | tail -1
-for r in 1 7 8 9 1 7 8 9; do
-  echo "cfg $r: $(PM_STREAM_CFG=$r timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["ms_per_step"],5), round(d["roofline"]["kernel_ms"],5), round(d["value"]), round(d["roofline"]["frac"],4))')"
+L=paper_1604_05937_b200/_native/libprismesh_cuda.so
+for v in st256 st128 st512 st256 st128; do
+  cp build/exp/$v.so $L
+  for c in C5a C4-CG1xCG1-rcm-L50; do echo "$v $(timeout 600 python tools/ab_sched.py $c stripred 2>&1 | grep -v Warn | awk '{print $1, $3}')"; done
 done
+cp build/exp/st256.so $L
