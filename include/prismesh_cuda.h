@@ -24,6 +24,8 @@
  *   pm_build_strips          <- host planner of that schedule
  *   pm_column_mass_strip_red <- same, global strips + REDG
  *   pm_build_global_strips   <- host planner of that schedule
+ *   pm_column_mass_tile      <- same, band tiles staged by TMA bulk copies
+ *   pm_tiles_build / _info / _export / _free <- host planner of that schedule
  *   pm_column_mass_patch_strips <- same, store-first strips inside patches
  *   pm_build_patch_strips    <- host planner of that schedule
  *   pm_column_mass_strip_bulk<- same, TMA bulk-copy prefetch
@@ -170,6 +172,61 @@ int pm_column_mass_strip_red(const int32_t *delta6, int32_t k, int32_t layers,
                              const int32_t *steps,
                              const int32_t *steps_e /* P2: 2 edges/step */,
                              int64_t n_vertices, void *stream);
+
+/* Band-tile schedule for vertex-column layouts (P1, 3-vector P1, CG1 x DG0,
+ * CG1 x DG1; a vertex-permutation invariant triangle factor).  A persistent
+ * grid, one CTA per SM; CTA c takes tiles c, c + G, ... of pm_tiles_build:
+ * producer warps stage each tile's vertex runs (whole columns of x and of
+ * the coordinate field) in shared memory with one cp.async.bulk per run and
+ * array (stages = pm_tile_smem_layout's *stages tiles in flight), a zeroing
+ * warp zeroes the output columns each tile touches first (y needs no
+ * memset) and publishes that, the tile waits for the tiles zeroing its
+ * columns, and the other warps walk the tile's strips as in
+ * pm_column_mass_strip_red.  blob / off = pm_tiles_blob's records, zero_ptr
+ * / zero_v0 / zero_n = pm_tiles_export's first-touch runs (device); ctl =
+ * int32[3] initially {0, 0, 1}, flags = int32[n_tiles] initially 0 (so one
+ * plan must not serve concurrent calls).  x and y index global DoFs;
+ * n_dofs / n_coords = valid doubles from x / coords.  area_c = byte offset
+ * of the coordinate area in a data buffer of data_bytes (a multiple of 128)
+ * bytes; width = lanes (layers) per segment: 8, 16 or 32. */
+int pm_column_mass_tile(const int32_t *delta6, int32_t layers,
+                        const double *coords, int64_t n_coords,
+                        const double *mtri, const double *mline,
+                        const double *x, double *y, int64_t n_dofs,
+                        const int32_t *blob, const int64_t *off,
+                        const int32_t *zero_ptr, const int32_t *zero_v0,
+                        const int32_t *zero_n, int32_t *ctl, int32_t *flags,
+                        int32_t n_tiles, int32_t area_c,
+                        int32_t data_bytes, int32_t max_slots,
+                        int32_t max_words, int32_t width, void *stream);
+/* Shared-memory bytes in front of the data buffers; *stages = buffers,
+ * *threads = CTA size (both compile-time). */
+int pm_tile_smem_layout(const int32_t *delta6, int32_t max_words,
+                        int32_t max_slots, int32_t width, int32_t *stages,
+                        int32_t *threads);
+
+/* Host planner of the band-tile schedule: cells in index order cut into
+ * tiles of consecutive cells whose vertex columns (col_f + col_c bytes
+ * each, + 32 bytes slack) fit `budget`, at most max_cells each; strips
+ * split until a tile has min_strips of at least min_sub cells.  *handle
+ * receives the plan (pm_tiles_info: {tiles, runs, zero runs, deps, strips,
+ * steps, max field area, max coordinate area, max slots, max cells, max
+ * strips per tile};
+ * pm_tiles_export: the 14 int32 arrays cell_ptr, run_ptr, run_v0, run_n,
+ * run_fa, run_ca, zero_ptr, zero_v0, zero_n, dep_ptr, deps, strip_ptr,
+ * strip_step0, strip_len and the int16 steps; pm_tiles_free). */
+int pm_tiles_build(int64_t n_cells, int64_t n_vertices, int64_t n_edges,
+                   const int32_t *cell_vertices, const int32_t *cell_edges,
+                   int64_t col_f, int64_t col_c, int64_t budget,
+                   int32_t max_cells, int32_t min_strips, int32_t min_sub,
+                   void **handle);
+int pm_tiles_info(void *handle, int64_t *info);
+int pm_tiles_export(void *handle, int32_t **arrays, int16_t *steps);
+/* The plan as one int32 record per tile (the kernel's input): off[t] ..
+ * off[t+1] (n_tiles + 1 entries) = tile t's words of blob; NULL blob / off
+ * only sizes it: sizes = {total words, longest record}. */
+int pm_tiles_blob(void *handle, int32_t *blob, int64_t *off, int64_t *sizes);
+void pm_tiles_free(void *handle);
 
 /* The same schedule with TMA bulk-copy prefetch (one lane per segment issues
  * cp.async.bulk copies completing on per-slot mbarriers).  x/y hold global

@@ -12,7 +12,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_native", "libprismesh_cuda.so")
+# PM_NATIVE_LIB: an experimental build of the same library (tools/)
+LIB_PATH = os.environ.get("PM_NATIVE_LIB") or \
+    os.path.join(_HERE, "_native", "libprismesh_cuda.so")
 
 PM_OK, PM_EINVAL, PM_ECUDA, PM_EOVERFLOW = 0, 1, 2, 3
 SHARE_NONE, SHARE_VERTICAL, SHARE_HORIZONTAL = 0, 1, 2
@@ -110,6 +112,19 @@ SIGNATURES = {
     "pm_set_launch_overlap": (ctypes.c_int, [_i32]),
     "pm_stream_triad": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, _i64,
                                        _vp]),
+    "pm_tiles_build": (ctypes.c_int, [_i64, _i64, _i64, _vp, _vp, _i64, _i64,
+                                      _i64, _i32, _i32, _i32,
+                                      ctypes.POINTER(_vp)]),
+    "pm_tiles_info": (ctypes.c_int, [_vp, _i64p]),
+    "pm_tiles_export": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), _vp]),
+    "pm_tiles_free": (None, [_vp]),
+    "pm_tiles_blob": (ctypes.c_int, [_vp, _vp, _vp, _i64p]),
+    "pm_tile_smem_layout": (ctypes.c_int, [_i32p, _i32, _i32, _i32, _i32p,
+                                           _i32p]),
+    "pm_column_mass_tile": (ctypes.c_int, [
+        _i32p, _i32, _vp, _i64, ctypes.POINTER(_f64), ctypes.POINTER(_f64),
+        _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32,
+        _i32, _i32, _i32, _vp]),
 }
 
 
@@ -612,3 +627,93 @@ def device_info():
     l2 = ctypes.c_int64(0)
     check(host_lib().pm_device_info(ctypes.byref(sm), ctypes.byref(l2)))
     return sm.value, l2.value
+
+
+# ---------------------------------------------------------------------------
+# band-tile schedule (csrc/tile_plan.cpp, csrc/tile.cu)
+# ---------------------------------------------------------------------------
+
+TILE_ARRAYS = ("cell_ptr", "run_ptr", "run_v0", "run_n", "run_fa", "run_ca",
+               "zero_ptr", "zero_v0", "zero_n", "dep_ptr", "deps",
+               "strip_ptr", "strip_step0", "strip_len")
+
+
+def build_tiles(base, col_f_bytes, col_c_bytes, budget, max_cells=256,
+                min_strips=1, min_sub=4, arrays=True):
+    """Host plan of the tile schedule (pm_tiles_build): the per-tile records
+    ``blob`` (int32) with offsets ``off`` (int64) the kernel reads, and the
+    sizes ``n_tiles``, ``max_fa``, ``max_ca`` (bytes), ``max_slots``,
+    ``max_cells``, ``max_words``; ``arrays``: also the plan as separate
+    int32 arrays (TILE_ARRAYS) and int16 ``steps`` (tests)."""
+    cv = np.ascontiguousarray(base.cell_vertices, dtype=np.int32)
+    ce = np.ascontiguousarray(base.cell_edges, dtype=np.int32)
+    h = ctypes.c_void_p()
+    L = host_lib()
+    check(L.pm_tiles_build(cv.shape[0], base.num_vertices, base.num_edges,
+                           cv.ctypes.data_as(ctypes.c_void_p),
+                           ce.ctypes.data_as(ctypes.c_void_p), int(col_f_bytes),
+                           int(col_c_bytes), int(budget), int(max_cells),
+                           int(min_strips), int(min_sub), ctypes.byref(h)))
+    try:
+        info = np.zeros(11, dtype=np.int64)
+        check(L.pm_tiles_info(h, info.ctypes.data_as(_i64p)))
+        nt, nr, nz, nd, ns, nk = (int(v) for v in info[:6])
+        sizes = np.zeros(2, dtype=np.int64)
+        check(L.pm_tiles_blob(h, None, None, sizes.ctypes.data_as(_i64p)))
+        blob = np.zeros(max(1, int(sizes[0])), dtype=np.int32)
+        off = np.zeros(nt + 1, dtype=np.int64)
+        check(L.pm_tiles_blob(h, blob.ctypes.data_as(ctypes.c_void_p),
+                              off.ctypes.data_as(ctypes.c_void_p),
+                              sizes.ctypes.data_as(_i64p)))
+        plan = {"blob": blob, "off": off, "n_tiles": nt,
+                "max_fa": int(info[6]), "max_ca": int(info[7]),
+                "max_slots": int(info[8]), "max_cells": int(info[9]),
+                "max_strips": int(info[10]), "max_words": int(sizes[1])}
+        if arrays:
+            lens = {"cell_ptr": nt + 1, "run_ptr": nt + 1, "run_v0": nr,
+                    "run_n": nr, "run_fa": nr, "run_ca": nr,
+                    "zero_ptr": nt + 1, "zero_v0": nz, "zero_n": nz,
+                    "dep_ptr": nt + 1, "deps": nd, "strip_ptr": nt + 1,
+                    "strip_step0": ns, "strip_len": ns}
+            out = {k: np.zeros(max(lens[k], 1), dtype=np.int32)
+                   for k in TILE_ARRAYS}
+            steps = np.zeros(max(nk, 1), dtype=np.int16)
+            arr = (_vp * 14)(*[out[k].ctypes.data_as(ctypes.c_void_p)
+                               for k in TILE_ARRAYS])
+            check(L.pm_tiles_export(h, arr,
+                                    steps.ctypes.data_as(ctypes.c_void_p)))
+            plan.update({k: out[k][:lens[k]] for k in TILE_ARRAYS})
+            plan["steps"] = steps[:nk]
+    finally:
+        L.pm_tiles_free(h)
+    return plan
+
+
+def tile_smem_layout(layout, max_words, max_slots, width):
+    """(bytes in front of the data buffers, number of buffers, CTA size)."""
+    d = layout.delta6()
+    st, th = ctypes.c_int32(0), ctypes.c_int32(0)
+    off = host_lib().pm_tile_smem_layout(d.ctypes.data_as(_i32p),
+                                         int(max_words), int(max_slots),
+                                         int(width), ctypes.byref(st),
+                                         ctypes.byref(th))
+    return int(off), int(st.value), int(th.value)
+
+
+def column_mass_tile(layout, layers, coords, x, y, n_dofs, dplan, kron,
+                     width, stream=None, x_base=0, y_base=0, coords_base=0):
+    """pm_column_mass_tile: y = M x with the band-tile schedule (y needs no
+    zeroing: every output column is zeroed by the tile that touches it
+    first)."""
+    mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
+    ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
+    d = layout.delta6()
+    check(host_lib().pm_column_mass_tile(
+        d.ctypes.data_as(_i32p), layers, ptr(coords, coords_base),
+        coords_base + coords.shape[0], _f64ptr(mt), _f64ptr(ml),
+        ptr(x, x_base), ptr(y, y_base), n_dofs, ptr(dplan["blob"]),
+        ptr(dplan["off"]), ptr(dplan["zero_ptr"]), ptr(dplan["zero_v0"]),
+        ptr(dplan["zero_n"]), ptr(dplan["ctl"]), ptr(dplan["flags"]),
+        dplan["n_tiles"], dplan["area_c"], dplan["data_bytes"],
+        dplan["max_slots"], dplan["max_words"], int(width),
+        stream_ptr(stream)))

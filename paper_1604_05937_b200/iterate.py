@@ -43,7 +43,7 @@ import numpy as np
 from . import _lib
 
 SCHEDULES = ("auto", "atomic", "colored", "sequential", "column", "stream",
-             "patch", "strip", "stripred")
+             "patch", "strip", "stripred", "pstrip", "tile")
 
 
 @dataclass(frozen=True)

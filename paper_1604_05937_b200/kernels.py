@@ -155,6 +155,8 @@ class MassOperator:
         self._strip = None
         self._gstrips = None
         self._pstrips = None
+        self._tiles = None
+        self._tile_tmp = None
         self._strip_inv = None
         self._hbuf = None
         self._dev = _lib.cuda_device()
@@ -208,6 +210,63 @@ class MassOperator:
             self._strip_inv = bool(self.kron_ok and
                                    tri_permutation_invariant(self.kron[0]))
         return self._strip_inv
+
+    @property
+    def tile_ok(self) -> bool:
+        """Layouts of the band-tile kernel (csrc/tile.cu): vertex columns
+        only, vertex-permutation invariant triangle factor."""
+        d = tuple(self.fs.layout.delta6())
+        return d in _STRIP_LAYOUTS and self.strip_invariant
+
+    def _tile_plan(self):
+        """Band tiles (cached): host plan (pm_tiles_build), its per-tile
+        records on the device and the plan's ticket / epoch words."""
+        if self._tiles is None:
+            import os
+            import torch
+            L = self.layers
+            d = self.fs.layout.delta6()
+            colf = 8 * (int(d[0]) * (L + 1) + int(d[1]) * L)
+            colc = 24 * (L + 1)
+            W = strip_chunk_width(L)
+            # one CTA of PM_TILE_THREADS threads per SM (228 KB of shared
+            # memory, 1 KB reserved), `stages` tile buffers in it;
+            # PM_TILE_BUDGET overrides the bytes per buffer
+            cap = 233472 - 1024
+            off, stages, threads = _lib.tile_smem_layout(self.fs.layout,
+                                                         1024, 128, W)
+            budget = int(os.environ.get("PM_TILE_BUDGET", "0")) or \
+                (cap - off) // stages - 256
+            nchunks = -(-L // W)
+            # walking warps take items from several staged tiles at once:
+            # no strip splitting needed for parallelism
+            min_strips = int(os.environ.get("PM_TILE_MIN_STRIPS", "1"))
+            while True:
+                plan = _lib.build_tiles(self.fs.mesh.base, colf, colc, budget,
+                                        max_cells=256, min_strips=min_strips)
+                area_c = (plan["max_fa"] + 127) // 128 * 128
+                data = (area_c + plan["max_ca"] + 127) // 128 * 128
+                off, stages, _ = _lib.tile_smem_layout(
+                    self.fs.layout, plan["max_words"], plan["max_slots"], W)
+                if off + stages * data <= cap or \
+                        budget < 3 * (colf + colc + 32) + 4096:
+                    break
+                budget -= (off + stages * data - cap) // stages + 256
+            dev = {k: torch.from_numpy(np.resize(plan[k], max(1, plan[k].size))
+                                       ).to(self._dev)
+                   for k in ("blob", "off", "zero_ptr", "zero_v0", "zero_n")}
+            dev.update({
+                   "ctl": torch.tensor([0, 0, 1, 0], dtype=torch.int32,
+                                       device=self._dev),
+                   "flags": torch.zeros(max(1, plan["n_tiles"]),
+                                        dtype=torch.int32, device=self._dev)})
+            dev.update(n_tiles=plan["n_tiles"], area_c=area_c,
+                       data_bytes=data, max_slots=plan["max_slots"],
+                       max_words=plan["max_words"],
+                       max_cells=plan["max_cells"], width=W, budget=budget,
+                       smem=off + stages * data, stages=stages)
+            self._tiles = dev
+        return self._tiles
 
     @property
     def dg_only(self) -> bool:
@@ -413,6 +472,24 @@ class MassOperator:
                                        self.kron, W, accumulate=accumulate,
                                        stream=stream,
                                        n_vertices=self.fs.mesh.base.num_vertices)
+            return y
+        if sched == "tile":
+            if not self.tile_ok:
+                raise ValueError(
+                    f"the tile schedule needs a vertex-column layout (P1, "
+                    f"3-vector P1, CG1xDG0, CG1xDG1) and a vertex-permutation "
+                    f"invariant triangle factor, got {self.fs.layout.name}")
+            plan = self._tile_plan()
+            out = y
+            if accumulate:
+                if self._tile_tmp is None or self._tile_tmp.shape != y.shape:
+                    self._tile_tmp = torch.empty_like(y)
+                out = self._tile_tmp
+            _lib.column_mass_tile(self.fs.layout, self.layers, coords, x, out,
+                                  n, plan, self.kron, plan["width"],
+                                  stream=stream)
+            if accumulate:
+                y += out
             return y
         if sched == "pstrip":
             if not self.stripred_ok:
