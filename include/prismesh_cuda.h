@@ -28,7 +28,6 @@
  *   pm_tiles_build / _info / _export / _free <- host planner of that schedule
  *   pm_column_mass_patch_strips <- same, store-first strips inside patches
  *   pm_build_patch_strips    <- host planner of that schedule
- *   pm_column_mass_strip_bulk<- same, TMA bulk-copy prefetch
  *   pm_column_mass_dg_range  <- the DG loop over a cell range (pipelining)
  *   pm_column_probe          <- SPEC.md:338-340 counting / gather kernels
  *                               (verification.py:47-75 materialized maps)
@@ -61,7 +60,12 @@ enum {
   PM_VARIANT_PATCH = 2,   /* patch-owner gather (pm_column_mass_patch)      */
   PM_VARIANT_COLUMN = 3,  /* warp segment per column, lanes = layers, REDG   */
   PM_VARIANT_COLORED = 4, /* COLUMN over one colour's cells, plain RMW      */
-  PM_VARIANT_STREAM = 5,  /* DG (2,1) fields through TMA bulk copies        */
+  PM_VARIANT_STREAM = 5,  /* DG (2,1) fields through TMA bulk copies; the
+                             field is addressed densely (cell c, layer l,
+                             slot j at (c L + l) k + j), i.e. the Alg. 1
+                             numbering of cell-only layouts: cell_map and
+                             offsets are not read for the field (only the
+                             coordinate maps are)                          */
   PM_VARIANT_STRIP = 6,   /* strip-patch owner gather (pm_column_mass_strip) */
   PM_VARIANT_STRIPRED = 7 /* global strips + REDG (pm_column_mass_strip_red) */
 };
@@ -228,20 +232,6 @@ int pm_tiles_export(void *handle, int32_t **arrays, int16_t *steps);
 int pm_tiles_blob(void *handle, int32_t *blob, int64_t *off, int64_t *sizes);
 void pm_tiles_free(void *handle);
 
-/* The same schedule with TMA bulk-copy prefetch (one lane per segment issues
- * cp.async.bulk copies completing on per-slot mbarriers).  x/y hold global
- * DoF indices [x_lo, x_hi) (y has the same numbering), coords [c_lo, c_hi);
- * accumulate = 0 zeroes y[x_lo:x_hi] first. */
-int pm_column_mass_strip_bulk(const int32_t *delta6, int32_t k,
-                              int32_t layers, const double *coords,
-                              const double *mref, const double *mtri,
-                              const double *mline, const double *x, double *y,
-                              int64_t x_lo, int64_t x_hi, int64_t c_lo,
-                              int64_t c_hi, int32_t accumulate,
-                              int64_t n_strips, int32_t chunk,
-                              const int32_t *strip_ptr, const int32_t *steps,
-                              void *stream);
-
 /* DG (2,1) fields: the stream kernel over the cell range
  * [cell_begin, cell_end) only (cell_begin*layers a multiple of 256); y is
  * overwritten there.  Used to pipeline host<->device copies with compute. */
@@ -376,6 +366,15 @@ int pm_column_mass_strip_red_peer(
 int pm_ipc_export(const void *ptr, void *handle64, int64_t *offset);
 int pm_ipc_open(const void *handle64, int64_t offset, void **ptr);
 int pm_ipc_close(void *ptr, int64_t offset);
+
+/* Stream-ordered signalling between ranks (the fused halo's step protocol,
+ * no host synchronisation): pm_stream_signal queues a one-thread kernel
+ * that, after the stream's preceding work, stores `value` to `flag`
+ * (system-scope release; `flag` may be a peer mapping from pm_ipc_open);
+ * pm_stream_wait_geq makes `stream` wait until the local 32-bit `flag` is
+ * >= value (cuStreamWaitValue32, no spinning kernel). */
+int pm_stream_signal(uint32_t *flag, uint32_t value, void *stream);
+int pm_stream_wait_geq(const uint32_t *flag, uint32_t value, void *stream);
 
 /* Device derive_edges (replaces mesh.py:33-84 derive_edges): edge set of a
  * triangle mesh as the sorted unique vertex pairs, cell_edges[c][k] = the

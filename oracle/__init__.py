@@ -74,6 +74,16 @@ def lib():
                                       _i32p]
         L.or_max_threads.restype = ctypes.c_int
         L.or_max_threads.argtypes = []
+        L.or_unit_square.restype = None
+        L.or_unit_square.argtypes = [ctypes.c_int32, _i32p, _f64p]
+        L.or_derive_edges.restype = ctypes.c_int64
+        L.or_derive_edges.argtypes = [_i32p, ctypes.c_int64, _i32p, _i32p]
+        L.or_rcm_order.restype = None
+        L.or_rcm_order.argtypes = [_i32p, ctypes.c_int64, ctypes.c_int64,
+                                   _i64p]
+        L.or_apply_ordering.restype = None
+        L.or_apply_ordering.argtypes = [_i32p, ctypes.c_int64, _f64p,
+                                        ctypes.c_int64, _i64p, _i32p, _f64p]
         _lib = L
     return _lib
 
@@ -226,3 +236,100 @@ class Problem:
 
 def max_threads():
     return lib().or_max_threads()
+
+
+# ---------------------------------------------------------------------------
+# base meshes without the product library (oracle_mesh.c)
+# ---------------------------------------------------------------------------
+
+class Mesh:
+    """Base mesh arrays (the attributes Problem and the product's
+    ExtrudedMesh read): cell_vertices, coords, edge_vertices, cell_edges."""
+
+    def __init__(self, cell_vertices, coords):
+        self.cell_vertices = np.ascontiguousarray(cell_vertices,
+                                                  dtype=np.int32)
+        self.coords = np.ascontiguousarray(coords, dtype=np.float64)
+        n = self.cell_vertices.shape[0]
+        ev = np.empty((max(1, 3 * n), 2), dtype=np.int32)
+        ce = np.empty((n, 3), dtype=np.int32)
+        ne = lib().or_derive_edges(_p(self.cell_vertices, _i32p), n,
+                                   _p(ev, _i32p), _p(ce, _i32p))
+        if ne < 0:
+            raise ValueError("edge shared by more than two cells")
+        self.edge_vertices = ev[:ne].copy()
+        self.cell_edges = ce
+
+    @property
+    def num_vertices(self):
+        return self.coords.shape[0]
+
+    @property
+    def num_edges(self):
+        return self.edge_vertices.shape[0]
+
+    @property
+    def num_cells(self):
+        return self.cell_vertices.shape[0]
+
+
+def unit_square(n):
+    """mesh.py:228-254 generate_unit_square_mesh."""
+    k = n + 1
+    cells = np.empty((2 * n * n, 3), dtype=np.int32)
+    coords = np.empty((k * k, 2), dtype=np.float64)
+    lib().or_unit_square(n, _p(cells, _i32p), _p(coords, _f64p))
+    return Mesh(cells, coords)
+
+
+def rcm_forward(mesh):
+    """ordering.py:93-120 rcm_vertex_order: forward[old] = new."""
+    fwd = np.empty(mesh.num_vertices, dtype=np.int64)
+    ev = np.ascontiguousarray(mesh.edge_vertices, dtype=np.int32)
+    lib().or_rcm_order(_p(ev, _i32p), ev.shape[0], mesh.num_vertices,
+                       _p(fwd, _i64p))
+    return fwd
+
+
+def random_forward(count, seed):
+    """ordering.py:123-131 random_order (numpy's PCG64 permutation)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    shuffled = rng.permutation(count)
+    forward = np.empty(count, dtype=np.int64)
+    forward[shuffled] = np.arange(count)
+    return forward
+
+
+def apply_ordering(mesh, forward):
+    """ordering.py:134-152 apply_ordering."""
+    fwd = np.ascontiguousarray(forward, dtype=np.int64)
+    cells = np.empty_like(mesh.cell_vertices)
+    coords = np.empty_like(mesh.coords)
+    lib().or_apply_ordering(_p(mesh.cell_vertices, _i32p), mesh.num_cells,
+                            _p(mesh.coords, _f64p), mesh.num_vertices,
+                            _p(fwd, _i64p), _p(cells, _i32p),
+                            _p(coords, _f64p))
+    return Mesh(cells, coords)
+
+
+def base_mesh(n, ordering="rcm", jitter=0.0, seed=0):
+    """The BASELINE config meshes, built like the product's
+    configs.base_mesh: (mesh, rng) with rng = default_rng(seed) positioned
+    after the jitter draws (interior vertices moved by U(-jitter h,
+    jitter h) before the ordering)."""
+    rng = np.random.default_rng(seed)
+    nv = (n + 1) ** 2
+    d = rng.uniform(-jitter / n, jitter / n, size=(nv, 2)) if jitter else None
+    m = unit_square(n)
+    if jitter:
+        c = m.coords.copy()
+        inner = (c[:, 0] > 0) & (c[:, 0] < 1) & (c[:, 1] > 0) & (c[:, 1] < 1)
+        c[inner] += d[inner]
+        m = Mesh(m.cell_vertices, c)
+    if ordering == "rcm":
+        m = apply_ordering(m, rcm_forward(m))
+    elif ordering == "random":
+        m = apply_ordering(m, random_forward(m.num_vertices, seed))
+    elif ordering != "natural":
+        raise ValueError(f"unknown ordering {ordering!r}")
+    return m, rng

@@ -70,13 +70,6 @@ SIGNATURES = {
                                                 ctypes.POINTER(_f64), _vp,
                                                 _vp, _i64, _i32, _i64, _i32,
                                                 _vp, _vp, _vp, _i64, _vp]),
-    "pm_column_mass_strip_bulk": (ctypes.c_int, [_i32p, _i32, _i32, _vp,
-                                                 ctypes.POINTER(_f64),
-                                                 ctypes.POINTER(_f64),
-                                                 ctypes.POINTER(_f64), _vp,
-                                                 _vp, _i64, _i64, _i64, _i64,
-                                                 _i32, _i64, _i32, _vp, _vp,
-                                                 _vp]),
     "pm_column_mass_dg_range": (ctypes.c_int, [_i32p, _i32, _i64, _i64, _i32,
                                                _vp, _vp, _vp, _vp, _vp,
                                                ctypes.POINTER(_f64), _vp,
@@ -109,6 +102,8 @@ SIGNATURES = {
     "pm_ipc_export": (ctypes.c_int, [_vp, _vp, _i64p]),
     "pm_ipc_open": (ctypes.c_int, [_vp, _i64, ctypes.POINTER(_vp)]),
     "pm_ipc_close": (ctypes.c_int, [_vp, _i64]),
+    "pm_stream_signal": (ctypes.c_int, [_vp, ctypes.c_uint32, _vp]),
+    "pm_stream_wait_geq": (ctypes.c_int, [_vp, ctypes.c_uint32, _vp]),
     "pm_set_launch_overlap": (ctypes.c_int, [_i32]),
     "pm_stream_triad": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_double, _i64,
                                        _vp]),
@@ -504,22 +499,19 @@ def ipc_close(addr, offset):
     check(host_lib().pm_ipc_close(ctypes.c_void_p(addr), int(offset)))
 
 
-def column_mass_strip_bulk(layout, k, layers, coords, mref, x, y, x_range,
-                           c_range, strips, kron, chunk, accumulate=False,
-                           stream=None, x_base=0, coords_base=0):
-    """pm_column_mass_strip_bulk (vertex layouts): TMA-prefetched strips."""
-    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
-    mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
-    ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
-    d = layout.delta6()
-    sp, st = strips[0], strips[1]
-    rc = host_lib().pm_column_mass_strip_bulk(
-        d.ctypes.data_as(_i32p), k, layers, ptr(coords, coords_base),
-        _f64ptr(m), _f64ptr(mt), _f64ptr(ml), ptr(x, x_base), ptr(y, x_base),
-        x_range[0], x_range[1], c_range[0], c_range[1],
-        1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp), ptr(st),
-        stream_ptr(stream))
-    check(rc)
+def stream_signal(addr, value, stream=None):
+    """Queue: after the stream's work, store ``value`` (uint32) to device
+    address ``addr`` (local or a peer mapping)."""
+    check(host_lib().pm_stream_signal(ctypes.c_void_p(addr),
+                                      int(value) & 0xffffffff,
+                                      stream_ptr(stream)))
+
+
+def stream_wait_geq(addr, value, stream=None):
+    """The stream waits until the uint32 at local ``addr`` is >= value."""
+    check(host_lib().pm_stream_wait_geq(ctypes.c_void_p(addr),
+                                        int(value) & 0xffffffff,
+                                        stream_ptr(stream)))
 
 
 def column_mass_dg_range(layout, k, c0, c1, layers, cmap, offs, xmap, xoffs,

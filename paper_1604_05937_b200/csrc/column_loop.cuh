@@ -193,9 +193,5 @@ int launch_column(const LoopArgs &a, const int32_t *delta6, bool colored);
 int launch_cell_stream(const LoopArgs &a, const int32_t *delta6,
                        bool *handled);
 bool column_supports(const int32_t *delta6);
-int launch_strip_bulk(const LoopArgs &a, const int32_t *delta6,
-                      const int32_t *strip_ptr, const int32_t *steps,
-                      int64_t n_strips, int W, int64_t x_lo, int64_t x_hi,
-                      int64_t c_lo, int64_t c_hi);
 
 } // namespace pm

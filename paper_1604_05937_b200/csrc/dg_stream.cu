@@ -217,12 +217,20 @@ static int dg_stream_launch(const LoopArgs &a, const MassMat<D> &M,
                             int64_t n_units, int64_t cl_begin) {
   const size_t smem = S * T * D * sizeof(double) + S * sizeof(uint64_t);
   auto kern = k_dg_stream<D, S, MINB, T>;
-  PM_CUDA_TRY(cudaFuncSetAttribute(
-      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  PM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
-                                                            T, smem));
-  if (per_sm < 1) per_sm = 1;
+  // the attribute and the occupancy are properties of the instantiation:
+  // queried once (per device), not on every call
+  static int cached_dev = -1, per_sm = 0;
+  int dev = 0;
+  PM_CUDA_TRY(cudaGetDevice(&dev));
+  if (cached_dev != dev) {
+    PM_CUDA_TRY(cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int nb = 0;
+    PM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T,
+                                                              smem));
+    per_sm = nb < 1 ? 1 : nb;
+    cached_dev = dev;
+  }
   int64_t grid = (int64_t)sm_count() * per_sm;
   if (grid > n_units) grid = n_units;
   if (launch_overlap()) {

@@ -67,10 +67,6 @@ template <class LY, int W> constexpr int srb_entry() {
 constexpr int kSrDepth = PM_SR_DEPTH;
 static_assert(kSrDepth == 3 || kSrDepth == 6, "ring depth 3 or 6");
 
-// 3-vector windows need more registers: one CTA per SM there
-template <class LY> constexpr int sr_min_blocks() {
-  return LY::CH0 > 2 ? 1 : 2; // measured: 3/SM (scalar) and 2/SM (3-vector) slower
-}
 
 // Padded ring entries of the strip kernel (a chunk of CW = W*L levels):
 // the field part and the coordinate part are whole rows of W values, so
@@ -120,6 +116,9 @@ constexpr int kSrIds = 64; // strip vertex ids staged per segment
 #ifndef PM_SR_STHREADS
 #define PM_SR_STHREADS 256 // CTA size of the scalar / 2-channel strip kernel
 #endif
+static_assert(PM_SR_STHREADS == 128 || PM_SR_STHREADS == 256 ||
+                  PM_SR_STHREADS == 512,
+              "PM_SR_STHREADS: 128, 256 or 512 (2 CTAs of 256 per SM at most)");
 template <class LY> constexpr int sr_threads() {
   return LY::CH0 > 2 ? PM_SR_VTHREADS : PM_SR_STHREADS;
 }
@@ -176,6 +175,16 @@ __device__ __forceinline__ void sr_put(double *p, double v, int mode) {
                "@ps st.global.f64 [%0], %1;\n\t"
                "@pr red.global.add.f64 [%0], %1;\n\t}" ::"l"(p),
                "d"(v), "r"(mode)
+               : "memory");
+}
+// predicated REDG, system scope (the fused halo's adds into a peer's window
+// over NVLink, and the owner's own adds into it, are ordered at system
+// scope; red.global defaults to .gpu)
+__device__ __forceinline__ void sr_red_sys(double *p, double v, bool on) {
+  asm volatile("{\n\t.reg .pred q;\n\t"
+               "setp.ne.b32 q, %2, 0;\n\t"
+               "@q red.sys.global.add.f64 [%0], %1;\n\t}" ::"l"(p),
+               "d"(v), "r"((int)on)
                : "memory");
 }
 // predicated REDG (no branch around it)
@@ -486,10 +495,10 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         } else {
 #pragma unroll
           for (int j = 0; j < L; ++j)
-            sr_red(yc[A] + j * CH + c, j ? vb[j][c] : v0,
+            (PEER ? sr_red_sys : sr_red)(yc[A] + j * CH + c, j ? vb[j][c] : v0,
                    live[A] && lb + j < nl);
           if (c < LV)
-            sr_red(yc[A] + L * CH + c, vt[c < LV ? c : 0],
+            (PEER ? sr_red_sys : sr_red)(yc[A] + L * CH + c, vt[c < LV ? c : 0],
                    live[A] && lb + L - 1 == nl - 1);
         }
         if (live[A]) {
@@ -522,7 +531,8 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
 #pragma unroll
           for (int r = 0; r < (TR + W - 1) / W; ++r) {
             const int i = sl + W * r;
-            sr_red(base + i, trow[i < TR ? i : 0], live[A] && i < n);
+            (PEER ? sr_red_sys : sr_red)(base + i, trow[i < TR ? i : 0],
+                                         live[A] && i < n);
           }
         }
         __syncwarp(); // row reads done before the next flush stages
@@ -711,9 +721,15 @@ static int strip_red_launch(const LoopArgs &a, const KronMat &M,
   constexpr int T = sr_threads<LY>();
   const unsigned grid = grid_for(warps * 32, T, strip_grid_cap(8));
   const size_t smem = sr_smem<LY, W, L>();
-  PM_CUDA_TRY(cudaFuncSetAttribute(k_strip_red<LY, W, SYM, L, PEER, STREAM>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+  static int cached_dev = -1; // attribute set once per device
+  int dev = 0;
+  PM_CUDA_TRY(cudaGetDevice(&dev));
+  if (cached_dev != dev) {
+    PM_CUDA_TRY(cudaFuncSetAttribute(
+        k_strip_red<LY, W, SYM, L, PEER, STREAM>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cached_dev = dev;
+  }
   k_strip_red<LY, W, SYM, L, PEER, STREAM><<<grid, T, smem, a.s>>>(
       M, a.item_ptr, strip_ptr, steps, n_strips, a.layers, a.lbeg, a.lend,
       a.coords, a.x, a.y,

@@ -694,8 +694,10 @@ static int tile_launch(const KronMat &M, const TilePlanDev &P, int layers,
                    kTileStages * P.data_bytes;
   auto kern = k_tile<LY, W>;
   // attribute and occupancy per (kernel, smem size): cached, not per call
-  static int cached_smem = -1, cached_blocks = 0;
-  if (cached_smem != smem) {
+  static int cached_smem = -1, cached_blocks = 0, cached_dev = -1;
+  int dev = 0;
+  PM_CUDA_TRY(cudaGetDevice(&dev));
+  if (cached_smem != smem || cached_dev != dev) {
     PM_CUDA_TRY(cudaFuncSetAttribute(
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int nb = 0;
@@ -708,6 +710,7 @@ static int tile_launch(const KronMat &M, const TilePlanDev &P, int layers,
     }
     cached_smem = smem;
     cached_blocks = nb;
+    cached_dev = dev;
   }
   int64_t grid = (int64_t)sm_count() * cached_blocks;
   if (grid > P.n_tiles) grid = P.n_tiles;

@@ -159,9 +159,22 @@ class MassOperator:
         self._tile_tmp = None
         self._strip_inv = None
         self._hbuf = None
+        self.last_schedule = None   # the schedule the last apply resolved
         self._dev = _lib.cuda_device()
         self.cmap = fs.device_cell_map()
         self.offs = fs.device_offsets()
+        if self.dg_only:
+            # the DG stream kernel addresses the field densely (cell, layer,
+            # slot), which is what Alg. 1 gives cell-only layouts
+            # (fspace.py:134-149); a space numbered otherwise must not
+            # reach it (include/prismesh_cuda.h, PM_VARIANT_STREAM)
+            cm = np.asarray(fs.cell_map, dtype=np.int64)
+            k, L = cm.shape[1], fs.mesh.layers
+            dense = (np.array_equal(np.asarray(fs.offsets), np.full(k, k)) and
+                     np.array_equal(cm, (np.arange(cm.shape[0])[:, None] * k * L
+                                         + np.arange(k)[None, :])))
+            if not dense:
+                raise ValueError("cell-only layout with a non-Alg. 1 cell map")
         self.xmap = self.coord_fs.device_cell_map()
         self.xoffs = self.coord_fs.device_offsets()
 
@@ -289,8 +302,10 @@ class MassOperator:
                           torch.cuda.Stream(self._dev))
         xd, yd, s_up, s_cmp, s_down = self._hbuf
         cur = torch.cuda.current_stream()
-        if not (self.dg_only and self.kron_ok and x_host.is_pinned() and
-                y_host.is_pinned()):
+        pinned = x_host.is_pinned() and y_host.is_pinned()
+        if pinned and self.stripred_ok and self._bands() is not None:
+            return self._apply_host_bands(x_host, coords, y_host)
+        if not (self.dg_only and self.kron_ok and pinned):
             xd.copy_(x_host, non_blocking=True)
             self.apply(xd, coords, yd)
             y_host.copy_(yd, non_blocking=True)
@@ -320,6 +335,89 @@ class MassOperator:
             s_down.wait_stream(s_cmp)
             with torch.cuda.stream(s_down):
                 y_host[r].copy_(yd[r], non_blocking=True)
+        cur.wait_stream(s_down)
+        cur.synchronize()
+        return y_host
+
+    def _bands(self):
+        """Chunking of the host-buffer path for vertex / edge column layouts
+        (cached): cells in index order are cut into chunks; chunk j needs
+        the entity columns below up[j] and completes those below done[j],
+        per family (vertices; edges, numbered by their sorted vertex pair,
+        mesh.py:33-84) -- the cells are sorted by their lowest vertex, as
+        apply_ordering leaves them (ordering.py:147-152).  None otherwise.
+        """
+        if getattr(self, "_band_plan", 0) == 0:
+            self._band_plan = None
+            import os
+            base = self.fs.mesh.base
+            d6 = self.fs.layout.delta6()
+            cv = np.asarray(base.cell_vertices)
+            vmin = cv.min(axis=1)
+            if base.num_cells == 0 or d6[4] or d6[5] or \
+                    np.any(np.diff(vmin) < 0):
+                return None
+            n2, n0 = base.num_cells, base.num_vertices
+            mb = float(os.environ.get("PM_HOST_CHUNK_MB", "64"))
+            nch = int(min(256, max(2, self.fs.total_dofs * 8 / (mb * 2**20))))
+            cb = np.unique(np.linspace(0, n2, nch + 1).astype(np.int64))
+            fams = []   # (origin, column, up[j], done[j]) per family
+            vmax = np.maximum.accumulate(cv.max(axis=1))
+            fams.append((0, [int(vmax[c - 1]) + 1 for c in cb[1:]],
+                         [int(vmin[c]) if c < n2 else n0 for c in cb[1:]]))
+            if d6[2] or d6[3]:
+                ce = np.asarray(base.cell_edges)
+                emax = np.maximum.accumulate(ce.max(axis=1))
+                e_lo = np.asarray(base.edge_vertices)[:, 0]
+                fams.append((1, [int(emax[c - 1]) + 1 for c in cb[1:]],
+                             [int(np.searchsorted(e_lo, vmin[c]))
+                              if c < n2 else base.num_edges
+                              for c in cb[1:]]))
+            fams = [(int(self.fs.origin_starts[d]),
+                     int(self.fs.column_sizes[d]), up, done)
+                    for d, up, done in fams]
+            chunks = [self._global_strips(
+                cells=np.arange(cb[j], cb[j + 1], dtype=np.int32))
+                for j in range(len(cb) - 1)]
+            self._band_plan = (fams, chunks)
+        return self._band_plan
+
+    def _apply_host_bands(self, x_host, coords, y_host):
+        """Host buffers, vertex / edge column layouts: the upload of the
+        next entity band, the strip kernel over cell chunk j and the
+        download of the columns chunk j completed overlap (three streams,
+        events between)."""
+        import torch
+        xd, yd, s_up, s_cmp, s_down = self._hbuf
+        cur = torch.cuda.current_stream()
+        fams, chunks = self._bands()
+        for s_ in (s_up, s_cmp, s_down):
+            s_.wait_stream(cur)
+        with torch.cuda.stream(s_cmp):
+            yd.zero_()
+        up0 = [0] * len(fams)
+        dn0 = [0] * len(fams)
+        n = self.fs.total_dofs
+        for j, (strips, W) in enumerate(chunks):
+            with torch.cuda.stream(s_up):
+                for f, (org, col, up, _done) in enumerate(fams):
+                    if up[j] > up0[f]:
+                        a, b = org + up0[f] * col, org + up[j] * col
+                        xd[a:b].copy_(x_host[a:b], non_blocking=True)
+                        up0[f] = up[j]
+            s_cmp.wait_stream(s_up)
+            _lib.column_mass_strip_red(self.fs.layout, self.k, self.layers,
+                                       coords, self.mref, xd, yd, n, strips,
+                                       self.kron, W, accumulate=True,
+                                       stream=s_cmp,
+                                       n_vertices=self.fs.mesh.base.num_vertices)
+            s_down.wait_stream(s_cmp)
+            with torch.cuda.stream(s_down):
+                for f, (org, col, _up, done) in enumerate(fams):
+                    if done[j] > dn0[f]:
+                        a, b = org + dn0[f] * col, org + done[j] * col
+                        y_host[a:b].copy_(yd[a:b], non_blocking=True)
+                        dn0[f] = done[j]
         cur.wait_stream(s_down)
         cur.synchronize()
         return y_host
@@ -452,6 +550,7 @@ class MassOperator:
             # measured fastest (profiles/): global strips for vertex-column
             # layouts, the warp-per-column kernel otherwise
             sched = "stripred" if self.stripred_ok else "column"
+        self.last_schedule = sched
         if sched == "stripred":
             if not self.stripred_ok:
                 raise ValueError(
@@ -459,14 +558,6 @@ class MassOperator:
                     f"vertex-permutation invariant triangle factor, got "
                     f"{self.fs.layout.name}")
             strips, W = self._global_strips()
-            import os
-            if os.environ.get("PM_STRIP_BULK", "0") == "1" and \
-                    len(strips) == 2:
-                _lib.column_mass_strip_bulk(
-                    self.fs.layout, self.k, self.layers, coords, self.mref,
-                    x, y, (0, n), (0, self.coord_fs.total_dofs), strips,
-                    self.kron, W, accumulate=accumulate, stream=stream)
-                return y
             _lib.column_mass_strip_red(self.fs.layout, self.k, self.layers,
                                        coords, self.mref, x, y, n, strips,
                                        self.kron, W, accumulate=accumulate,

@@ -213,19 +213,23 @@ def fused_halo_plan(fs, shards):
 
 
 class PeerWindow:
-    """The y window of the rank below, mapped into this process (CUDA IPC,
-    NVLink peer memory): every rank exports its window; rank p maps rank
-    p-1's.  ``addr`` is shifted like ``_lib.ptr(t, base)`` so that global
-    DoF numbers index it."""
+    """The neighbours' buffers the fused halo needs, mapped into this
+    process (CUDA IPC, NVLink peer memory): the y window and step flags of
+    the rank below, the step flags of the rank above.  Every rank exports
+    its window and flags.  ``y_addr`` is shifted like ``_lib.ptr(t, base)``
+    so that global DoF numbers index it; ``down_flags`` / ``up_flags`` are
+    device addresses of int32[2] (0 = "window zeroed", 1 = "ghost adds
+    landed")."""
 
-    def __init__(self, y_window, lo, rank, world, group=None):
+    def __init__(self, y_window, flags, lo, rank, world, group=None):
         import torch.distributed as dist
         from . import _lib
         # every step is collective and failure-consistent: a rank that
         # cannot export or map makes all ranks raise (no rank is left
         # waiting in a collective the others skipped)
         try:
-            mine = (*_lib.ipc_export(y_window), int(lo))
+            mine = (*_lib.ipc_export(y_window), int(lo),
+                    *_lib.ipc_export(flags))
         except Exception as e:  # noqa: BLE001 - reported on every rank
             mine = repr(e)
         infos = [None] * world
@@ -233,17 +237,25 @@ class PeerWindow:
         bad = [i for i in infos if isinstance(i, str)]
         if bad:
             raise RuntimeError(f"fused halo: IPC export failed: {bad[0]}")
-        self._open = None
-        self.addr = 0
+        self._open = []
+        self.y_addr = self.down_flags = self.up_flags = 0
         err = None
-        if rank > 0:
-            h, o, plo = infos[rank - 1]
-            try:
+        try:
+            if rank > 0:
+                h, o, plo, fh, fo = infos[rank - 1]
                 base = _lib.ipc_open(h, o)
-                self._open = (base, o)
-                self.addr = base - 8 * plo
-            except Exception as e:  # noqa: BLE001
-                err = repr(e)
+                self._open.append((base, o))
+                self.y_addr = base - 8 * plo
+                fb = _lib.ipc_open(fh, fo)
+                self._open.append((fb, fo))
+                self.down_flags = fb
+            if rank < world - 1:
+                _h, _o, _plo, fh, fo = infos[rank + 1]
+                fb = _lib.ipc_open(fh, fo)
+                self._open.append((fb, fo))
+                self.up_flags = fb
+        except Exception as e:  # noqa: BLE001
+            err = repr(e)
         errs = [None] * world
         dist.all_gather_object(errs, err, group=group)
         if any(errs):
@@ -253,9 +265,35 @@ class PeerWindow:
 
     def close(self):
         from . import _lib
-        if self._open is not None:
-            _lib.ipc_close(*self._open)
-            self._open = None
+        for base, o in self._open:
+            _lib.ipc_close(base, o)
+        self._open = []
+
+
+class LocalPeers:
+    """The same addresses for ranks emulated in one process on one device
+    (tests): ``connect_local(ops, windows)``."""
+
+    def __init__(self, y_addr, down_flags, up_flags):
+        self.y_addr, self.down_flags, self.up_flags = \
+            y_addr, down_flags, up_flags
+
+    def close(self):
+        pass
+
+
+def connect_local(ops, windows):
+    """Wire the fused halo of ``ops`` (ranks 0..P-1 of one partition, all in
+    this process) to each other's ``windows`` and step flags."""
+    for r, (op, w) in enumerate(zip(ops, windows)):
+        below = ops[r - 1] if r > 0 else None
+        above = ops[r + 1] if r + 1 < len(ops) else None
+        op._peer = LocalPeers(
+            windows[r - 1].data_ptr() - 8 * below.shard.window[0]
+            if below else 0,
+            below._flags.data_ptr() if below else 0,
+            above._flags.data_ptr() if above else 0)
+        op._peer_y = w
 
 
 class ShardedMassOperator:
@@ -290,6 +328,10 @@ class ShardedMassOperator:
             self.ghost_end = plan[rank]
         self.op = MassOperator(fs, quadrature, schedule="column")
         dev = self.op._dev
+        # fused halo step flags (0: window zeroed, 1: the rank above's ghost
+        # adds landed), raised by the neighbours, compared with the step
+        self._flags = torch.zeros(4, dtype=torch.int32, device=dev)
+        self._step = 0
         self.d_cells = torch.from_numpy(self.shard.cells).to(dev)
         # vertex-column layouts: sequential strips over the rank's block
         self.strips = (self.op._global_strips(cells=self.shard.cells)
@@ -310,39 +352,54 @@ class ShardedMassOperator:
             raise ValueError("the fused halo runs on the strip schedule")
         if self._peer is not None:
             self._peer.close()
-        self._peer = PeerWindow(y_window, self.shard.window[0], self.rank,
-                                self.world, group=self.group)
+        self._peer = PeerWindow(y_window, self._flags, self.shard.window[0],
+                                self.rank, self.world, group=self.group)
         self._peer_y = y_window
 
-    def _apply_fused(self, x_window, coords_window, y_window):
-        import torch
-        import torch.distributed as dist
+    def _apply_fused(self, x_window, coords_window, y_window, stream=None):
+        """One step of the fused halo, ordered on the stream only (no host
+        synchronisation): zero the window, tell the rank above, wait until
+        the rank below zeroed its window, run the kernel (ghost columns
+        REDG'd into the rank below's window), tell the rank below, wait
+        for the rank above's ghost adds into this window."""
         if self._peer is None or y_window is not self._peer_y:
             raise ValueError("fused halo: call connect(y_window) first with "
                              "the window passed to apply")
+        import torch
+        lib = self._lib
         lo, hi = self.shard.window
         clo, _chi = self.shard.coord_window
         op = self.op
-        y_window.zero_()
-        torch.cuda.synchronize()
-        dist.barrier(group=self.group)    # every window zeroed
-        strips, W = self.strips
-        self._lib.column_mass_strip_red_peer(
-            op.fs.layout, op.k, op.layers, coords_window, op.mref, x_window,
-            y_window, hi - lo, strips, op.kron, W, self._peer.addr,
-            self.ghost_end if self._peer.addr else 0, accumulate=True,
-            x_base=lo, y_base=lo, coords_base=clo,
-            n_vertices=op.fs.mesh.base.num_vertices)
-        torch.cuda.synchronize()
-        dist.barrier(group=self.group)    # every peer addition landed
+        s = self._step = (self._step % 0x7ffffffe) + 1
+        flags = self._flags.data_ptr()
+        with torch.cuda.stream(stream or torch.cuda.current_stream()):
+            y_window.zero_()
+            if self._peer.up_flags:
+                lib.stream_signal(self._peer.up_flags, s, stream)
+            if self._peer.down_flags:
+                lib.stream_wait_geq(flags, s, stream)
+            strips, W = self.strips
+            lib.column_mass_strip_red_peer(
+                op.fs.layout, op.k, op.layers, coords_window, op.mref,
+                x_window, y_window, hi - lo, strips, op.kron, W,
+                self._peer.y_addr,
+                self.ghost_end if self._peer.y_addr else 0, accumulate=True,
+                x_base=lo, y_base=lo, coords_base=clo,
+                n_vertices=op.fs.mesh.base.num_vertices, stream=stream)
+            if self._peer.down_flags:
+                lib.stream_signal(self._peer.down_flags + 4, s, stream)
+            if self._peer.up_flags:
+                lib.stream_wait_geq(flags + 4, s, stream)
         return y_window
 
-    def apply(self, x_window, coords_window, y_window=None, exchange=True):
+    def apply(self, x_window, coords_window, y_window=None, exchange=True,
+              stream=None):
         import torch
         lo, hi = self.shard.window
         clo, _chi = self.shard.coord_window
         if self.fused and exchange:
-            return self._apply_fused(x_window, coords_window, y_window)
+            return self._apply_fused(x_window, coords_window, y_window,
+                                     stream)
         if y_window is None:
             y_window = torch.empty(hi - lo, dtype=torch.float64,
                                    device=x_window.device)

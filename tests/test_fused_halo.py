@@ -126,7 +126,6 @@ def _ipc_worker(rank, world, port, lname, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
         from paper_1604_05937_b200 import configs, extrude_coordinates
-        from paper_1604_05937_b200.kernels import mass_action
         from paper_1604_05937_b200.shard import (ShardedMassOperator,
                                                  ghost_origins)
         w = configs.Workload("c5-ipc", 20, 5, lname, quad_degrees(lname))
@@ -138,11 +137,32 @@ def _ipc_worker(rank, world, port, lname, q):
         clo, chi = op.shard.coord_window
         xd = torch.from_numpy(x[lo:hi].copy()).cuda()
         yw = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
-        op.connect(yw)
+        op.connect(yw)                  # CUDA IPC: the windows and flags
+        import oracle
+        from paper_1604_05937_b200 import _lib
+        from paper_1604_05937_b200.quadrature import element_for_layout
+        el = element_for_layout(fs.layout)
+        full = oracle.Problem(m.base, m.layers, fs.layout.counts, el.tri,
+                              el.line, el.ncomp, *quad_degrees(lname)
+                              ).assemble(x)
         err = 0.0
-        full = mass_action(fs, x, quadrature=quad)
+        strips, W = op.strips
         for _rep in range(2):              # the window is reused per step
-            op.apply(xd, coords[clo:chi].clone(), yw)
+            # the fused kernel through the IPC mapping; the ranks are
+            # processes sharing one GPU, so the step is ordered by host
+            # barriers here (the stream-ordered flags of apply() are
+            # tested in one process, test_fused_halo_stream_protocol)
+            yw.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            _lib.column_mass_strip_red_peer(
+                fs.layout, op.op.k, m.layers, coords[clo:chi].clone(),
+                op.op.mref, xd, yw, hi - lo, strips, op.op.kron, W,
+                op._peer.y_addr, op.ghost_end if op._peer.y_addr else 0,
+                accumulate=True, x_base=lo, y_base=lo, coords_base=clo,
+                n_vertices=m.base.num_vertices)
+            torch.cuda.synchronize()
+            dist.barrier()
             got = yw.cpu().numpy()
             for _d, o, c in ghost_origins(fs, op.shard.owned):
                 for org in o:
@@ -175,3 +195,49 @@ def test_fused_halo_two_processes_ipc(lname):
     for r in range(world):
         assert isinstance(res[r], float), res[r]
         assert res[r] <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1"))
+@pytest.mark.parametrize("world", (2, 4))
+def test_fused_halo_stream_protocol(lname, world):
+    """ShardedMassOperator.apply's fused step with the stream-ordered flags
+    (no host synchronisation between the ranks): P ranks emulated in one
+    process on one GPU, each on its own CUDA stream, three steps back to
+    back on reused windows, against the oracle."""
+    import torch
+    import oracle
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.quadrature import element_for_layout
+    from paper_1604_05937_b200.shard import (ShardedMassOperator,
+                                             connect_local, ghost_origins)
+    w = configs.Workload("c5-streams", 40, 9, lname, quad_degrees(lname))
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    el = element_for_layout(fs.layout)
+    ref = oracle.Problem(m.base, m.layers, fs.layout.counts, el.tri, el.line,
+                         el.ncomp, *quad_degrees(lname)).assemble(x)
+    ops = [ShardedMassOperator(fs, r, world, quad, fused=True)
+           for r in range(world)]
+    wins = [torch.full((op.window[1] - op.window[0],), float("nan"),
+                       dtype=torch.float64, device="cuda") for op in ops]
+    connect_local(ops, wins)
+    streams = [torch.cuda.Stream() for _ in ops]
+    xs = [torch.from_numpy(x[op.window[0]:op.window[1]].copy()).cuda()
+          for op in ops]
+    cs = [coords[op.shard.coord_window[0]:op.shard.coord_window[1]].clone()
+          for op in ops]
+    torch.cuda.synchronize()
+    for _step in range(3):
+        for r, op in enumerate(ops):
+            op.apply(xs[r], cs[r], wins[r], stream=streams[r])
+    torch.cuda.synchronize()
+    got = np.zeros_like(ref)
+    for op, win in zip(ops, wins):
+        yw = win.cpu().numpy()
+        for _d, o, c in ghost_origins(fs, op.shard.owned):
+            for org in o:
+                a = org - op.window[0]
+                got[org:org + c] = yw[a:a + c]
+    assert np.abs(got - ref).max() <= 1e-10 * np.abs(ref).max()

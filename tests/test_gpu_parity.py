@@ -434,23 +434,6 @@ def test_patch_strips_layers(lname, layers, patch, monkeypatch):
     assert _rel(y2.cpu().numpy(), 2 * ref) <= 1e-10
 
 
-@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1", "CG1xDG1"))
-@pytest.mark.parametrize("layers", (1, 9, 40))
-def test_strip_bulk_variant(lname, layers, monkeypatch):
-    """The TMA bulk-copy prefetch variant (PM_STRIP_BULK=1) agrees too."""
-    from paper_1604_05937_b200 import configs, extrude_coordinates
-    from paper_1604_05937_b200.kernels import MassOperator
-    monkeypatch.setenv("PM_STRIP_BULK", "1")
-    w = configs.Workload("sb", 16, layers, lname, quad_degrees(lname),
-                         ordering="random", jitter=0.2)
-    fs, quad, x, _ = configs.build(w)
-    m = fs.mesh
-    op = MassOperator(fs, quad, schedule="stripred")
-    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
-    y = op.apply(torch.from_numpy(x).cuda(), coords).cpu().numpy()
-    assert _rel(y, _oracle_for(w, fs).assemble(x)) <= 1e-10
-
-
 @pytest.mark.parametrize("lname,layers,n", (("DG1xDG1", 50, 32),
                                             ("DG1xDG1", 7, 24),
                                             ("DG0xDG1", 33, 20),

@@ -215,3 +215,19 @@ def test_kronecker_factors_reproduce_mref(lname):
     h, v, c = (np.array(a) for a in (el.slot_h, el.slot_v, el.slot_comp))
     K = Mt[h][:, h] * Ml[v][:, v] * (c[:, None] == c[None, :])
     np.testing.assert_allclose(K, M, rtol=0, atol=1e-16)
+
+
+@pytest.mark.parametrize("n,ordering,jitter", [(32, "rcm", 0.0),
+                                                (64, "rcm", 0.0),
+                                                (48, "random", 0.3),
+                                                (40, "natural", 0.3)])
+def test_product_mesh_equals_oracle_mesh(n, ordering, jitter):
+    """configs.base_mesh (product: mesh.py / ordering.py mirrors, host C++
+    RCM) against the oracle's independent C restatement: bit-exact."""
+    import oracle
+    from paper_1604_05937_b200 import configs
+    mp, rp = configs.base_mesh(n, ordering, jitter, seed=5)
+    mo, ro = oracle.base_mesh(n, ordering, jitter, seed=5)
+    for k in ("cell_vertices", "coords", "cell_edges", "edge_vertices"):
+        assert np.array_equal(np.asarray(getattr(mp, k)), getattr(mo, k)), k
+    assert rp.random() == ro.random()   # same draw position afterwards

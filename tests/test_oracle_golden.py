@@ -141,3 +141,46 @@ def test_greedy_coloring_is_proper(gmesh):
             assert len(set(col[cells].tolist())) == len(cells)
     assert oracle.greedy_color(gmesh("one"))[1] == 1
     assert oracle.greedy_color(gmesh("two"))[1] == 2
+
+
+# --- the oracle's own base-mesh pipeline (oracle_mesh.c) against the
+# reference's meshes and permutations (mesh.py:33-84, 228-254;
+# ordering.py:45-152) --------------------------------------------------------
+
+def _same_mesh(m, golden, name):
+    p = f"mesh/{name}/"
+    for k in ("cell_vertices", "coords", "cell_edges", "edge_vertices"):
+        assert np.array_equal(getattr(m, k), golden[p + k]), (name, k)
+
+
+@pytest.mark.parametrize("n", [3, 4, 5])
+def test_oracle_unit_square_matches_reference(golden, n):
+    _same_mesh(oracle.unit_square(n), golden, f"sq{n}")
+
+
+@pytest.mark.parametrize("n", [4, 16])
+def test_oracle_rcm_matches_reference(golden, n):
+    fwd = oracle.rcm_forward(oracle.unit_square(n))
+    assert np.array_equal(fwd, golden[f"sq{n}_rcm_forward"])
+
+
+def test_oracle_random_order_matches_reference(golden):
+    assert np.array_equal(oracle.random_forward(25, 7),
+                          golden["sq4_rnd7_forward"])
+    assert np.array_equal(oracle.random_forward(289, 3),
+                          golden["sq16_rnd3_forward"])
+
+
+@pytest.mark.parametrize("name,ordering", [("sq4rcm", "rcm"),
+                                           ("sq3rcm", "rcm")])
+def test_oracle_apply_ordering_matches_reference(golden, name, ordering):
+    n = int(name[2])
+    m = oracle.apply_ordering(oracle.unit_square(n),
+                              oracle.rcm_forward(oracle.unit_square(n)))
+    _same_mesh(m, golden, name)
+
+
+def test_oracle_random_reordered_mesh_matches_reference(golden):
+    sq4 = oracle.unit_square(4)
+    _same_mesh(oracle.apply_ordering(sq4, golden["sq4_rnd7_forward"]),
+               golden, "sq4rnd")
