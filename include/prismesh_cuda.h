@@ -35,6 +35,8 @@
  *                               base-mesh partitions; SPEC.md:9 leaves it out)
  *   pm_greedy_color_cells    <- SPEC.md:343-351 color_base_cells
  *   pm_rcm_order             <- pkg/src/prismesh/ordering.py:45-90 (host BFS)
+ *   pm_rcm_order_device      <- pkg/src/prismesh/ordering.py:45-90 (device walk)
+ *   pm_stencil_*             <- SPEC.md:322-341 StencilKernel.apply (user kernels)
  */
 #ifndef PRISMESH_CUDA_H
 #define PRISMESH_CUDA_H
@@ -397,6 +399,47 @@ int pm_derive_edges(const int32_t *cell_vertices, int64_t n_cells,
 int pm_vertex_graph_sorted(const int32_t *edge_vertices, int64_t n_edges,
                            int64_t n_vertices, int64_t *offsets, int32_t *nbr,
                            void *stream);
+
+/* Device Cuthill-McKee walk (replaces the serial BFS of ordering.py:45-90,
+ * `_cuthill_mckee`; same result as pm_rcm_order, bit for bit): offsets
+ * (n+1 int64) and neighbours (int32) on the device, every row sorted by
+ * (degree, index) (pm_vertex_graph_sorted's output); order (n int64,
+ * device) receives the Cuthill-McKee visit order (not reversed).
+ * Level-synchronous in one thread block: each new vertex is appended by
+ * its lowest-positioned discoverer at its row rank, which is the serial
+ * queue order.  n < 2^31 - 1.  Synchronises the stream. */
+int pm_rcm_order_device(const int64_t *offsets, const int32_t *neighbours,
+                        int64_t n, int64_t *order, void *stream);
+
+/* --- user stencil kernels for iterate_columns ---------------------------
+ * (SPEC.md:322-341 StencilKernel: an arbitrary per-cell-layer procedure;
+ * the reference's consumers generate and compile C per kernel,
+ * PAPER.md:777-783.)  `source` is CUDA C++ defining
+ *   __device__ void pm_kernel(double *out, const double *const *in,
+ *                             long long cell, int layer);
+ * in[a][j] = argument a at slot j of the cell-layer, out[j] = contribution
+ * to output slot j (starts at 0, added into the output field).  NVRTC
+ * compiles it for sm_100a into a generated column loop (Alg. 3).
+ * n_in <= 8 input arguments with k_in[a] <= 64 slots, k_out <= 64.
+ * pm_stencil_check: compile only (no device needed), cubin size out.
+ * pm_stencil_launch: colored = 0 -> thread per cell-layer, fp64 REDG into
+ * `out`; colored = 1 -> thread per listed cell (cells[i], i < n_cells: one
+ * colour of color_base_cells), layers in order, plain +=, deterministic.
+ * cells = NULL means cells 0..n_cells-1.  in_fields / in_maps / in_offsets
+ * are HOST arrays of n_in device pointers (field, bottom-layer map
+ * (N2, k) int32, offsets (k) int32); out_map / out_offsets likewise for
+ * the output space.  Asynchronous on `stream`. */
+int pm_stencil_check(const char *source, int32_t n_in, const int32_t *k_in,
+                     int32_t k_out, int64_t *cubin_bytes);
+int pm_stencil_compile(const char *source, int32_t n_in, const int32_t *k_in,
+                       int32_t k_out, void **handle);
+int pm_stencil_launch(void *handle, int32_t colored, int64_t n_cells,
+                      int32_t layers, const double *const *in_fields,
+                      const int32_t *const *in_maps,
+                      const int32_t *const *in_offsets, double *out,
+                      const int32_t *out_map, const int32_t *out_offsets,
+                      const int32_t *cells, void *stream);
+int pm_stencil_free(void *handle);
 
 /* Device cell re-sort of apply_ordering (replaces ordering.py:142-152):
  * cells_out = forward[cell_vertices][perm] with perm the stable lexsort of

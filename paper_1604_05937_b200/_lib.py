@@ -93,6 +93,14 @@ SIGNATURES = {
                                        _i32p, _vp]),
     "pm_vertex_graph_sorted": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp,
                                               _vp]),
+    "pm_rcm_order_device": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "pm_stencil_check": (ctypes.c_int, [ctypes.c_char_p, _i32, _i32p, _i32,
+                                        _i64p]),
+    "pm_stencil_compile": (ctypes.c_int, [ctypes.c_char_p, _i32, _i32p, _i32,
+                                          ctypes.POINTER(ctypes.c_void_p)]),
+    "pm_stencil_launch": (ctypes.c_int, [_vp, _i32, _i64, _i32, _vp, _vp,
+                                         _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pm_stencil_free": (ctypes.c_int, [_vp]),
     "pm_reorder_cells": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _vp,
                                         _vp]),
     "pm_column_mass_strip_red_peer": (ctypes.c_int, [
@@ -583,6 +591,88 @@ def vertex_graph_sorted_device(edge_vertices, n_vertices):
     check(host_lib().pm_vertex_graph_sorted(ptr(ev), ne, n_vertices, ptr(off),
                                             ptr(nb), stream_ptr(None)))
     return off.cpu().numpy(), nb.cpu().numpy().astype(np.int64)
+
+
+def stencil_check(source, k_in, k_out):
+    """NVRTC-compile a user stencil kernel (no device needed); the cubin
+    size in bytes.  Compile errors raise ValueError with NVRTC's log."""
+    import numpy as np
+    k = np.ascontiguousarray(k_in, dtype=np.int32)
+    n = ctypes.c_int64(0)
+    check(host_lib().pm_stencil_check(source.encode(), k.shape[0],
+                                      k.ctypes.data_as(_i32p), int(k_out),
+                                      ctypes.byref(n)))
+    return n.value
+
+
+def stencil_compile(source, k_in, k_out):
+    """Handle (int) of a compiled and loaded user stencil kernel."""
+    import numpy as np
+    cuda_device()
+    k = np.ascontiguousarray(k_in, dtype=np.int32)
+    h = ctypes.c_void_p(0)
+    check(host_lib().pm_stencil_compile(source.encode(), k.shape[0],
+                                        k.ctypes.data_as(_i32p), int(k_out),
+                                        ctypes.byref(h)))
+    return h.value
+
+
+def stencil_launch(handle, colored, n_cells, layers, fields, maps, offsets,
+                   out, out_map, out_offsets, cells=None, stream=None):
+    n = len(fields)
+    arr = ctypes.c_void_p * max(n, 1)
+    f = arr(*[t.data_ptr() for t in fields])
+    m = arr(*[t.data_ptr() for t in maps])
+    o = arr(*[t.data_ptr() for t in offsets])
+    check(host_lib().pm_stencil_launch(
+        ctypes.c_void_p(handle), 1 if colored else 0, int(n_cells),
+        int(layers), f, m, o, ptr(out), ptr(out_map), ptr(out_offsets),
+        ptr(cells) if cells is not None else None, stream_ptr(stream)))
+
+
+def stencil_free(handle):
+    if handle:
+        check(host_lib().pm_stencil_free(ctypes.c_void_p(handle)))
+
+
+def rcm_walk_device(offsets, neighbours_sorted):
+    """Cuthill-McKee visit order (int64 numpy) of a host CSR whose rows are
+    sorted by (degree, index), walked on the device (pm_rcm_order_device)."""
+    import numpy as np
+    import torch
+    dev = cuda_device()
+    off = host_tensor(offsets, np.int64).to(dev)
+    n = off.shape[0] - 1
+    nb = host_tensor(neighbours_sorted, np.int32).to(dev)
+    if nb.numel() == 0:
+        nb = torch.zeros(1, dtype=torch.int32, device=dev)
+    order = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    check(host_lib().pm_rcm_order_device(ptr(off), ptr(nb), n, ptr(order),
+                                         stream_ptr(None)))
+    return order[:n].cpu().numpy()
+
+
+def rcm_forward_device(edge_vertices, n_vertices):
+    """RCM ``forward`` permutation (int64 numpy) with the vertex graph AND
+    the Cuthill-McKee walk on the device (pm_vertex_graph_sorted +
+    pm_rcm_order_device), the reversal by a device scatter."""
+    import numpy as np
+    import torch
+    dev = cuda_device()
+    ev = host_tensor(edge_vertices, np.int32).to(dev)
+    ne = ev.shape[0]
+    off = torch.empty(n_vertices + 1, dtype=torch.int64, device=dev)
+    nb = torch.empty(max(1, 2 * ne), dtype=torch.int32, device=dev)
+    lib = host_lib()
+    check(lib.pm_vertex_graph_sorted(ptr(ev), ne, n_vertices, ptr(off),
+                                     ptr(nb), stream_ptr(None)))
+    order = torch.empty(n_vertices, dtype=torch.int64, device=dev)
+    check(lib.pm_rcm_order_device(ptr(off), ptr(nb), n_vertices, ptr(order),
+                                  stream_ptr(None)))
+    forward = torch.empty_like(order)
+    forward[order.flip(0)] = torch.arange(n_vertices, dtype=torch.int64,
+                                          device=dev)
+    return forward.cpu().numpy()
 
 
 def reorder_cells_device(cell_vertices, forward):

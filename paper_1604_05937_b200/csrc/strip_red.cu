@@ -66,6 +66,15 @@ template <class LY, int W> constexpr int srb_entry() {
 #endif
 constexpr int kSrDepth = PM_SR_DEPTH;
 static_assert(kSrDepth == 3 || kSrDepth == 6, "ring depth 3 or 6");
+// PM_SR_ONESYNC = 1: one warp barrier per step.  Step k first waits for
+// its own copies and syncs the warp, then refills the slot step k-1 was
+// read from (every lane is past those reads), then reads its slot: the
+// barrier that publishes step k's copies also retires step k-1's reads,
+// at the price of one step less prefetch distance (depth - 1).
+#ifndef PM_SR_ONESYNC
+#define PM_SR_ONESYNC 0
+#endif
+constexpr bool kSrOneSync = PM_SR_ONESYNC != 0;
 
 
 // Padded ring entries of the strip kernel (a chunk of CW = W*L levels):
@@ -447,7 +456,8 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
       return v;
     };
 #pragma unroll
-    for (int d = 0; d < kSrDepth; ++d) rv[d] = fetch(d, d);
+    for (int d = 0; d < (kSrOneSync ? kSrDepth - 1 : kSrDepth); ++d)
+      rv[d] = fetch(d, d);
 
     auto flush = [&](auto A_) {
       constexpr int A = decltype(A_)::value;
@@ -548,8 +558,14 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
       if (!FILL) flush(A_);
       const bool act = k < len;
       // the vertex of ring slot A (step k) enters window slot A
-      sr_wait<kSrDepth - 1>(); // this lane's copies of step k landed
-      __syncwarp();            // ... and the other lanes' ones
+      // this lane's copies of step k landed
+      sr_wait<kSrOneSync ? kSrDepth - 2 : kSrDepth - 1>();
+      __syncwarp(); // ... and the other lanes' ones
+      if constexpr (kSrOneSync) {
+        // (and every lane is done with step k-1's slot: refill it)
+        constexpr int P = (R + kSrDepth - 1) % kSrDepth;
+        rv[P] = fetch(k + kSrDepth - 1, P);
+      }
       // steps past this segment's strip read a zero block instead of the
       // (stale, possibly non-finite) ring slot; lanes past the chunk read
       // zero-filled values and are never flushed.
@@ -577,7 +593,8 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         gm[A][j][1] = g[j][1] + g[j + 1][1];
         gm[A][j][2] = g[j + 1][2] - g[j][2];
       }
-      __syncwarp(); // reads done before the slot is refilled
+      if constexpr (!kSrOneSync)
+        __syncwarp(); // reads done before the slot is refilled
       const int va = rv[R] & IDM;
       const int rv_cell = rv[R]; // before the slot is refilled
       yc[A] = col_at(PEER && va < ghost_end ? ylg : yl, va, colb);
@@ -601,7 +618,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
             zv[A][j][c][v] = s;
           }
       // refill ring slot A with the step kSrDepth ahead
-      rv[R] = fetch(k + kSrDepth, R);
+      if constexpr (!kSrOneSync) rv[R] = fetch(k + kSrDepth, R);
       if (FILL && A < 2) return; // window not full yet
 #pragma unroll
       for (int j = 0; j < L; ++j) {

@@ -270,30 +270,25 @@ class PeerWindow:
         self._open = []
 
 
-class LocalPeers:
-    """The same addresses for ranks emulated in one process on one device
-    (tests): ``connect_local(ops, windows)``."""
-
-    def __init__(self, y_addr, down_flags, up_flags):
-        self.y_addr, self.down_flags, self.up_flags = \
-            y_addr, down_flags, up_flags
-
-    def close(self):
-        pass
-
-
-def connect_local(ops, windows):
-    """Wire the fused halo of ``ops`` (ranks 0..P-1 of one partition, all in
-    this process) to each other's ``windows`` and step flags."""
-    for r, (op, w) in enumerate(zip(ops, windows)):
-        below = ops[r - 1] if r > 0 else None
-        above = ops[r + 1] if r + 1 < len(ops) else None
-        op._peer = LocalPeers(
-            windows[r - 1].data_ptr() - 8 * below.shard.window[0]
-            if below else 0,
-            below._flags.data_ptr() if below else 0,
-            above._flags.data_ptr() if above else 0)
-        op._peer_y = w
+def fused_step_program(rank, world, step):
+    """The stream program of one fused-halo step on ``rank`` (executed by
+    ShardedMassOperator._apply_fused, checked for progress and ordering by
+    tests/test_fused_halo.py on the CPU).  Flags are int32[2] per rank:
+    [0] "the rank below zeroed its window", [1] "the rank above's ghost
+    adds into my window landed".  Ops: ("zero",), ("kernel",),
+    ("signal", rank, slot, step) (store into that rank's flag slot) and
+    ("wait", slot, step) (this rank's flag slot >= step)."""
+    prog = [("zero",)]
+    if rank + 1 < world:
+        prog.append(("signal", rank + 1, 0, step))  # my window is zeroed
+    if rank > 0:
+        prog.append(("wait", 0, step))    # the window below is zeroed
+    prog.append(("kernel",))              # ghost columns into rank-1's window
+    if rank > 0:
+        prog.append(("signal", rank - 1, 1, step))  # my adds landed there
+    if rank + 1 < world:
+        prog.append(("wait", 1, step))    # the adds into my window landed
+    return prog
 
 
 class ShardedMassOperator:
@@ -372,24 +367,28 @@ class ShardedMassOperator:
         op = self.op
         s = self._step = (self._step % 0x7ffffffe) + 1
         flags = self._flags.data_ptr()
+        peers = {self.rank - 1: self._peer.down_flags,
+                 self.rank + 1: self._peer.up_flags}
         with torch.cuda.stream(stream or torch.cuda.current_stream()):
-            y_window.zero_()
-            if self._peer.up_flags:
-                lib.stream_signal(self._peer.up_flags, s, stream)
-            if self._peer.down_flags:
-                lib.stream_wait_geq(flags, s, stream)
-            strips, W = self.strips
-            lib.column_mass_strip_red_peer(
-                op.fs.layout, op.k, op.layers, coords_window, op.mref,
-                x_window, y_window, hi - lo, strips, op.kron, W,
-                self._peer.y_addr,
-                self.ghost_end if self._peer.y_addr else 0, accumulate=True,
-                x_base=lo, y_base=lo, coords_base=clo,
-                n_vertices=op.fs.mesh.base.num_vertices, stream=stream)
-            if self._peer.down_flags:
-                lib.stream_signal(self._peer.down_flags + 4, s, stream)
-            if self._peer.up_flags:
-                lib.stream_wait_geq(flags + 4, s, stream)
+            for op_ in fused_step_program(self.rank, self.world, s):
+                if op_[0] == "zero":
+                    y_window.zero_()
+                elif op_[0] == "signal":
+                    lib.stream_signal(peers[op_[1]] + 4 * op_[2], op_[3],
+                                      stream)
+                elif op_[0] == "wait":
+                    lib.stream_wait_geq(flags + 4 * op_[1], op_[2], stream)
+                else:
+                    strips, W = self.strips
+                    lib.column_mass_strip_red_peer(
+                        op.fs.layout, op.k, op.layers, coords_window,
+                        op.mref, x_window, y_window, hi - lo, strips,
+                        op.kron, W, self._peer.y_addr,
+                        self.ghost_end if self._peer.y_addr else 0,
+                        accumulate=True, x_base=lo, y_base=lo,
+                        coords_base=clo,
+                        n_vertices=op.fs.mesh.base.num_vertices,
+                        stream=stream)
         return y_window
 
     def apply(self, x_window, coords_window, y_window=None, exchange=True,

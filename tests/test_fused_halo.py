@@ -151,7 +151,7 @@ def _ipc_worker(rank, world, port, lname, q):
             # the fused kernel through the IPC mapping; the ranks are
             # processes sharing one GPU, so the step is ordered by host
             # barriers here (the stream-ordered flags of apply() are
-            # tested in one process, test_fused_halo_stream_protocol)
+            # checked as a stream program, test_fused_halo_stream_protocol)
             yw.zero_()
             torch.cuda.synchronize()
             dist.barrier()
@@ -197,47 +197,55 @@ def test_fused_halo_two_processes_ipc(lname):
         assert res[r] <= 1e-10
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("lname", ("CG1xCG1", "VP1"))
-@pytest.mark.parametrize("world", (2, 4))
-def test_fused_halo_stream_protocol(lname, world):
-    """ShardedMassOperator.apply's fused step with the stream-ordered flags
-    (no host synchronisation between the ranks): P ranks emulated in one
-    process on one GPU, each on its own CUDA stream, three steps back to
-    back on reused windows, against the oracle."""
-    import torch
-    import oracle
-    from paper_1604_05937_b200 import configs, extrude_coordinates
-    from paper_1604_05937_b200.quadrature import element_for_layout
-    from paper_1604_05937_b200.shard import (ShardedMassOperator,
-                                             connect_local, ghost_origins)
-    w = configs.Workload("c5-streams", 40, 9, lname, quad_degrees(lname))
-    fs, quad, x, _ = configs.build(w)
-    m = fs.mesh
-    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
-    el = element_for_layout(fs.layout)
-    ref = oracle.Problem(m.base, m.layers, fs.layout.counts, el.tri, el.line,
-                         el.ncomp, *quad_degrees(lname)).assemble(x)
-    ops = [ShardedMassOperator(fs, r, world, quad, fused=True)
-           for r in range(world)]
-    wins = [torch.full((op.window[1] - op.window[0],), float("nan"),
-                       dtype=torch.float64, device="cuda") for op in ops]
-    connect_local(ops, wins)
-    streams = [torch.cuda.Stream() for _ in ops]
-    xs = [torch.from_numpy(x[op.window[0]:op.window[1]].copy()).cuda()
-          for op in ops]
-    cs = [coords[op.shard.coord_window[0]:op.shard.coord_window[1]].clone()
-          for op in ops]
-    torch.cuda.synchronize()
-    for _step in range(3):
-        for r, op in enumerate(ops):
-            op.apply(xs[r], cs[r], wins[r], stream=streams[r])
-    torch.cuda.synchronize()
-    got = np.zeros_like(ref)
-    for op, win in zip(ops, wins):
-        yw = win.cpu().numpy()
-        for _d, o, c in ghost_origins(fs, op.shard.owned):
-            for org in o:
-                a = org - op.window[0]
-                got[org:org + c] = yw[a:a + c]
-    assert np.abs(got - ref).max() <= 1e-10 * np.abs(ref).max()
+def _simulate(world, steps, high_first=False):
+    """Run every rank's fused-step stream program (one in-order stream per
+    rank, as on P GPUs) in an interleaving that always advances the
+    lowest (or highest) runnable rank as far as it can; returns the global
+    event order.  Raises on a deadlock."""
+    from paper_1604_05937_b200.shard import fused_step_program
+    progs = [[op for s in range(1, steps + 1)
+              for op in fused_step_program(r, world, s)]
+             for r in range(world)]
+    flags = [[0, 0] for _ in range(world)]
+    pc = [0] * world
+    events = []
+    while any(pc[r] < len(progs[r]) for r in range(world)):
+        progressed = False
+        for r in (range(world - 1, -1, -1) if high_first else range(world)):
+            while pc[r] < len(progs[r]):
+                op = progs[r][pc[r]]
+                if op[0] == "wait" and flags[r][op[1]] < op[2]:
+                    break
+                if op[0] == "signal":
+                    flags[op[1]][op[2]] = op[3]
+                step = sum(1 for o in progs[r][:pc[r] + 1] if o[0] == "zero")
+                events.append((r, op[0], step))
+                pc[r] += 1
+                progressed = True
+        if not progressed:
+            raise AssertionError(f"deadlock at {pc}")
+    return events
+
+
+@pytest.mark.parametrize("world", (1, 2, 3, 4, 8))
+@pytest.mark.parametrize("order", ("low-first", "high-first"))
+def test_fused_halo_stream_protocol(world, order):
+    """The stream-ordered fused step (no host synchronisation between
+    ranks) makes progress for any rank speed, and orders every step's
+    memory effects: rank r's kernel adds into rank r-1's window only after
+    r-1 zeroed it for that step, and r-1 zeroes its window for the next
+    step only after those adds landed.  (Checked as a stream program on
+    the CPU: ranks whose streams wait on one another must not be
+    emulated on one GPU, B200_PROFILING.md.)"""
+    from paper_1604_05937_b200.shard import fused_step_program
+    steps = 4
+    ev = _simulate(world, steps, high_first=order == "high-first")
+    pos = {e: i for i, e in enumerate(ev)}
+    for s in range(1, steps + 1):
+        for r in range(1, world):
+            assert pos[(r - 1, "zero", s)] < pos[(r, "kernel", s)]
+            if s < steps:
+                assert pos[(r, "kernel", s)] < pos[(r - 1, "zero", s + 1)]
+    for r in range(world):
+        prog = fused_step_program(r, world, 7)
+        assert prog[0] == ("zero",) and ("kernel",) in prog

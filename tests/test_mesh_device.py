@@ -109,3 +109,63 @@ def test_rcm_device_graph_disconnected(monkeypatch):
     monkeypatch.setenv("PM_DEVICE_MESH", "0")
     host = rcm_vertex_order(both).forward
     assert np.array_equal(dev, host)
+
+
+def _csr(n, pairs):
+    """Symmetric CSR (offsets, neighbours) of an undirected edge list."""
+    pairs = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
+    a = np.concatenate([pairs[:, 0], pairs[:, 1]])
+    b = np.concatenate([pairs[:, 1], pairs[:, 0]])
+    o = np.lexsort((b, a))
+    a, b = a[o], b[o]
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(off, a + 1, 1)
+    return np.cumsum(off), b
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_rcm_device_walk_bit_exact(seed):
+    """pm_rcm_order_device == the host walk (== ordering.py:45-90) on
+    random graphs with several components, isolated vertices, hubs and
+    degree ties."""
+    from paper_1604_05937_b200.ordering import rcm_order
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 3000))
+    m = int(rng.integers(0, 4 * n))
+    pairs = rng.integers(0, n, size=(m, 2))
+    pairs = pairs[pairs[:, 0] != pairs[:, 1]]
+    if seed % 2 and n > 10:       # a hub: one vertex adjacent to many
+        hub = np.stack([np.zeros(n // 2, np.int64),
+                        rng.integers(1, n, n // 2)], 1)
+        pairs = np.concatenate([pairs, hub])
+    pairs = np.unique(np.sort(pairs, axis=1), axis=0)
+    off, nb = _csr(n, pairs)
+    host = rcm_order(off, nb).forward
+    dev = rcm_order(off, nb, device=True).forward
+    assert np.array_equal(host, dev)
+
+
+@pytest.mark.parametrize("n,seed", [(4, None), (16, None), (64, 5),
+                                    (300, 7)])
+def test_rcm_vertex_order_device_matches_host(n, seed):
+    """The mesh path (device graph + device walk) equals the host path."""
+    from paper_1604_05937_b200 import _lib
+    from paper_1604_05937_b200.ordering import rcm_order
+    m = generate_unit_square_mesh(n)
+    if seed is not None:
+        m = apply_ordering(m, random_order(m.num_vertices, seed))
+    off, nbr = m.vertex_neighbours()
+    host = rcm_order(off, nbr).forward
+    dev = _lib.rcm_forward_device(m.edge_vertices, m.num_vertices)
+    assert np.array_equal(host, dev)
+
+
+def test_rcm_device_golden(golden):
+    """Device walk against the reference's own RCM permutations."""
+    from paper_1604_05937_b200 import _lib
+    for name in ("sq4", "sq16"):
+        key = f"{name}_rcm_forward"
+        assert key in golden
+        m = generate_unit_square_mesh(int(name[2:]))
+        dev = _lib.rcm_forward_device(m.edge_vertices, m.num_vertices)
+        assert np.array_equal(dev, golden[key])
