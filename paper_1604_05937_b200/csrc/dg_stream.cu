@@ -270,11 +270,83 @@ static int stream_cfg(int D) {
   return cfg >= 0 ? cfg : (D >= 6 ? 1 : 2);
 }
 
+// The stream kernel never reads the field's cell map: it relies on the
+// (2,1)-only layout being numbered by Alg. 1 (fspace.py:134-229), which
+// makes the field a dense (cell, layer, slot) array: map[c][j] =
+// c*k*layers + j, offsets[j] = k.  A caller-supplied map is checked once on
+// the device (maps are immutable, fspace.py:159-174; the verdict is cached
+// per (map, offsets, k, layers) and checked prefix); a map that is not dense, or an
+// unchecked one met during stream capture, sends the launch to the
+// map-reading kernels instead.
+__global__ void k_dense_map_check(const int32_t *__restrict__ map,
+                                  const int32_t *__restrict__ off,
+                                  int64_t n_cells, int k, int layers,
+                                  int *__restrict__ bad) {
+  const int64_t n = n_cells * k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / k;
+    const int j = (int)(i - c * k);
+    if ((int64_t)map[i] != c * k * layers + j) atomicOr(bad, 1);
+    if (i < k && off[i] != k) atomicOr(bad, 1);
+  }
+}
+
+static int dense_map_ok(const LoopArgs &a, bool *ok) {
+  struct Entry {
+    const int32_t *map, *off;
+    int64_t n_cells;
+    int k, layers, dev;
+    bool ok;
+  };
+  static Entry cache[32];
+  static int next = 0;
+  int dev = 0;
+  PM_CUDA_TRY(cudaGetDevice(&dev));
+  // an entry covers the map's first n_cells rows (the host path's chunks
+  // are prefixes [0, cell_end) of one map)
+  for (const Entry &e : cache)
+    if (e.map == a.cmap && e.off == a.coff && e.k == a.k &&
+        e.layers == a.layers && e.dev == dev &&
+        (!e.ok || a.n_cells <= e.n_cells)) {
+      *ok = e.ok;
+      return PM_OK;
+    }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  PM_CUDA_TRY(cudaStreamIsCapturing(a.s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) { // cannot synchronise: unchecked
+    *ok = false;
+    return PM_OK;
+  }
+  int *bad = nullptr;
+  PM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&bad), sizeof(int),
+                              a.s));
+  int h = 1;
+  cudaError_t err = cudaMemsetAsync(bad, 0, sizeof(int), a.s);
+  if (err == cudaSuccess) {
+    k_dense_map_check<<<grid_for(a.n_cells * a.k, 256, 4), 256, 0, a.s>>>(
+        a.cmap, a.coff, a.n_cells, a.k, a.layers, bad);
+    err = cudaGetLastError();
+  }
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, a.s);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(a.s);
+  cudaFreeAsync(bad, a.s);
+  PM_CUDA_TRY(err);
+  *ok = h == 0;
+  cache[next] = {a.cmap, a.coff, a.n_cells, a.k, a.layers, dev, *ok};
+  next = (next + 1) % 32;
+  return PM_OK;
+}
+
 // cell-layers [cl_begin, n_cells*layers) of the DG field (cl_begin must be
 // a multiple of the unit size so the bulk copies stay 16-byte aligned)
 template <int D>
 static int dg_stream_k(const LoopArgs &a, bool *handled, int64_t cl_begin) {
   *handled = false;
+  bool dense = false;
+  int rc0 = dense_map_ok(a, &dense);
+  if (rc0 || !dense) return rc0; // the map-reading kernels take the launch
   const int64_t n_cl = a.n_cells * (int64_t)a.layers - cl_begin;
   const int cfg = stream_cfg(D);
   const int T = cfg == 2 ? 128 : cfg == 3 ? 512 : kStreamT;

@@ -66,15 +66,20 @@ template <class LY, int W> constexpr int srb_entry() {
 #endif
 constexpr int kSrDepth = PM_SR_DEPTH;
 static_assert(kSrDepth == 3 || kSrDepth == 6, "ring depth 3 or 6");
-// PM_SR_ONESYNC = 1: one warp barrier per step.  Step k first waits for
-// its own copies and syncs the warp, then refills the slot step k-1 was
-// read from (every lane is past those reads), then reads its slot: the
-// barrier that publishes step k's copies also retires step k-1's reads,
-// at the price of one step less prefetch distance (depth - 1).
-#ifndef PM_SR_ONESYNC
-#define PM_SR_ONESYNC 0
+// PM_SR_CELLSUM = 1 (default, scalar vertex columns): with the invariant
+// triangle factor
+// (Mtri = ta I + tb J) a window vertex's contribution from cell j is
+// dta_j z_h + d_j, d_j = dtb_j (z_0 + z_1 + z_2): the same d_j for all
+// three window vertices, and z_h fixed while h is in the window.  A vertex
+// lives in exactly the three cells formed while it is in the window, the
+// last three cells when it leaves, so instead of three accumulators
+// updated every step (3 DADD + 3 DFMA per channel) the kernel keeps the
+// last three cells' dta and d in a 3-slot ring (slot = cell % 3) and
+// forms z_h (dta_k + dta_k+1 + dta_k+2) + (d_k + d_k+1 + d_k+2) once, when
+// the vertex leaves.
+#ifndef PM_SR_CELLSUM
+#define PM_SR_CELLSUM 1
 #endif
-constexpr bool kSrOneSync = PM_SR_ONESYNC != 0;
 
 
 // Padded ring entries of the strip kernel (a chunk of CW = W*L levels):
@@ -349,6 +354,22 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
     // layers and the geometry the Jacobian needs, derived once on entry:
     // xm, ym (mid-layer), dz; per-vertex accumulators acc[j][c][v]
     double zv[3][L][NC][NV], gm[3][L][3], acc[3][L][NC][NV];
+    // PM_SR_CELLSUM: the last three cells' dta (tr) and d (dr), ring slot
+    // = the window slot of the step that formed the cell
+    // (scalar columns: measured -1..3 % on P1; the 3-vector columns lose
+    // 2.5 % -- the flush's dependent sums lengthen its critical path)
+    constexpr bool CSUM = SYM && PM_SR_CELLSUM && NC == 1;
+    double tr[CSUM ? 3 : 1][L], dr[CSUM ? 3 : 1][L][NC][NV];
+#pragma unroll
+    for (int a = 0; a < (CSUM ? 3 : 1); ++a)
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        tr[a][j] = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) dr[a][j][c][v] = 0.0;
+      }
     double *yc[3] = {yl, yl, yl}; // lane's first element of the column
     bool live[3] = {false, false, false}, st[3] = {false, false, false};
 #pragma unroll
@@ -456,11 +477,24 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
       return v;
     };
 #pragma unroll
-    for (int d = 0; d < (kSrOneSync ? kSrDepth - 1 : kSrDepth); ++d)
-      rv[d] = fetch(d, d);
+    for (int d = 0; d < kSrDepth; ++d) rv[d] = fetch(d, d);
 
     auto flush = [&](auto A_) {
       constexpr int A = decltype(A_)::value;
+      if constexpr (CSUM) {
+        // the leaving vertex's cells are the last three: all ring slots
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+          const double t = tr[0][j] + tr[1][j] + tr[2][j];
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+              acc[A][j][c][v] =
+                  fma(zv[A][j][c][v], t,
+                      dr[0][j][c][v] + dr[1][j][c][v] + dr[2][j][c][v]);
+        }
+      }
       // back to the vertex column's layer blocks: per level j the bottom /
       // connecting channels vb[j], the top copies of the lane's last level
       // vt (added by the lane above, or by the chunk's last lane)
@@ -558,14 +592,8 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
       if (!FILL) flush(A_);
       const bool act = k < len;
       // the vertex of ring slot A (step k) enters window slot A
-      // this lane's copies of step k landed
-      sr_wait<kSrOneSync ? kSrDepth - 2 : kSrDepth - 1>();
-      __syncwarp(); // ... and the other lanes' ones
-      if constexpr (kSrOneSync) {
-        // (and every lane is done with step k-1's slot: refill it)
-        constexpr int P = (R + kSrDepth - 1) % kSrDepth;
-        rv[P] = fetch(k + kSrDepth - 1, P);
-      }
+      sr_wait<kSrDepth - 1>(); // this lane's copies of step k landed
+      __syncwarp();            // ... and the other lanes' ones
       // steps past this segment's strip read a zero block instead of the
       // (stale, possibly non-finite) ring slot; lanes past the chunk read
       // zero-filled values and are never flushed.
@@ -593,8 +621,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         gm[A][j][1] = g[j][1] + g[j + 1][1];
         gm[A][j][2] = g[j + 1][2] - g[j][2];
       }
-      if constexpr (!kSrOneSync)
-        __syncwarp(); // reads done before the slot is refilled
+      __syncwarp(); // reads done before the slot is refilled
       const int va = rv[R] & IDM;
       const int rv_cell = rv[R]; // before the slot is refilled
       yc[A] = col_at(PEER && va < ghost_end ? ylg : yl, va, colb);
@@ -618,7 +645,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
             zv[A][j][c][v] = s;
           }
       // refill ring slot A with the step kSrDepth ahead
-      if constexpr (!kSrOneSync) rv[R] = fetch(k + kSrDepth, R);
+      rv[R] = fetch(k + kSrDepth, R);
       if (FILL && A < 2) return; // window not full yet
 #pragma unroll
       for (int j = 0; j < L; ++j) {
@@ -635,7 +662,16 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
                 ? dj
                 : 0.0;
         // triangle stage, det folded into the accumulation
-        if constexpr (SYM) { // Mtri = ta I + tb J
+        if constexpr (CSUM) { // Mtri = ta I + tb J, cell ring slot A
+          tr[A][j] = det * M.ta;
+          const double dtb = det * M.tb;
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+              dr[A][j][c][v] = dtb * (zv[0][j][c][v] + zv[1][j][c][v] +
+                                      zv[2][j][c][v]);
+        } else if constexpr (SYM) { // Mtri = ta I + tb J
           const double dta = det * M.ta, dtb = det * M.tb;
 #pragma unroll
           for (int c = 0; c < NC; ++c)
@@ -704,9 +740,27 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         step(S2{}, S5{}, FF{}, k + 5);
       }
     }
+    // the last window: vertex k in slot 1 / 2 has no cell k+... past the
+    // loop, so the ring slots of cells it was not in are cleared first
+    auto clear_cell = [&](auto A_) {
+      constexpr int A = decltype(A_)::value;
+      if constexpr (CSUM) {
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+          tr[A][j] = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) dr[A][j][c][v] = 0.0;
+        }
+      }
+    };
     flush(S0{});
+    clear_cell(S0{});
     flush(S1{});
+    clear_cell(S1{});
     flush(S2{});
+    clear_cell(S2{});
     sr_wait<0>(); // no copy in flight into the ring across items
   }
   if constexpr (PEER) __threadfence_system(); // peer REDs land before exit

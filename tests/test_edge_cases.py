@@ -168,3 +168,39 @@ def test_cell_stream_vs_oracle(lname, n, layers, ordering):
     f = np.random.default_rng(layers).uniform(-1, 1, fs.total_dofs)
     got = mass_action(fs, f, quadrature=prism_quadrature(*quad_degrees(lname)))
     assert _rel(got, _oracle(base, layers, lname, f)) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_dg_stream_honours_a_caller_map():
+    """pm_column_mass (AUTO) with a DG layout and a caller-supplied map that
+    is not the dense Alg. 1 numbering (cells' blocks in reverse order): the
+    stream kernel, which never reads the field map, must not take it."""
+    import torch
+    from paper_1604_05937_b200 import (ExtrudedMesh, builtin_layout,
+                                       extrude_coordinates,
+                                       generate_unit_square_mesh,
+                                       number_dofs)
+    from paper_1604_05937_b200 import _lib
+    from paper_1604_05937_b200.kernels import MassOperator
+    m = ExtrudedMesh(generate_unit_square_mesh(16), 8)
+    fs = number_dofs(m, builtin_layout("DG1", "DG1"))
+    op = MassOperator(fs)
+    n2, k, L = m.base.num_cells, fs.num_slots, m.layers
+    coords = extrude_coordinates(m.base.coords, L, m.layer_height)
+    x = torch.from_numpy(np.random.default_rng(5).uniform(
+        -1, 1, fs.total_dofs)).cuda()
+    y_ref = op.apply(x, coords).cpu().numpy().reshape(n2, L * k)
+    rev = torch.arange(n2 - 1, -1, -1, device="cuda", dtype=torch.int32)
+    cmap2 = (rev[:, None] * (k * L) +
+             torch.arange(k, device="cuda", dtype=torch.int32)).contiguous()
+    x2 = x.reshape(n2, L * k).flip(0).contiguous().reshape(-1)
+    y2 = torch.full_like(x2, float("nan"))
+    _lib.column_mass(fs.layout, k, n2, L, cmap2, op.offs, op.xmap, op.xoffs,
+                     coords, op.mref, x2, y2, fs.total_dofs)
+    got = y2.cpu().numpy().reshape(n2, L * k)[::-1]
+    assert np.abs(got - y_ref).max() <= 1e-12 * np.abs(y_ref).max()
+    # and the dense map itself still takes the stream kernel's result
+    y3 = torch.empty_like(x)
+    _lib.column_mass(fs.layout, k, n2, L, op.cmap, op.offs, op.xmap,
+                     op.xoffs, coords, op.mref, x, y3, fs.total_dofs)
+    assert np.array_equal(y3.cpu().numpy().reshape(n2, L * k), y_ref)

@@ -19,7 +19,7 @@ torch = pytest.importorskip("torch")
 def test_host_buffers_pipelined(lname, ordering, monkeypatch):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    monkeypatch.setenv("PM_HOST_CHUNK_MB", "0.05")   # many chunks
+    monkeypatch.setenv("PM_HOST_CHUNK_MB", "0.01")   # many chunks
     from paper_1604_05937_b200 import configs
     from paper_1604_05937_b200.kernels import MassOperator, mass_action
     from paper_1604_05937_b200.quadrature import element_for_layout
