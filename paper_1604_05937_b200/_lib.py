@@ -340,10 +340,13 @@ def column_mass_strip(layout, k, layers, coords, mref, x, y, plan, dplan,
     check(rc)
 
 
-def build_global_strips(base, max_len=32, cells=None, edges=False):
+def build_global_strips(base, max_len=32, cells=None, edges=False,
+                        order=None):
     """(strip_ptr int32, steps int32[, steps_e int32 (n_steps, 2)]):
     sequential strips over the mesh or over the subset ``cells`` (host
-    C++); with ``edges`` also the two window edges each step brings in."""
+    C++); with ``edges`` also the two window edges each step brings in.
+    ``order``: "morton" (default, PM_STRIP_ORDER), "rcm" (mean vertex id)
+    or "creation" (as built: each strip starts at the lowest unused cell)."""
     cv = np.ascontiguousarray(base.cell_vertices, dtype=np.int32)
     ce = np.ascontiguousarray(base.cell_edges, dtype=np.int32)
     n = cv.shape[0]
@@ -369,11 +372,14 @@ def build_global_strips(base, max_len=32, cells=None, edges=False):
     # share a vertex row run close in time and the second one finds the
     # row in L2 (C5b: HBM reads 30.8 -> 21.0 GB, -10 % time; measured,
     # profiles/README.md).  PM_STRIP_ORDER=rcm: by mean vertex id instead.
+    mode = order or os.environ.get("PM_STRIP_ORDER", "morton")
+    if mode == "creation":
+        return (sp, st) if se is None else (sp, st, se)
     lens = np.diff(sp)
     sums = np.add.reduceat(st.astype(np.int64), sp[:-1]) if lens.size else \
         np.zeros(0)
     order = np.argsort(sums / np.maximum(lens, 1), kind="stable")
-    if os.environ.get("PM_STRIP_ORDER", "morton") == "morton" and lens.size:
+    if mode == "morton" and lens.size:
         from .schedule import morton_order
         xy = np.asarray(base.coords)[st]
         cx = np.add.reduceat(xy[:, 0], sp[:-1]) / np.maximum(lens, 1)
@@ -428,6 +434,7 @@ def build_patch_strips(base, patch_cells, patch_ptr, max_len=1 << 30,
 #: the step (a strip's first two fill steps)
 STEP_STORE = 1 << 30
 STEP_NOCELL = 1 << 29
+
 
 
 def column_mass_patch_strips(layout, k, layers, coords, mref, x, y, n_dofs,

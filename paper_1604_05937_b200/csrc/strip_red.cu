@@ -152,13 +152,21 @@ template <class LY> constexpr int sr_threads() {
 template <class LY, int W, int L> constexpr int sr_trow() {
   return (PM_SR_TROW && L == 1 && LY::CH0 > 1) ? (W + 1) * LY::CH0 : 0;
 }
+// PM_SR_DEFER = 1: the staged row's REDs are issued one flush later, from
+// the other of two staging rows, after the next row was staged: the row's
+// LDS results are ready by then (without it every RED waited on its LDS,
+// 15 % of the C5b warp stall samples, ncu source page)
+#ifndef PM_SR_DEFER
+#define PM_SR_DEFER 1
+#endif
+constexpr int kSrTrowBufs = PM_SR_DEFER ? 2 : 1;
 template <class LY, int W, int L> constexpr size_t sr_smem() {
   return sizeof(double) *
              ((size_t)(sr_threads<LY>() / 32) * kSrDepth * (32 / W) + 1) *
              sr_pentry<LY, W, L>() +
          sizeof(int) * (sr_threads<LY>() / 32) * (32 / W) * kSrIds +
          sizeof(double) * (sr_threads<LY>() / 32) * (32 / W) *
-             sr_trow<LY, W, L>();
+             sr_trow<LY, W, L>() * kSrTrowBufs;
 }
 
 __device__ __forceinline__ void sr_cp16z(double *dst, const double *src,
@@ -279,11 +287,13 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
                                                               SEGS + 1) * ES) +
                    ((threadIdx.x >> 5) * SEGS + seg) * kSrIds;
   constexpr int TR = sr_trow<LY, W, L>();
-  double *const trow =
+  // deferred REDs of the staged rows (non-stream strips only)
+  constexpr bool DEFER = TR > 0 && PM_SR_DEFER && !STREAM;
+  double *const trow0 =
       reinterpret_cast<double *>(reinterpret_cast<int *>(
           sr_ring + (size_t)(NWARP * kSrDepth * SEGS + 1) * ES) +
                                  NWARP * SEGS * kSrIds) +
-      ((threadIdx.x >> 5) * SEGS + seg) * TR;
+      ((threadIdx.x >> 5) * SEGS + seg) * TR * kSrTrowBufs;
   // the zero block (and, without zero-filling copies, the whole ring)
   for (int i = threadIdx.x; i < (PM_SR_ZFILL ? 1 : NWARP * kSrDepth * SEGS + 1) * ES;
        i += blockDim.x)
@@ -372,6 +382,11 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
       }
     double *yc[3] = {yl, yl, yl}; // lane's first element of the column
     bool live[3] = {false, false, false}, st[3] = {false, false, false};
+    // DEFER: staging row in use, the previously staged row's chunk origin
+    // and liveness (its REDs are still to be issued)
+    int tb = 0;
+    double *pbase = y;
+    bool plive = false;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -481,6 +496,17 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
 
     auto flush = [&](auto A_) {
       constexpr int A = decltype(A_)::value;
+      double *const trow = trow0 + (DEFER ? tb * TR : 0);
+      constexpr int NR = TR > 0 ? (TR + W - 1) / W : 1;
+      double pv[NR];
+      if constexpr (DEFER) { // the previous row's values (staged, synced)
+        const double *prow = trow0 + (tb ^ 1) * TR;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const int i = sl + W * r;
+          pv[r] = prow[i < TR ? i : 0];
+        }
+      }
       if constexpr (CSUM) {
         // the leaving vertex's cells are the last three: all ring slots
 #pragma unroll
@@ -557,7 +583,7 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
         }
       }
       if constexpr (TR > 0) { // the staged chunk, lane-contiguous REDs
-        __syncwarp();
+        if constexpr (!DEFER) __syncwarp();
         double *const base = yc[A] - sl * CH; // the chunk's first value
         const int n = nl * CH + LV;
         if constexpr (STREAM) {
@@ -571,6 +597,17 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
             sr_put(base + i, trow[i < TR ? i : 0],
                    i >= n ? 0 : (i < lo || i >= hi) ? (put & kPutAdd) : put);
           }
+        } else if constexpr (DEFER) {
+          // the previous row's REDs now; this row's at the next flush (the
+          // step's own __syncwarp orders the STS above before those LDS)
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            const int i = sl + W * r;
+            (PEER ? sr_red_sys : sr_red)(pbase + i, pv[r], plive && i < n);
+          }
+          pbase = base;
+          plive = live[A];
+          tb ^= 1;
         } else {
 #pragma unroll
           for (int r = 0; r < (TR + W - 1) / W; ++r) {
@@ -579,7 +616,8 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
                                          live[A] && i < n);
           }
         }
-        __syncwarp(); // row reads done before the next flush stages
+        if constexpr (!DEFER)
+          __syncwarp(); // row reads done before the next flush stages
       }
     };
 
@@ -757,10 +795,23 @@ k_strip_red(const KronMat M, const int32_t *__restrict__ item_ptr,
     };
     flush(S0{});
     clear_cell(S0{});
+    __syncwarp(); // (DEFER: each flush's staged row before the next's LDS)
     flush(S1{});
     clear_cell(S1{});
+    __syncwarp();
     flush(S2{});
     clear_cell(S2{});
+    if constexpr (DEFER) { // the last staged row
+      __syncwarp();
+      const double *prow = trow0 + (tb ^ 1) * TR;
+#pragma unroll
+      for (int r = 0; r < (TR + W - 1) / W; ++r) {
+        const int i = sl + W * r;
+        (PEER ? sr_red_sys : sr_red)(pbase + i, prow[i < TR ? i : 0],
+                                     plive && i < nl * CH + LV);
+      }
+      __syncwarp(); // row reads done before the next item stages
+    }
     sr_wait<0>(); // no copy in flight into the ring across items
   }
   if constexpr (PEER) __threadfence_system(); // peer REDs land before exit
