@@ -651,7 +651,9 @@ def run_sharded(args):
 
     def step(exchange=True):
         for q in parts:
-            q["op"].apply(q["x"], q["cw"], q["y"], exchange=exchange)
+            # the kernel alone (roofline): no exchange, no output memset
+            q["op"].apply(q["x"], q["cw"], q["y"], exchange=exchange,
+                          accumulate=not exchange)
 
     for _ in range(max(1, args.warmup)):
         step()
@@ -711,7 +713,8 @@ def run_sharded(args):
                          "frac": V / world / (kms * 1e-3) / 1e9 / peak,
                          "traffic": None, "kernel_ms": kms,
                          "kernel": "the rank's column loop (all parts, no "
-                                   "exchange), max over ranks",
+                                   "exchange, no output memset), max over "
+                                   "ranks",
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": V // world},
             "cpu_baseline": None,

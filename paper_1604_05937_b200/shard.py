@@ -392,7 +392,10 @@ class ShardedMassOperator:
         return y_window
 
     def apply(self, x_window, coords_window, y_window=None, exchange=True,
-              stream=None):
+              stream=None, accumulate=False):
+        """The rank's column loop into ``y_window`` (zeroed first unless
+        ``accumulate``), then the halo exchange (``exchange``; the fused
+        halo's step zeroes and synchronises on its own)."""
         import torch
         lo, hi = self.shard.window
         clo, _chi = self.shard.coord_window
@@ -402,7 +405,8 @@ class ShardedMassOperator:
         if y_window is None:
             y_window = torch.empty(hi - lo, dtype=torch.float64,
                                    device=x_window.device)
-        y_window.zero_()
+        if not accumulate:
+            y_window.zero_()
         op = self.op
         if self.strips is not None:
             strips, W = self.strips
