@@ -441,6 +441,11 @@ int pm_stencil_launch(void *handle, int32_t colored, int64_t n_cells,
                       const int32_t *cells, void *stream);
 int pm_stencil_free(void *handle);
 
+/* Build features: bit 0 = the experimental schedules (tile, store-first
+ * patch strips) are compiled in (PM_EXPERIMENTAL=1 at build time); without
+ * them pm_column_mass_tile / pm_column_mass_patch_strips return PM_EINVAL. */
+int pm_build_flags(void);
+
 /* Device cell re-sort of apply_ordering (replaces ordering.py:142-152):
  * cells_out = forward[cell_vertices][perm] with perm the stable lexsort of
  * the rows' sorted new vertex triples; perm_out (optional) receives perm.

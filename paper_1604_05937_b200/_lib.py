@@ -101,6 +101,7 @@ SIGNATURES = {
     "pm_stencil_launch": (ctypes.c_int, [_vp, _i32, _i64, _i32, _vp, _vp,
                                          _vp, _vp, _vp, _vp, _vp, _vp]),
     "pm_stencil_free": (ctypes.c_int, [_vp]),
+    "pm_build_flags": (ctypes.c_int, []),
     "pm_reorder_cells": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _vp,
                                         _vp]),
     "pm_column_mass_strip_red_peer": (ctypes.c_int, [
@@ -598,6 +599,12 @@ def vertex_graph_sorted_device(edge_vertices, n_vertices):
     check(host_lib().pm_vertex_graph_sorted(ptr(ev), ne, n_vertices, ptr(off),
                                             ptr(nb), stream_ptr(None)))
     return off.cpu().numpy(), nb.cpu().numpy().astype(np.int64)
+
+
+def experimental() -> bool:
+    """The library was built with the experimental schedules (tile,
+    store-first patch strips): PM_EXPERIMENTAL=1 at build time."""
+    return bool(host_lib().pm_build_flags() & 1)
 
 
 def stencil_check(source, k_in, k_out):

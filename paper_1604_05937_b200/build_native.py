@@ -47,6 +47,16 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) +
                   glob.glob(os.path.join(CSRC, "*.cpp")))
     headers = _headers()
+    # objects built with other -D flags are stale
+    flags = " ".join([os.environ.get("PM_EXPERIMENTAL", "0"),
+                      os.environ.get("PM_NVCC_EXTRA", "")])
+    stamp = os.path.join(OBJDIR, ".flags")
+    old = open(stamp).read() if os.path.exists(stamp) else None
+    if old != flags:
+        for o in glob.glob(os.path.join(OBJDIR, "*.o")):
+            os.remove(o)
+        with open(stamp, "w") as fh:
+            fh.write(flags)
     objs, cmds = [], []
     for src in srcs:
         obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")
@@ -54,7 +64,12 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
         if not _stale(obj, [src] + headers):
             continue
         # PM_NVCC_EXTRA: extra -D tuning flags (experiments, e.g. -DPM_SR_DEPTH=6)
-        cmd = [NVCC, *ARCH, *FLAGS, *os.environ.get("PM_NVCC_EXTRA", "").split(),
+        # PM_EXPERIMENTAL=1: also compile the experimental schedules (tile,
+        # store-first patch strips), slower than the defaults
+        exp = ["-DPM_EXPERIMENTAL=1"] if os.environ.get(
+            "PM_EXPERIMENTAL", "0") != "0" else []
+        cmd = [NVCC, *ARCH, *FLAGS, *exp,
+               *os.environ.get("PM_NVCC_EXTRA", "").split(),
                "-c", src, "-o", obj]
         if ptxas_verbose and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]

@@ -109,6 +109,12 @@ extern "C" int pm_set_launch_overlap(int32_t on) {
   return prev;
 }
 
+#ifndef PM_EXPERIMENTAL
+#define PM_EXPERIMENTAL 0
+#endif
+// bit 0: built with the experimental schedules (PM_EXPERIMENTAL=1)
+extern "C" int pm_build_flags(void) { return PM_EXPERIMENTAL ? 1 : 0; }
+
 extern "C" int pm_device_info(int32_t *sm, int64_t *l2) {
   int dev = 0, n = 0, l2b = 0;
   PM_CUDA_TRY(cudaGetDevice(&dev));

@@ -65,6 +65,12 @@ template <class LY, int W> constexpr int srb_entry() {
 #define PM_SR_DEPTH 3
 #endif
 constexpr int kSrDepth = PM_SR_DEPTH;
+// PM_EXPERIMENTAL = 1: also compile the store-first patch-strip kernels
+// (stream mode, schedule "pstrip"; slower than the global strips on every
+// config, profiles/README.md)
+#ifndef PM_EXPERIMENTAL
+#define PM_EXPERIMENTAL 0
+#endif
 static_assert(kSrDepth == 3 || kSrDepth == 6, "ring depth 3 or 6");
 // PM_SR_CELLSUM = 1 (default, scalar vertex columns): with the invariant
 // triangle factor
@@ -872,11 +878,16 @@ static int strip_red_w(const LoopArgs &a, const KronMat &M, bool sym,
                                                    n_strips);
   }
   if (a.item_ptr) { // store-first patch strips: one level per lane
+#if PM_EXPERIMENTAL
     if (sym)
       return strip_red_launch<LY, W, true, 1, false, true>(a, M, strip_ptr,
                                                            steps, n_strips);
     return strip_red_launch<LY, W, false, 1, false, true>(a, M, strip_ptr,
                                                           steps, n_strips);
+#else
+    set_error("patch strips are experimental: rebuild with PM_EXPERIMENTAL=1");
+    return PM_EINVAL;
+#endif
   }
   if constexpr (LY::CH0 <= 2 && W <= 16) {
     if (L == 2 && sym)
@@ -1347,6 +1358,7 @@ static int strip_red_e_k1(const LoopArgs &a, const int32_t *strip_ptr,
     else                                                                     \
       PM_SRE2(WW, false);                                                    \
   } while (0)
+#if PM_EXPERIMENTAL
 #define PM_SRE2(WW, SS)                                                      \
   do {                                                                       \
     if (a.item_ptr)                                                          \
@@ -1354,6 +1366,17 @@ static int strip_red_e_k1(const LoopArgs &a, const int32_t *strip_ptr,
     else                                                                     \
       PM_SRE3(WW, SS, false);                                                \
   } while (0)
+#else
+#define PM_SRE2(WW, SS)                                                      \
+  do {                                                                       \
+    if (a.item_ptr) {                                                        \
+      set_error("patch strips are experimental: rebuild with "              \
+                "PM_EXPERIMENTAL=1");                                        \
+      return PM_EINVAL;                                                      \
+    }                                                                        \
+    PM_SRE3(WW, SS, false);                                                  \
+  } while (0)
+#endif
 #define PM_SRE3(WW, SS, ST)                                                  \
   do {                                                                       \
     constexpr int T = sre_threads<SS>(), NW = T / 32;                        \
@@ -1362,9 +1385,15 @@ static int strip_red_e_k1(const LoopArgs &a, const int32_t *strip_ptr,
                             sre_entry<LY, WW>() +                            \
                         sizeof(int) * NW * (32 / WW) * 3 * kSrIds +          \
                         sizeof(double) * NW * (32 / WW) * sre_trow<LY, WW>(); \
-    PM_CUDA_TRY(cudaFuncSetAttribute(                                        \
-        k_strip_red_e<LY, WW, SS, ST>,                                       \
-        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
+    static int attr_dev = -1; /* attribute set once per device */           \
+    int dev_ = 0;                                                            \
+    PM_CUDA_TRY(cudaGetDevice(&dev_));                                       \
+    if (attr_dev != dev_) {                                                  \
+      PM_CUDA_TRY(cudaFuncSetAttribute(                                      \
+          k_strip_red_e<LY, WW, SS, ST>,                                     \
+          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));          \
+      attr_dev = dev_;                                                       \
+    }                                                                        \
     k_strip_red_e<LY, WW, SS, ST><<<grid, T, smem, a.s>>>(                   \
         M, a.item_ptr, strip_ptr, steps, steps_e, n_strips, a.layers,        \
         a.lbeg, a.lend, e_start, a.coords, a.x, a.y, a.store);                               \

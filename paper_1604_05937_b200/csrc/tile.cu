@@ -27,6 +27,15 @@
 
 #include <type_traits>
 
+// Experimental schedule (slower than the strip kernels on every config,
+// profiles/r02_tile_experiments.md): compiled only with PM_EXPERIMENTAL=1
+// (build_native: PM_EXPERIMENTAL=1 in the environment); otherwise the entry
+// points below report that and the library stays lean.
+#ifndef PM_EXPERIMENTAL
+#define PM_EXPERIMENTAL 0
+#endif
+#if PM_EXPERIMENTAL
+
 namespace pm {
 
 struct TilePlanDev {
@@ -827,3 +836,31 @@ extern "C" int pm_tile_trace(unsigned long long *out) {
   return 0;
 #endif
 }
+
+#else // !PM_EXPERIMENTAL
+
+extern "C" int pm_tile_smem_layout(const int32_t *, int32_t, int32_t,
+                                   int32_t, int32_t *stages,
+                                   int32_t *threads) {
+  if (stages) *stages = 0;
+  if (threads) *threads = 0;
+  return -1;
+}
+
+extern "C" int pm_column_mass_tile(const int32_t *, int32_t, const double *,
+                                   int64_t, const double *, const double *,
+                                   const double *, double *, int64_t,
+                                   const int32_t *, const int64_t *,
+                                   const int32_t *, const int32_t *,
+                                   const int32_t *, int32_t *, int32_t *,
+                                   int32_t, int32_t, int32_t, int32_t,
+                                   int32_t, int32_t, void *) {
+  pm::clear_error();
+  pm::set_error("the tile schedule is experimental: rebuild with "
+                "PM_EXPERIMENTAL=1");
+  return PM_EINVAL;
+}
+
+extern "C" int pm_tile_trace(unsigned long long *) { return PM_EINVAL; }
+
+#endif // PM_EXPERIMENTAL

@@ -64,3 +64,12 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("has a GPU")
     with pytest.raises(RuntimeError):
         _lib.cuda_device()
+
+
+def test_experimental_schedules_gated():
+    """The default build leaves the slower experimental kernels out (tile,
+    store-first patch strips) and says so through pm_build_flags."""
+    import os
+    from paper_1604_05937_b200 import _lib
+    want = os.environ.get("PM_EXPERIMENTAL", "0") != "0"
+    assert _lib.experimental() == want

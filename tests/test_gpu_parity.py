@@ -130,7 +130,14 @@ SCHEDULES = ("auto", "atomic", "colored", "column", "patch", "strip",
              "stripred", "pstrip")
 
 
+def _experimental():
+    from paper_1604_05937_b200 import _lib
+    return _lib.experimental()
+
+
 def _schedule_applies(lname, schedule):
+    if schedule == "pstrip" and not _experimental():
+        return False    # built without PM_EXPERIMENTAL
     if schedule == "patch":
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "P2xP2", "VP1")
     if schedule == "strip":
@@ -416,6 +423,8 @@ def test_patch_strips_layers(lname, layers, patch, monkeypatch):
     whole-mesh patches and every chunk-boundary case; accumulate adds."""
     from paper_1604_05937_b200 import configs, extrude_coordinates
     from paper_1604_05937_b200.kernels import MassOperator
+    if not _experimental():
+        pytest.skip("patch strips: library built without PM_EXPERIMENTAL")
     monkeypatch.setenv("PM_PATCH_CELLS", str(patch))
     w = configs.Workload("psl", 12, layers, lname, quad_degrees(lname),
                          ordering="random", jitter=0.2)
