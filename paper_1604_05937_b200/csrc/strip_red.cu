@@ -1001,12 +1001,15 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
   // values, added with lane-contiguous REDs (level copies and mid values
   // alternate in the column: per-lane REDs run at a 16-byte stride)
   constexpr int TR = sre_trow<LY, W>();
-  double *const trow =
+  // PM_SR_DEFER: two staging rows, REDs one flush late (see k_strip_red)
+  constexpr bool DEFER = TR > 0 && PM_SR_DEFER && !STREAM;
+  double *const trow0 =
       reinterpret_cast<double *>(
           reinterpret_cast<int *>(sr_ring + (size_t)(kSreWarps * kSrDepth *
                                                          SEGS + 1) * ES) +
           kSreWarps * SEGS * 3 * kSrIds) +
-      ((threadIdx.x >> 5) * SEGS + (threadIdx.x & 31) / W) * TR;
+      ((threadIdx.x >> 5) * SEGS + (threadIdx.x & 31) / W) * TR *
+          kSrTrowBufs;
   // the zero block; in STREAM mode the whole ring (dead edge slots read
   // stale ring entries, which must be finite)
   for (int i = threadIdx.x; i < (STREAM ? kSreWarps * kSrDepth * SEGS + 1 : 1) * ES;
@@ -1058,6 +1061,9 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
     double *yvc[3] = {yv0, yv0, yv0}, *yec[3] = {ye0, ye0, ye0};
     // flush mode per window slot (sr_put: 0 empty, 1 add, 3 store first)
     int vm[3] = {0, 0, 0}, em[3] = {0, 0, 0};
+    // DEFER: staging row in use, the previous row's origin and mode
+    int tb = 0, pm_ = 0;
+    double *pbase = y;
     auto mode = [&](bool live, int id) {
       return !live ? 0 : (store && (id & PM_STEP_STORE)) ? kPutStore : kPutAdd;
     };
@@ -1120,6 +1126,17 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
     // (bottom copy v = 0, connecting v = 1..NV-2, top copy v = NV-1 added
     // one lane up; the chunk's top level by the last lane)
     auto flush = [&](double (&acc)[NV], double *yp, int m) {
+      double *const trow = trow0 + (DEFER ? tb * TR : 0);
+      constexpr int NR = TR > 0 ? (TR + W - 1) / W : 1;
+      double pv[NR];
+      if constexpr (DEFER) { // the previous row (staged, synced)
+        const double *prow = trow0 + (tb ^ 1) * TR;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const int i = sl + W * r;
+          pv[r] = prow[i < TR ? i : 0];
+        }
+      }
       const double below = __shfl_up_sync(FULL, acc[NV - 1], 1, W);
       if constexpr (STREAM && TR == 0) { // store-first patch strips
         sr_put(yp, sl > 0 ? acc[0] + below : acc[0], m & bmask);
@@ -1134,9 +1151,22 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
           for (int v = 1; v < NV - 1; ++v) trow[sl * (NV - 1) + v] = acc[v];
         }
         if (sl == nl - 1) trow[(sl + 1) * (NV - 1)] = acc[NV - 1];
-        __syncwarp();
         double *const base = yp - sl * (NV - 1); // the chunk's first value
         const int n = nl * (NV - 1) + 1;
+        if constexpr (DEFER) {
+          // the previous row's REDs; this row's at the next flush, after
+          // the barrier below orders this STS before those LDS
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            const int i = sl + W * r;
+            sr_red(pbase + i, pv[r], pm_ && i < n);
+          }
+          pbase = base;
+          pm_ = m;
+          tb ^= 1;
+          __syncwarp();
+        } else {
+        __syncwarp();
         if constexpr (STREAM) { // store-first (m = 3): shared level copies add
           const int lo = l0 > 0 ? 1 : 0, hi = l0 + nl < layers ? n - 1 : n;
 #pragma unroll
@@ -1153,6 +1183,7 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
           }
         }
         __syncwarp(); // row reads done before the next flush stages
+        }
       } else if (m && lane_ok) {
         atomicAdd(yp, sl > 0 ? acc[0] + below : acc[0]);
 #pragma unroll
@@ -1311,6 +1342,17 @@ k_strip_red_e(const KronMat M, const int32_t *__restrict__ item_ptr,
       flush(av[a], yvc[a], vm[a]);
       flush(ae[a], yec[a], em[a]);
     }
+    if constexpr (DEFER) { // the last staged row (synced by its flush)
+      const double *prow = trow0 + (tb ^ 1) * TR;
+      const int n = nl * (NV - 1) + 1;
+#pragma unroll
+      for (int r = 0; r < (TR + W - 1) / W; ++r) {
+        const int i = sl + W * r;
+        sr_red(pbase + i, prow[i < TR ? i : 0], pm_ && i < n);
+      }
+      pm_ = 0;
+      __syncwarp(); // row reads done before the next item stages
+    }
     sr_wait<0>(); // no copy in flight into the ring across items
   }
 }
@@ -1384,7 +1426,8 @@ static int strip_red_e_k1(const LoopArgs &a, const int32_t *strip_ptr,
     const size_t smem = sizeof(double) * (NW * kSrDepth * (32 / WW) + 1) *   \
                             sre_entry<LY, WW>() +                            \
                         sizeof(int) * NW * (32 / WW) * 3 * kSrIds +          \
-                        sizeof(double) * NW * (32 / WW) * sre_trow<LY, WW>(); \
+                        sizeof(double) * NW * (32 / WW) * sre_trow<LY, WW>() *  \
+                            kSrTrowBufs;                                     \
     static int attr_dev = -1; /* attribute set once per device */           \
     int dev_ = 0;                                                            \
     PM_CUDA_TRY(cudaGetDevice(&dev_));                                       \

@@ -196,11 +196,12 @@ def test_dg_stream_honours_a_caller_map():
     x2 = x.reshape(n2, L * k).flip(0).contiguous().reshape(-1)
     y2 = torch.full_like(x2, float("nan"))
     _lib.column_mass(fs.layout, k, n2, L, cmap2, op.offs, op.xmap, op.xoffs,
-                     coords, op.mref, x2, y2, fs.total_dofs)
+                     coords, op.mref, x2, y2, fs.total_dofs, kron=op.kron)
     got = y2.cpu().numpy().reshape(n2, L * k)[::-1]
     assert np.abs(got - y_ref).max() <= 1e-12 * np.abs(y_ref).max()
     # and the dense map itself still takes the stream kernel's result
     y3 = torch.empty_like(x)
     _lib.column_mass(fs.layout, k, n2, L, op.cmap, op.offs, op.xmap,
-                     op.xoffs, coords, op.mref, x, y3, fs.total_dofs)
+                     op.xoffs, coords, op.mref, x, y3, fs.total_dofs,
+                     kron=op.kron)
     assert np.array_equal(y3.cpu().numpy().reshape(n2, L * k), y_ref)
