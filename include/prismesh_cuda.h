@@ -194,7 +194,9 @@ int pm_column_mass_strip_red(const int32_t *delta6, int32_t k, int32_t layers,
  * plan must not serve concurrent calls).  x and y index global DoFs;
  * n_dofs / n_coords = valid doubles from x / coords.  area_c = byte offset
  * of the coordinate area in a data buffer of data_bytes (a multiple of 128)
- * bytes; width = lanes (layers) per segment: 8, 16 or 32. */
+ * bytes; width = lanes (layers) per segment: 8, 16 or 32.
+ * Experimental (slower than pm_column_mass_strip_red): compiled only with
+ * PM_EXPERIMENTAL=1, otherwise PM_EINVAL (pm_build_flags bit 0). */
 int pm_column_mass_tile(const int32_t *delta6, int32_t layers,
                         const double *coords, int64_t n_coords,
                         const double *mtri, const double *mline,
@@ -337,6 +339,10 @@ int pm_build_patch_strips(int64_t n_cells, int64_t n_vertices, int64_t n_edges,
  * accumulate = 0: the zero pass clears the zero_list columns and the
  * chunk-boundary levels, flagged residencies store; accumulate = 1: every
  * residency adds (no zero pass). */
+/* pm_column_mass_patch_strips: the patch-strip (stream-mode) kernel is
+ * experimental (slower than the global strips): compiled only with
+ * PM_EXPERIMENTAL=1, otherwise PM_EINVAL (pm_build_flags bit 0); the host
+ * planner pm_build_patch_strips is always available. */
 int pm_column_mass_patch_strips(
     const int32_t *delta6, int32_t k, int32_t layers, const double *coords,
     const double *mref, const double *mtri, const double *mline,
