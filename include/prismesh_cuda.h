@@ -113,7 +113,15 @@ int pm_extrude_coordinates(const double *base_coords, int64_t n_vertices,
  *            colour for PM_VARIANT_COLORED, which always accumulates);
  *            NULL -> all n_cells cells
  * Each cell-layer's |det J| comes from the six prism vertices read out of
- * `coords`. */
+ * `coords`.
+ * DG (2,1)-only layouts with PM_VARIANT_AUTO / _STREAM take the bulk-copy
+ * stream kernel, which does not read cell_map: it needs the dense Alg. 1
+ * numbering (cell_map[c][j] = c*k*layers + j, offsets[j] = k).  A map is
+ * checked once on the device (one synchronisation; skipped during stream
+ * capture, where an unchecked map takes the map-reading kernels) and the
+ * verdict cached per (cell_map, offsets, k, layers) pointer values, so a
+ * map must not be changed in place while cached (the reference's maps are
+ * immutable, fspace.py:159-174). */
 int pm_column_mass(const int32_t *delta6, int32_t k, int64_t n_cells,
                    int32_t layers, const int32_t *cell_map,
                    const int32_t *offsets, const int32_t *coord_map,
