@@ -37,6 +37,7 @@
  *   pm_rcm_order             <- pkg/src/prismesh/ordering.py:45-90 (host BFS)
  *   pm_rcm_order_device      <- pkg/src/prismesh/ordering.py:45-90 (device walk)
  *   pm_stencil_*             <- SPEC.md:322-341 StencilKernel.apply (user kernels)
+ *   pm_column_mass_strip_dg  <- SPEC.md:333-341 iterate_columns, DG layouts along strips
  */
 #ifndef PRISMESH_CUDA_H
 #define PRISMESH_CUDA_H
@@ -459,6 +460,29 @@ int pm_stencil_free(void *handle);
  * patch strips) are compiled in (PM_EXPERIMENTAL=1 at build time); without
  * them pm_column_mass_tile / pm_column_mass_patch_strips return PM_EINVAL. */
 int pm_build_flags(void);
+
+/* --- DG layouts along strips --------------------------------------------
+ * pm_strip_step_cells: for a strip plan (pm_build_global_strips: strip_ptr
+ * n_strips+1, steps = entering vertices) the cell each step forms
+ * (step_cells, one per step; -1 on a strip's two fill steps), host.
+ * pm_column_mass_strip_dg: y = M x for a layout with DoFs on the prism
+ * cells only (delta6 = {0,0,0,0,0,k}, k in {1,2,3,6}; x, y in the dense
+ * Alg. 1 numbering): the cells are walked along the strips, one new
+ * vertex's coordinate chunk and the formed cell's field chunk per step
+ * through a cp.async ring, every DoF stored once (no zeroing, no atomics).
+ * Replaces the per-cell-layer coordinate gathers of the DG stream kernel
+ * (reference loop: SPEC.md:333-341 iterate_columns). chunk = 8, 16 or 32
+ * layers per warp segment.  Device pointers, asynchronous on `stream`. */
+int pm_strip_step_cells(int64_t n_cells, int64_t n_vertices,
+                        const int32_t *cell_vertices, const int32_t *strip_ptr,
+                        int64_t n_strips, const int32_t *steps,
+                        int32_t *step_cells);
+int pm_column_mass_strip_dg(const int32_t *delta6, int32_t k, int32_t layers,
+                            const double *coords, const double *mref,
+                            const double *x, double *y, int64_t n_strips,
+                            int32_t chunk, const int32_t *strip_ptr,
+                            const int32_t *steps, const int32_t *step_cells,
+                            void *stream);
 
 /* Device cell re-sort of apply_ordering (replaces ordering.py:142-152):
  * cells_out = forward[cell_vertices][perm] with perm the stable lexsort of

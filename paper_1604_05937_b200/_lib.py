@@ -102,6 +102,12 @@ SIGNATURES = {
                                          _vp, _vp, _vp, _vp, _vp, _vp]),
     "pm_stencil_free": (ctypes.c_int, [_vp]),
     "pm_build_flags": (ctypes.c_int, []),
+    "pm_strip_step_cells": (ctypes.c_int, [_i64, _i64, _vp, _vp, _i64, _vp,
+                                           _vp]),
+    "pm_column_mass_strip_dg": (ctypes.c_int, [_i32p, _i32, _i32, _vp,
+                                               ctypes.POINTER(_f64), _vp,
+                                               _vp, _i64, _i32, _vp, _vp,
+                                               _vp, _vp]),
     "pm_reorder_cells": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _vp,
                                         _vp]),
     "pm_column_mass_strip_red_peer": (ctypes.c_int, [
@@ -599,6 +605,33 @@ def vertex_graph_sorted_device(edge_vertices, n_vertices):
     check(host_lib().pm_vertex_graph_sorted(ptr(ev), ne, n_vertices, ptr(off),
                                             ptr(nb), stream_ptr(None)))
     return off.cpu().numpy(), nb.cpu().numpy().astype(np.int64)
+
+
+def strip_step_cells(base, strip_ptr, steps):
+    """The cell each strip step forms (-1 on fill steps), host C++."""
+    cv = np.ascontiguousarray(base.cell_vertices, dtype=np.int32)
+    sp = np.ascontiguousarray(strip_ptr, dtype=np.int32)
+    st = np.ascontiguousarray(steps, dtype=np.int32)
+    out = np.empty(st.shape[0], dtype=np.int32)
+    check(host_lib().pm_strip_step_cells(
+        cv.shape[0], base.num_vertices, cv.ctypes.data_as(ctypes.c_void_p),
+        sp.ctypes.data_as(ctypes.c_void_p), sp.shape[0] - 1,
+        st.ctypes.data_as(ctypes.c_void_p),
+        out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def column_mass_strip_dg(layout, k, layers, coords, mref, x, y, strips,
+                         chunk, stream=None):
+    """pm_column_mass_strip_dg: ``strips`` = device (strip_ptr, steps,
+    step_cells)."""
+    m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
+    d = layout.delta6()
+    sp, st, sc = strips
+    check(host_lib().pm_column_mass_strip_dg(
+        d.ctypes.data_as(_i32p), k, layers, ptr(coords), _f64ptr(m), ptr(x),
+        ptr(y), sp.shape[0] - 1, chunk, ptr(sp), ptr(st), ptr(sc),
+        stream_ptr(stream)))
 
 
 def experimental() -> bool:

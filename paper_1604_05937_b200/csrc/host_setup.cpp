@@ -620,3 +620,60 @@ extern "C" int pm_build_patch_strips(
   totals[2] = nz;
   return PM_OK;
 }
+
+// ---------------------------------------------------------------------------
+// The cell each strip step forms (for the DG strip kernel, whose field is
+// per cell): step i >= 2 of a strip forms the cell of its window, the last
+// three entered vertices {steps[i-2], steps[i-1], steps[i]}; the first two
+// (fill) steps form none (-1).  Found through the vertex -> cell incidence
+// of steps[i].
+// ---------------------------------------------------------------------------
+extern "C" int pm_strip_step_cells(int64_t n_cells, int64_t n_vertices,
+                                   const int32_t *cell_vertices,
+                                   const int32_t *strip_ptr, int64_t n_strips,
+                                   const int32_t *steps, int32_t *step_cells) {
+  pm::clear_error();
+  if (n_cells < 0 || n_vertices < 0 || n_strips < 0 ||
+      (n_strips > 0 && (!strip_ptr || !steps || !step_cells))) {
+    pm::set_error("pm_strip_step_cells: bad arguments");
+    return PM_EINVAL;
+  }
+  std::vector<int64_t> off(n_vertices + 1, 0);
+  for (int64_t c = 0; c < 3 * n_cells; ++c) {
+    const int32_t v = cell_vertices[c];
+    if (v < 0 || v >= n_vertices) {
+      pm::set_error("pm_strip_step_cells: vertex %d out of range", v);
+      return PM_EINVAL;
+    }
+    ++off[v + 1];
+  }
+  for (int64_t v = 0; v < n_vertices; ++v) off[v + 1] += off[v];
+  std::vector<int32_t> vc(3 * n_cells);
+  std::vector<int64_t> fill(off.begin(), off.end() - 1);
+  for (int64_t c = 0; c < n_cells; ++c)
+    for (int k = 0; k < 3; ++k) vc[fill[cell_vertices[3 * c + k]]++] = (int32_t)c;
+  for (int64_t s = 0; s < n_strips; ++s) {
+    const int32_t a = strip_ptr[s], b = strip_ptr[s + 1];
+    for (int32_t i = a; i < b; ++i) {
+      step_cells[i] = -1;
+      if (i < a + 2) continue;
+      const int32_t u = steps[i - 2], w = steps[i - 1], v = steps[i];
+      for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+        const int32_t c = vc[e];
+        const int32_t *t = cell_vertices + 3 * (int64_t)c;
+        const bool hu = t[0] == u || t[1] == u || t[2] == u;
+        const bool hw = t[0] == w || t[1] == w || t[2] == w;
+        if (hu && hw) {
+          step_cells[i] = c;
+          break;
+        }
+      }
+      if (step_cells[i] < 0) {
+        pm::set_error("pm_strip_step_cells: step %d of strip %lld forms no "
+                      "cell", i - a, (long long)s);
+        return PM_EINVAL;
+      }
+    }
+  }
+  return PM_OK;
+}

@@ -1504,6 +1504,215 @@ __global__ void k_zero_chunk_levels(double *__restrict__ y, int64_t n_vertices,
   }
 }
 
+// ---------------------------------------------------------------------------
+// DG layouts along strips (pm_column_mass_strip_dg): the DG stream kernel
+// gathers every cell-layer's six prism vertices' coordinates through the
+// coordinate map, which dominates its L1 traffic when a cell-layer holds
+// few DoFs (DG0 x DG0: one).  Walking the cells as the CG strips do, a step
+// brings one new vertex's coordinate chunk (the window keeps the other two)
+// and the formed cell's field chunk, both by cp.async into the per-warp
+// ring; the element kernel runs per lane (= layer) and the cell's D values
+// per cell-layer are stored directly: every DoF belongs to one cell-layer,
+// so there is no accumulation, no output zeroing and no atomics.
+// step_cells[i] = the cell step i forms (-1 on a strip's two fill steps,
+// pm_strip_step_cells).
+// ---------------------------------------------------------------------------
+template <int D, int W> constexpr int sd_crows() {
+  return (3 * (W + 1) + W - 1) / W;
+}
+template <int D, int W> constexpr int sd_entry() {
+  return (sd_crows<D, W>() + D) * W;
+}
+constexpr int kSdThreads = 256;
+
+template <int D, int W>
+__global__ void __launch_bounds__(kSdThreads, 3)
+k_strip_dg(const MassMat<D> M, const int32_t *__restrict__ strip_ptr,
+           const int32_t *__restrict__ steps,
+           const int32_t *__restrict__ step_cells, int64_t n_strips,
+           int layers, const double *__restrict__ coords,
+           const double *__restrict__ x, double *__restrict__ y) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int SEGS = 32 / W;
+  constexpr int CR = sd_crows<D, W>(), ES = sd_entry<D, W>();
+  constexpr int CP = D * W; // coordinate part offset in an entry
+  constexpr int NWARP = kSdThreads / 32;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % W, seg = lane / W;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int ccolb = 8 * 3 * (layers + 1); // coordinate column bytes
+  extern __shared__ double sd_ring[];
+  double *const ring =
+      sd_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
+  const double *const zero = sd_ring + (size_t)NWARP * kSrDepth * SEGS * ES;
+  int *const sid = reinterpret_cast<int *>(sd_ring + (size_t)(NWARP * kSrDepth *
+                                                              SEGS + 1) * ES) +
+                   ((threadIdx.x >> 5) * SEGS + seg) * 2 * kSrIds;
+  int *const scid = sid + kSrIds;
+  for (int i = threadIdx.x; i < ES; i += blockDim.x)
+    sd_ring[(size_t)NWARP * kSrDepth * SEGS * ES + i] = 0.0;
+  __syncthreads();
+
+  const int n_chunks = (layers + W - 1) / W;
+  const int64_t n_items = n_strips * n_chunks;
+  for (int64_t i0 = warp * SEGS; i0 < n_items; i0 += n_warps * SEGS) {
+    const int64_t item = i0 + seg;
+    const bool has = item < n_items;
+    const int64_t s = has ? item / n_chunks : 0;
+    const int l0 = has ? (int)(item % n_chunks) * W : 0;
+    const int k0 = has ? __ldg(strip_ptr + s) : 0;
+    const int len = has ? __ldg(strip_ptr + s + 1) - k0 : 0;
+    int maxlen = len;
+#pragma unroll
+    for (int o = W; o < 32; o <<= 1)
+      maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
+    const int nl = has ? min(W, layers - l0) : 0;
+    int cz[CR];
+#pragma unroll
+    for (int r = 0; r < CR; ++r) cz[r] = sl + W * r < 3 * (nl + 1) ? 8 : 0;
+    const double *cl0 = coords + 3 * (int64_t)l0 + sl;
+    double gm[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) gm[a][q] = 0.0;
+    auto load_ids = [&](int base) {
+#pragma unroll
+      for (int r = 0; r < kSrIds / W; ++r) {
+        const int i = base + sl + W * r;
+        sid[sl + W * r] = i < len ? __ldg(steps + k0 + i) : 0;
+        scid[sl + W * r] = i < len ? __ldg(step_cells + k0 + i) : -1;
+      }
+      __syncwarp();
+    };
+    __syncwarp();
+    load_ids(0);
+    auto entry = [&](int slot) {
+      return ring + (size_t)(slot * SEGS + seg) * ES;
+    };
+    int rc[kSrDepth]; // the cell of each ring slot's step
+    auto fetch = [&](int k, int slot) {
+      if ((k & (kSrIds - 1)) == 0 && k > 0) { // warp-uniform
+        __syncwarp();
+        load_ids(k);
+      }
+      const int v = sid[k & (kSrIds - 1)];
+      const int c = scid[k & (kSrIds - 1)];
+      if (k < len) {
+        double *e = entry(slot) + sl;
+        const double *cp = col_at(cl0, v, ccolb);
+#pragma unroll
+        for (int r = 0; r < CR; ++r) sr_cp8z(e + CP + W * r, cp + W * r, cz[r]);
+        if (c >= 0) { // the cell's chunk: D values per layer, contiguous
+          const double *fp = x + ((int64_t)c * layers + l0) * D + sl;
+#pragma unroll
+          for (int r = 0; r < D; ++r)
+            sr_cp8z(e + W * r, fp + W * r, sl + W * r < nl * D ? 8 : 0);
+        }
+      }
+      sr_commit();
+      return c;
+    };
+#pragma unroll
+    for (int d = 0; d < kSrDepth; ++d) rc[d] = fetch(d, d);
+
+    auto step = [&](auto A_, auto R_, int k) {
+      constexpr int A = decltype(A_)::value; // window slot (k % 3)
+      constexpr int R = decltype(R_)::value; // ring slot (k % kSrDepth)
+      const bool act = k < len;
+      sr_wait<kSrDepth - 1>();
+      __syncwarp();
+      const double *e = act ? entry(R) : zero;
+      const double *ec = e + CP;
+      double g0[3], g1[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        g0[q] = ec[3 * sl + q];
+        g1[q] = ec[3 * (sl + 1) + q];
+      }
+      gm[A][0] = g0[0] + g1[0];
+      gm[A][1] = g0[1] + g1[1];
+      gm[A][2] = g1[2] - g0[2];
+      const int c = rc[R];
+      double xf[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) xf[d] = e[sl * D + d];
+      __syncwarp(); // reads done before the slot is refilled
+      rc[R] = fetch(k + kSrDepth, R);
+      if (act && c >= 0 && sl < nl) {
+        const double det = prism_abs_detj_12(gm[0][0], gm[0][1], gm[0][2],
+                                             gm[1][0], gm[1][1], gm[1][2],
+                                             gm[2][0], gm[2][1], gm[2][2]);
+        double *yp = y + ((int64_t)c * layers + l0 + sl) * D;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) sacc = fma(M.m[i * D + j], xf[j], sacc);
+          yp[i] = det * sacc;
+        }
+      }
+    };
+    using S0 = std::integral_constant<int, 0>;
+    using S1 = std::integral_constant<int, 1>;
+    using S2 = std::integral_constant<int, 2>;
+    for (int k = 0; k < maxlen; k += 3) {
+      step(S0{}, S0{}, k);
+      step(S1{}, S1{}, k + 1);
+      step(S2{}, S2{}, k + 2);
+    }
+    sr_wait<0>(); // no copy in flight into the ring across items
+  }
+}
+
+template <int D, int W>
+static int strip_dg_launch(const MassMat<D> &M, const int32_t *strip_ptr,
+                           const int32_t *steps, const int32_t *step_cells,
+                           int64_t n_strips, int layers, const double *coords,
+                           const double *x, double *y, cudaStream_t s) {
+  constexpr int SEGS = 32 / W, NW = kSdThreads / 32;
+  const size_t smem =
+      sizeof(double) * ((size_t)NW * kSrDepth * SEGS + 1) * sd_entry<D, W>() +
+      sizeof(int) * NW * SEGS * 2 * kSrIds;
+  static int cached_dev = -1;
+  int dev = 0;
+  PM_CUDA_TRY(cudaGetDevice(&dev));
+  if (cached_dev != dev) {
+    PM_CUDA_TRY(cudaFuncSetAttribute(
+        k_strip_dg<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (int)smem));
+    cached_dev = dev;
+  }
+  const int64_t items = n_strips * ((layers + W - 1) / W);
+  const int64_t warps = (items + SEGS - 1) / SEGS;
+  const unsigned grid = grid_for(warps * 32, kSdThreads, strip_grid_cap(8));
+  k_strip_dg<D, W><<<grid, kSdThreads, smem, s>>>(
+      M, strip_ptr, steps, step_cells, n_strips, layers, coords, x, y);
+  PM_LAUNCH_CHECK("k_strip_dg");
+  return PM_OK;
+}
+
+template <int D>
+static int strip_dg_w(const double *mref, int W, const int32_t *strip_ptr,
+                      const int32_t *steps, const int32_t *step_cells,
+                      int64_t n_strips, int layers, const double *coords,
+                      const double *x, double *y, cudaStream_t s) {
+  MassMat<D> M; // 12 |det J| from the strip geometry: fold 1/12 in
+  for (int i = 0; i < D * D; ++i) M.m[i] = mref[i] * (1.0 / 12.0);
+  switch (W) {
+  case 32: return strip_dg_launch<D, 32>(M, strip_ptr, steps, step_cells,
+                                         n_strips, layers, coords, x, y, s);
+  case 16: return strip_dg_launch<D, 16>(M, strip_ptr, steps, step_cells,
+                                         n_strips, layers, coords, x, y, s);
+  case 8: return strip_dg_launch<D, 8>(M, strip_ptr, steps, step_cells,
+                                       n_strips, layers, coords, x, y, s);
+  default:
+    set_error("strip chunk width must be 8, 16 or 32 (got %d)", W);
+    return PM_EINVAL;
+  }
+}
+
 } // namespace pm
 
 static int strip_red_entry(
@@ -1639,4 +1848,39 @@ extern "C" int pm_column_mass_patch_strips(
                          n_dofs, accumulate, n_patches, chunk, strip_ptr,
                          steps, steps_e, n_vertices, nullptr, 0, stream,
                          item_ptr, n_zero, zero_list);
+}
+
+extern "C" int pm_column_mass_strip_dg(
+    const int32_t *delta6, int32_t k, int32_t layers, const double *coords,
+    const double *mref, const double *x, double *y, int64_t n_strips,
+    int32_t chunk, const int32_t *strip_ptr, const int32_t *steps,
+    const int32_t *step_cells, void *stream) {
+  pm::clear_error();
+  const bool dg_only = delta6 && !delta6[0] && !delta6[1] && !delta6[2] &&
+                       !delta6[3] && !delta6[4] && delta6[5] == k;
+  if (!dg_only || layers < 1 || n_strips < 0 || !mref) {
+    pm::set_error("pm_column_mass_strip_dg: a DG layout (DoFs on the prism "
+                  "cells only, k = delta(2,1)) and layers >= 1");
+    return PM_EINVAL;
+  }
+  if (n_strips == 0) return PM_OK;
+  if (!coords || !x || !y || !strip_ptr || !steps || !step_cells) {
+    pm::set_error("NULL device pointer");
+    return PM_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (k) {
+  case 1: return pm::strip_dg_w<1>(mref, chunk, strip_ptr, steps, step_cells,
+                                   n_strips, layers, coords, x, y, s);
+  case 2: return pm::strip_dg_w<2>(mref, chunk, strip_ptr, steps, step_cells,
+                                   n_strips, layers, coords, x, y, s);
+  case 3: return pm::strip_dg_w<3>(mref, chunk, strip_ptr, steps, step_cells,
+                                   n_strips, layers, coords, x, y, s);
+  case 6: return pm::strip_dg_w<6>(mref, chunk, strip_ptr, steps, step_cells,
+                                   n_strips, layers, coords, x, y, s);
+  default:
+    pm::set_error("pm_column_mass_strip_dg: %d DoFs per cell-layer (1, 2, 3 "
+                  "or 6 compiled)", k);
+    return PM_EINVAL;
+  }
 }

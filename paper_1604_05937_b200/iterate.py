@@ -43,7 +43,7 @@ import numpy as np
 from . import _lib
 
 SCHEDULES = ("auto", "atomic", "colored", "sequential", "column", "stream",
-             "patch", "strip", "stripred", "pstrip", "tile")
+             "patch", "strip", "stripred", "pstrip", "stripdg", "tile")
 
 
 @dataclass(frozen=True)

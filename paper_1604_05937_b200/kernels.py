@@ -154,6 +154,7 @@ class MassOperator:
         self._patch = None
         self._strip = None
         self._gstrips = None
+        self._dgstrips = None
         self._pstrips = None
         self._tiles = None
         self._tile_tmp = None
@@ -438,6 +439,20 @@ class MassOperator:
             self._gstrips = g
         return self._gstrips
 
+    def _dg_strips(self):
+        """Global strips + the cell of every step (cached), for the DG
+        strip kernel."""
+        if self._dgstrips is None:
+            import torch
+            base = self.fs.mesh.base
+            sp, st = _lib.build_global_strips(
+                base, max_len=strip_max_len(self.n_cells, self.layers))
+            sc = _lib.strip_step_cells(base, sp, st)
+            self._dgstrips = (tuple(torch.from_numpy(a).to(self._dev)
+                                    for a in (sp, st, sc)),
+                              strip_chunk_width(self.layers))
+        return self._dgstrips
+
     def _patch_strips(self):
         """Store-first patch strips (cached): Morton patches of the cells,
         sequential strips inside each (pm_build_patch_strips)."""
@@ -544,8 +559,15 @@ class MassOperator:
         if y is None:
             y = torch.empty(n, dtype=torch.float64, device=x.device)
             accumulate = False
-        if not self.kron_ok and sched != "stream":
+        if not self.kron_ok and sched not in ("stream", "stripdg"):
             sched = "atomic"   # dense Mref in the generic kernel
+        if sched == "auto" and self.dg_only and self.k in (1, 2, 3):
+            # few DoFs per cell-layer: walking the cells along strips loads
+            # each vertex's coordinates once per strip instead of gathering
+            # six prism vertices per cell-layer (measured: DG0xDG0 +54 %,
+            # DG0xDG1 +20 %, DG1xDG0 +6 % at 100 layers; the stream kernel
+            # stays ahead for DG1xDG1, profiles/README.md)
+            sched = "stripdg"
         if sched == "auto" and self.share == 2:
             # measured fastest (profiles/): global strips for vertex-column
             # layouts, the warp-per-column kernel otherwise
@@ -563,6 +585,24 @@ class MassOperator:
                                        self.kron, W, accumulate=accumulate,
                                        stream=stream,
                                        n_vertices=self.fs.mesh.base.num_vertices)
+            return y
+        if sched == "stripdg":
+            if not self.dg_only or self.k not in (1, 2, 3, 6):
+                raise ValueError(
+                    f"the DG strip schedule needs DoFs on the prism cells "
+                    f"only (1, 2, 3 or 6 per cell-layer), got "
+                    f"{self.fs.layout.name}")
+            strips, W = self._dg_strips()
+            if not accumulate:
+                _lib.column_mass_strip_dg(self.fs.layout, self.k,
+                                          self.layers, coords, self.mref, x,
+                                          y, strips, W, stream=stream)
+            else:
+                tmp = torch.empty_like(y)
+                _lib.column_mass_strip_dg(self.fs.layout, self.k,
+                                          self.layers, coords, self.mref, x,
+                                          tmp, strips, W, stream=stream)
+                y += tmp
             return y
         if sched == "tile":
             if not self.tile_ok:

@@ -127,7 +127,7 @@ def test_arity_and_mesh_mismatch_rejected(gmesh):
 
 
 SCHEDULES = ("auto", "atomic", "colored", "column", "patch", "strip",
-             "stripred", "pstrip")
+             "stripred", "pstrip", "stripdg")
 
 
 def _experimental():
@@ -144,6 +144,8 @@ def _schedule_applies(lname, schedule):
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1")
     if schedule in ("stripred", "pstrip"):
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1", "P2xP2")
+    if schedule == "stripdg":
+        return lname in ("DG0xDG0", "DG0xDG1", "DG1xDG0", "DG1xDG1")
     return True
 
 
@@ -465,3 +467,30 @@ def test_host_pipelined_mass_action(lname, layers, n):
         assert np.array_equal(got, dev)
     assert _rel(got, dev) <= _tol(lname)
     assert _rel(got, _oracle_for(w, fs).assemble(x)) <= _tol(lname)
+
+
+@pytest.mark.parametrize("lname", ("DG0xDG0", "DG0xDG1", "DG1xDG0",
+                                   "DG1xDG1"))
+@pytest.mark.parametrize("ordering", ("rcm", "random"))
+@pytest.mark.parametrize("layers", (1, 7, 16, 33, 64, 100))
+def test_dg_strips(lname, ordering, layers):
+    """DG layouts along strips (schedule "stripdg"): every chunk width
+    (W by layers), ragged tails, jittered random meshes, NaN-filled output
+    (every DoF stored), accumulate mode."""
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.kernels import MassOperator
+    w = configs.Workload("sdg", 18, layers, lname, quad_degrees(lname),
+                         ordering=ordering, jitter=0.2)
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    op = MassOperator(fs, quad, schedule="stripdg")
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    ref = _oracle_for(w, fs).assemble(x)
+    xd = torch.from_numpy(x).cuda()
+    y = torch.full_like(xd, float("nan"))
+    op.apply(xd, coords, y)
+    yh = y.cpu().numpy()
+    assert np.isfinite(yh).all()
+    assert _rel(yh, ref) <= 1e-12
+    y2 = op.apply(xd, coords, y, accumulate=True)
+    assert _rel(y2.cpu().numpy(), 2 * ref) <= 1e-12

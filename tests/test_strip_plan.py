@@ -274,3 +274,25 @@ def test_integration_patch_strips_snippet():
     got = ns["patch_strips"](base, order, ptr, edges=True)
     want = _lib.build_patch_strips(base, order, ptr, edges=True)
     assert all(np.array_equal(a, b) for a, b in zip(got, want))
+
+
+@pytest.mark.parametrize("n,ordering", [(1, "rcm"), (6, "rcm"), (13, "random")])
+def test_strip_step_cells(n, ordering):
+    """pm_strip_step_cells: every cell formed by exactly one step, fill
+    steps form none, and a step's cell is its window (last three entered
+    vertices) -- the per-cell field addressing of the DG strip kernel."""
+    from paper_1604_05937_b200 import _lib, configs
+    w = configs.Workload("sc", n, 2, "DG1xDG1", (2, 2), ordering=ordering)
+    fs, _q, _x, _ = configs.build(w)
+    base = fs.mesh.base
+    sp, st = _lib.build_global_strips(base, max_len=7)
+    sc = _lib.strip_step_cells(base, sp, st)
+    assert sc.shape == st.shape
+    cells = sc[sc >= 0]
+    assert np.array_equal(np.sort(cells), np.arange(base.num_cells))
+    cv = np.asarray(base.cell_vertices)
+    for s in range(sp.shape[0] - 1):
+        a, b = sp[s], sp[s + 1]
+        assert sc[a] == -1 and sc[a + 1] == -1
+        for i in range(a + 2, b):
+            assert set(cv[sc[i]]) == {st[i - 2], st[i - 1], st[i]}
