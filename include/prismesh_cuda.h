@@ -466,10 +466,15 @@ int pm_build_flags(void);
  * n_strips+1, steps = entering vertices) the cell each step forms
  * (step_cells, one per step; -1 on a strip's two fill steps), host.
  * pm_column_mass_strip_dg: y = M x for a layout with DoFs on the prism
- * cells only (delta6 = {0,0,0,0,0,k}, k in {1,2,3,6}; x, y in the dense
- * Alg. 1 numbering): the cells are walked along the strips, one new
- * vertex's coordinate chunk and the formed cell's field chunk per step
- * through a cp.async ring, every DoF stored once (no zeroing, no atomics).
+ * cells only, x, y in the Alg. 1 numbering (dense per cell column):
+ * delta6 = {0,0,0,0,0,k}, k in {1,2,3,6} (DG x DG), or delta6 =
+ * {0,0,0,0,d0,0}, k = 2 d0, d0 in {1,3} (DG x CG1: level DoFs shared by
+ * the two layers of a cell that meet there).  The cells are walked along
+ * the strips, one new vertex's coordinate chunk and the formed cell's
+ * field chunk per step through a cp.async ring; DG x DG stores every DoF
+ * once (no zeroing, no atomics); DG x CG1 combines a level's two layers by
+ * shuffle and stores it once, except the levels between W-layer chunks,
+ * which are zeroed first and added.
  * Replaces the per-cell-layer coordinate gathers of the DG stream kernel
  * (reference loop: SPEC.md:333-341 iterate_columns). chunk = 8, 16 or 32
  * layers per warp segment.  Device pointers, asynchronous on `stream`. */
@@ -477,8 +482,9 @@ int pm_strip_step_cells(int64_t n_cells, int64_t n_vertices,
                         const int32_t *cell_vertices, const int32_t *strip_ptr,
                         int64_t n_strips, const int32_t *steps,
                         int32_t *step_cells);
-int pm_column_mass_strip_dg(const int32_t *delta6, int32_t k, int32_t layers,
-                            const double *coords, const double *mref,
+int pm_column_mass_strip_dg(const int32_t *delta6, int32_t k, int64_t n_cells,
+                            int32_t layers, const double *coords,
+                            const double *mref,
                             const double *x, double *y, int64_t n_strips,
                             int32_t chunk, const int32_t *strip_ptr,
                             const int32_t *steps, const int32_t *step_cells,

@@ -104,7 +104,7 @@ SIGNATURES = {
     "pm_build_flags": (ctypes.c_int, []),
     "pm_strip_step_cells": (ctypes.c_int, [_i64, _i64, _vp, _vp, _i64, _vp,
                                            _vp]),
-    "pm_column_mass_strip_dg": (ctypes.c_int, [_i32p, _i32, _i32, _vp,
+    "pm_column_mass_strip_dg": (ctypes.c_int, [_i32p, _i32, _i64, _i32, _vp,
                                                ctypes.POINTER(_f64), _vp,
                                                _vp, _i64, _i32, _vp, _vp,
                                                _vp, _vp]),
@@ -621,15 +621,16 @@ def strip_step_cells(base, strip_ptr, steps):
     return out
 
 
-def column_mass_strip_dg(layout, k, layers, coords, mref, x, y, strips,
-                         chunk, stream=None):
+def column_mass_strip_dg(layout, k, n_cells, layers, coords, mref, x, y,
+                         strips, chunk, stream=None):
     """pm_column_mass_strip_dg: ``strips`` = device (strip_ptr, steps,
     step_cells)."""
     m = np.ascontiguousarray(mref, dtype=np.float64).ravel()
     d = layout.delta6()
     sp, st, sc = strips
     check(host_lib().pm_column_mass_strip_dg(
-        d.ctypes.data_as(_i32p), k, layers, ptr(coords), _f64ptr(m), ptr(x),
+        d.ctypes.data_as(_i32p), k, n_cells, layers, ptr(coords), _f64ptr(m),
+        ptr(x),
         ptr(y), sp.shape[0] - 1, chunk, ptr(sp), ptr(st), ptr(sc),
         stream_ptr(stream)))
 

@@ -1713,6 +1713,268 @@ static int strip_dg_w(const double *mref, int W, const int32_t *strip_ptr,
   }
 }
 
+// Cell columns with level DoFs (DoFs on (2,0) only: DG0 x CG1, DG1 x CG1),
+// along strips: as k_strip_dg, but a cell column holds D0 values per LEVEL
+// (layers + 1 levels), the level between two layers shared by both.  Lane
+// l of a W-layer chunk computes cell-layer l0 + l from its bottom and top
+// levels; its top contribution reaches level l0 + l + 1 by shfl.up, so each
+// chunk-interior level is stored once.  The chunk's bottom level (shared
+// with the chunk below) and top level (with the chunk above) are added
+// (REDG) into levels zeroed first (pm_column_mass_strip_dgv zeroes only
+// those, k_zero_cell_levels); a column's first and last level are stored.
+template <int D0, int W> constexpr int sv_frows() {
+  return (D0 * (W + 1) + W - 1) / W;
+}
+template <int D0, int W> constexpr int sv_entry() {
+  return (sv_frows<D0, W>() + sd_crows<D0, W>()) * W;
+}
+
+template <int D0, int W>
+__global__ void __launch_bounds__(kSdThreads, 3)
+k_strip_dgv(const MassMat<2 * D0> M, const int32_t *__restrict__ strip_ptr,
+            const int32_t *__restrict__ steps,
+            const int32_t *__restrict__ step_cells, int64_t n_strips,
+            int layers, const double *__restrict__ coords,
+            const double *__restrict__ x, double *__restrict__ y) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int SEGS = 32 / W, K = 2 * D0;
+  constexpr int FR = sv_frows<D0, W>(), CR = sd_crows<D0, W>();
+  constexpr int ES = sv_entry<D0, W>(), CP = FR * W;
+  constexpr int NWARP = kSdThreads / 32;
+  const int lane = threadIdx.x & 31;
+  const int sl = lane % W, seg = lane / W;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int ccolb = 8 * 3 * (layers + 1);
+  const int64_t fcol = (int64_t)D0 * (layers + 1); // cell column length
+  extern __shared__ double sd_ring[];
+  double *const ring =
+      sd_ring + (size_t)(threadIdx.x >> 5) * kSrDepth * SEGS * ES;
+  const double *const zero = sd_ring + (size_t)NWARP * kSrDepth * SEGS * ES;
+  int *const sid = reinterpret_cast<int *>(sd_ring + (size_t)(NWARP * kSrDepth *
+                                                              SEGS + 1) * ES) +
+                   ((threadIdx.x >> 5) * SEGS + seg) * 2 * kSrIds;
+  int *const scid = sid + kSrIds;
+  for (int i = threadIdx.x; i < ES; i += blockDim.x)
+    sd_ring[(size_t)NWARP * kSrDepth * SEGS * ES + i] = 0.0;
+  __syncthreads();
+
+  const int n_chunks = (layers + W - 1) / W;
+  const int64_t n_items = n_strips * n_chunks;
+  for (int64_t i0 = warp * SEGS; i0 < n_items; i0 += n_warps * SEGS) {
+    const int64_t item = i0 + seg;
+    const bool has = item < n_items;
+    const int64_t s = has ? item / n_chunks : 0;
+    const int l0 = has ? (int)(item % n_chunks) * W : 0;
+    const int k0 = has ? __ldg(strip_ptr + s) : 0;
+    const int len = has ? __ldg(strip_ptr + s + 1) - k0 : 0;
+    int maxlen = len;
+#pragma unroll
+    for (int o = W; o < 32; o <<= 1)
+      maxlen = max(maxlen, __shfl_xor_sync(FULL, maxlen, o));
+    const int nl = has ? min(W, layers - l0) : 0;
+    int cz[CR], fz[FR];
+#pragma unroll
+    for (int r = 0; r < CR; ++r) cz[r] = sl + W * r < 3 * (nl + 1) ? 8 : 0;
+#pragma unroll
+    for (int r = 0; r < FR; ++r) fz[r] = sl + W * r < D0 * (nl + 1) ? 8 : 0;
+    const double *cl0 = coords + 3 * (int64_t)l0 + sl;
+    // bottom level of the chunk: shared with the chunk below unless the
+    // column starts here; top level: with the chunk above unless it ends
+    const bool bot_add = l0 > 0, top_add = l0 + nl < layers;
+    double gm[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) gm[a][q] = 0.0;
+    auto load_ids = [&](int base) {
+#pragma unroll
+      for (int r = 0; r < kSrIds / W; ++r) {
+        const int i = base + sl + W * r;
+        sid[sl + W * r] = i < len ? __ldg(steps + k0 + i) : 0;
+        scid[sl + W * r] = i < len ? __ldg(step_cells + k0 + i) : -1;
+      }
+      __syncwarp();
+    };
+    __syncwarp();
+    load_ids(0);
+    auto entry = [&](int slot) {
+      return ring + (size_t)(slot * SEGS + seg) * ES;
+    };
+    int rc[kSrDepth];
+    auto fetch = [&](int k, int slot) {
+      if ((k & (kSrIds - 1)) == 0 && k > 0) { // warp-uniform
+        __syncwarp();
+        load_ids(k);
+      }
+      const int v = sid[k & (kSrIds - 1)];
+      const int c = scid[k & (kSrIds - 1)];
+      if (k < len) {
+        double *e = entry(slot) + sl;
+        const double *cp = col_at(cl0, v, ccolb);
+#pragma unroll
+        for (int r = 0; r < CR; ++r) sr_cp8z(e + CP + W * r, cp + W * r, cz[r]);
+        if (c >= 0) {
+          const double *fp = x + (int64_t)c * fcol + (int64_t)l0 * D0 + sl;
+#pragma unroll
+          for (int r = 0; r < FR; ++r) sr_cp8z(e + W * r, fp + W * r, fz[r]);
+        }
+      }
+      sr_commit();
+      return c;
+    };
+#pragma unroll
+    for (int d = 0; d < kSrDepth; ++d) rc[d] = fetch(d, d);
+
+    auto step = [&](auto A_, auto R_, int k) {
+      constexpr int A = decltype(A_)::value;
+      constexpr int R = decltype(R_)::value;
+      const bool act = k < len;
+      sr_wait<kSrDepth - 1>();
+      __syncwarp();
+      const double *e = act ? entry(R) : zero;
+      const double *ec = e + CP;
+      double g0[3], g1[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        g0[q] = ec[3 * sl + q];
+        g1[q] = ec[3 * (sl + 1) + q];
+      }
+      gm[A][0] = g0[0] + g1[0];
+      gm[A][1] = g0[1] + g1[1];
+      gm[A][2] = g1[2] - g0[2];
+      const int c = rc[R];
+      double xv[K]; // bottom level (D0), top level (D0) of the lane's layer
+#pragma unroll
+      for (int d = 0; d < D0; ++d) {
+        xv[d] = e[sl * D0 + d];
+        xv[D0 + d] = e[(sl + 1) * D0 + d];
+      }
+      __syncwarp();
+      rc[R] = fetch(k + kSrDepth, R);
+      // warp-uniform: every lane of the segment takes part in the shuffle
+      const bool cell = act && c >= 0;
+      if (__any_sync(FULL, cell)) {
+        const double det = prism_abs_detj_12(gm[0][0], gm[0][1], gm[0][2],
+                                             gm[1][0], gm[1][1], gm[1][2],
+                                             gm[2][0], gm[2][1], gm[2][2]);
+        const double dd = (cell && sl < nl) ? det : 0.0;
+        double out[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int j = 0; j < K; ++j) sacc = fma(M.m[i * K + j], xv[j], sacc);
+          out[i] = dd * sacc;
+        }
+        double *col = y + (int64_t)(cell ? c : 0) * fcol;
+#pragma unroll
+        for (int d = 0; d < D0; ++d) {
+          // level l0 + sl: own bottom part + the lane below's top part
+          const double below = __shfl_up_sync(FULL, out[D0 + d], 1, W);
+          double *p = col + (int64_t)(l0 + sl) * D0 + d;
+          if (cell && sl < nl) {
+            if (sl > 0)
+              *p = out[d] + below;
+            else if (bot_add)
+              atomicAdd(p, out[d]);
+            else
+              *p = out[d];
+          }
+          if (cell && sl == nl - 1) { // the chunk's top level
+            double *pt = p + D0;
+            if (top_add)
+              atomicAdd(pt, out[D0 + d]);
+            else
+              *pt = out[D0 + d];
+          }
+        }
+      }
+    };
+    using S0 = std::integral_constant<int, 0>;
+    using S1 = std::integral_constant<int, 1>;
+    using S2 = std::integral_constant<int, 2>;
+    for (int k = 0; k < maxlen; k += 3) {
+      step(S0{}, S0{}, k);
+      step(S1{}, S1{}, k + 1);
+      step(S2{}, S2{}, k + 2);
+    }
+    sr_wait<0>();
+  }
+}
+
+// zero the chunk-boundary levels (l = W, 2W, ... < layers) of every cell
+// column with level DoFs: the two chunks meeting there add into them
+__global__ void k_zero_cell_levels(double *__restrict__ y, int64_t n_cells,
+                                   int layers, int d0, int w, int nb) {
+  const int64_t n = n_cells * nb * d0;
+  const int64_t fcol = (int64_t)d0 * (layers + 1);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / (nb * d0);
+    const int r = (int)(t - c * nb * d0);
+    y[c * fcol + (int64_t)(r / d0 + 1) * w * d0 + r % d0] = 0.0;
+  }
+}
+
+template <int D0, int W>
+static int strip_dgv_launch(const double *mref, const int32_t *strip_ptr,
+                            const int32_t *steps, const int32_t *step_cells,
+                            int64_t n_strips, int64_t n_cells, int layers,
+                            const double *coords, const double *x, double *y,
+                            cudaStream_t s) {
+  constexpr int SEGS = 32 / W, NW = kSdThreads / 32, K = 2 * D0;
+  MassMat<K> M;
+  for (int i = 0; i < K * K; ++i) M.m[i] = mref[i] * (1.0 / 12.0);
+  const int nb = (layers + W - 1) / W - 1; // interior chunk boundaries
+  if (nb > 0 && n_cells > 0) {
+    k_zero_cell_levels<<<grid_for(n_cells * nb * D0, 256, 4), 256, 0, s>>>(
+        y, n_cells, layers, D0, W, nb);
+    PM_LAUNCH_CHECK("k_zero_cell_levels");
+  }
+  const size_t smem =
+      sizeof(double) * ((size_t)NW * kSrDepth * SEGS + 1) * sv_entry<D0, W>() +
+      sizeof(int) * NW * SEGS * 2 * kSrIds;
+  static int cached_dev = -1;
+  int dev = 0;
+  PM_CUDA_TRY(cudaGetDevice(&dev));
+  if (cached_dev != dev) {
+    PM_CUDA_TRY(cudaFuncSetAttribute(
+        k_strip_dgv<D0, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (int)smem));
+    cached_dev = dev;
+  }
+  const int64_t items = n_strips * ((layers + W - 1) / W);
+  const int64_t warps = (items + SEGS - 1) / SEGS;
+  const unsigned grid = grid_for(warps * 32, kSdThreads, strip_grid_cap(8));
+  k_strip_dgv<D0, W><<<grid, kSdThreads, smem, s>>>(
+      M, strip_ptr, steps, step_cells, n_strips, layers, coords, x, y);
+  PM_LAUNCH_CHECK("k_strip_dgv");
+  return PM_OK;
+}
+
+template <int D0>
+static int strip_dgv_w(const double *mref, int W, const int32_t *strip_ptr,
+                       const int32_t *steps, const int32_t *step_cells,
+                       int64_t n_strips, int64_t n_cells, int layers,
+                       const double *coords, const double *x, double *y,
+                       cudaStream_t s) {
+  switch (W) {
+  case 32: return strip_dgv_launch<D0, 32>(mref, strip_ptr, steps, step_cells,
+                                           n_strips, n_cells, layers, coords,
+                                           x, y, s);
+  case 16: return strip_dgv_launch<D0, 16>(mref, strip_ptr, steps, step_cells,
+                                           n_strips, n_cells, layers, coords,
+                                           x, y, s);
+  case 8: return strip_dgv_launch<D0, 8>(mref, strip_ptr, steps, step_cells,
+                                         n_strips, n_cells, layers, coords,
+                                         x, y, s);
+  default:
+    set_error("strip chunk width must be 8, 16 or 32 (got %d)", W);
+    return PM_EINVAL;
+  }
+}
+
 } // namespace pm
 
 static int strip_red_entry(
@@ -1851,13 +2113,40 @@ extern "C" int pm_column_mass_patch_strips(
 }
 
 extern "C" int pm_column_mass_strip_dg(
-    const int32_t *delta6, int32_t k, int32_t layers, const double *coords,
+    const int32_t *delta6, int32_t k, int64_t n_cells, int32_t layers,
+    const double *coords,
     const double *mref, const double *x, double *y, int64_t n_strips,
     int32_t chunk, const int32_t *strip_ptr, const int32_t *steps,
     const int32_t *step_cells, void *stream) {
   pm::clear_error();
-  const bool dg_only = delta6 && !delta6[0] && !delta6[1] && !delta6[2] &&
-                       !delta6[3] && !delta6[4] && delta6[5] == k;
+  const bool cells_only = delta6 && !delta6[0] && !delta6[1] && !delta6[2] &&
+                          !delta6[3];
+  const bool dg_only = cells_only && !delta6[4] && delta6[5] == k;
+  const bool levels_only = cells_only && !delta6[5] && 2 * delta6[4] == k;
+  if (levels_only && layers >= 1 && n_strips >= 0 && mref) {
+    if (n_strips == 0) return PM_OK;
+    if (!coords || !x || !y || !strip_ptr || !steps || !step_cells) {
+      pm::set_error("NULL device pointer");
+      return PM_EINVAL;
+    }
+    if (n_cells < 0) {
+      pm::set_error("pm_column_mass_strip_dg: n_cells < 0");
+      return PM_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (delta6[4]) {
+    case 1: return pm::strip_dgv_w<1>(mref, chunk, strip_ptr, steps,
+                                      step_cells, n_strips, n_cells, layers,
+                                      coords, x, y, s);
+    case 3: return pm::strip_dgv_w<3>(mref, chunk, strip_ptr, steps,
+                                      step_cells, n_strips, n_cells, layers,
+                                      coords, x, y, s);
+    default:
+      pm::set_error("pm_column_mass_strip_dg: %d DoFs per cell level (1 or "
+                    "3 compiled)", delta6[4]);
+      return PM_EINVAL;
+    }
+  }
   if (!dg_only || layers < 1 || n_strips < 0 || !mref) {
     pm::set_error("pm_column_mass_strip_dg: a DG layout (DoFs on the prism "
                   "cells only, k = delta(2,1)) and layers >= 1");

@@ -184,6 +184,10 @@ class MassOperator:
         """Column-loop kernel launches one ``apply`` issues."""
         if self.schedule in ("colored", "sequential") and self.share == 2:
             return self._color_lists()[1].shape[0] - 1
+        d = self.fs.layout.delta6()
+        if self.stripdg_ok and d[4] and self.schedule in ("auto", "stripdg") \
+                and self.layers > strip_chunk_width(self.layers):
+            return 2    # chunk-boundary level zeroing + the strip kernel
         if self.schedule in ("auto", "patch", "stripred", "strip",
                              "pstrip") and \
                 self.share == 2:
@@ -439,6 +443,18 @@ class MassOperator:
             self._gstrips = g
         return self._gstrips
 
+    @property
+    def stripdg_ok(self) -> bool:
+        """Cell-only layouts the DG strip kernel compiles: DoFs on (2,1)
+        only (1, 2, 3 or 6 per cell-layer) or on (2,0) only (1 or 3 per
+        cell level)."""
+        d = self.fs.layout.delta6()
+        if d[0] or d[1] or d[2] or d[3]:
+            return False
+        if not d[4]:
+            return d[5] in (1, 2, 3, 6)
+        return not d[5] and d[4] in (1, 3)
+
     def _dg_strips(self):
         """Global strips + the cell of every step (cached), for the DG
         strip kernel."""
@@ -561,12 +577,15 @@ class MassOperator:
             accumulate = False
         if not self.kron_ok and sched not in ("stream", "stripdg"):
             sched = "atomic"   # dense Mref in the generic kernel
-        if sched == "auto" and self.dg_only and self.k in (1, 2, 3):
-            # few DoFs per cell-layer: walking the cells along strips loads
-            # each vertex's coordinates once per strip instead of gathering
-            # six prism vertices per cell-layer (measured: DG0xDG0 +54 %,
-            # DG0xDG1 +20 %, DG1xDG0 +6 % at 100 layers; the stream kernel
-            # stays ahead for DG1xDG1, profiles/README.md)
+        if sched == "auto" and self.stripdg_ok and \
+                not (self.dg_only and self.k == 6):
+            # cell-only layouts with few DoFs per cell-layer: walking the
+            # cells along strips loads each vertex's coordinates once per
+            # strip instead of gathering six prism vertices per cell-layer
+            # (measured at 100 layers: DG0xDG0 +54 %, DG0xDG1 +20 %,
+            # DG1xDG0 +6 % over the stream kernel, DG0xCG1 +44 %, DG1xCG1
+            # +12 % over the cell-stream kernel; DG1xDG1 keeps the stream
+            # kernel, profiles/README.md)
             sched = "stripdg"
         if sched == "auto" and self.share == 2:
             # measured fastest (profiles/): global strips for vertex-column
@@ -587,22 +606,18 @@ class MassOperator:
                                        n_vertices=self.fs.mesh.base.num_vertices)
             return y
         if sched == "stripdg":
-            if not self.dg_only or self.k not in (1, 2, 3, 6):
+            if not self.stripdg_ok:
                 raise ValueError(
                     f"the DG strip schedule needs DoFs on the prism cells "
-                    f"only (1, 2, 3 or 6 per cell-layer), got "
-                    f"{self.fs.layout.name}")
+                    f"only (1, 2, 3 or 6 per cell-layer, or 1 or 3 per "
+                    f"cell level), got {self.fs.layout.name}")
             strips, W = self._dg_strips()
-            if not accumulate:
-                _lib.column_mass_strip_dg(self.fs.layout, self.k,
-                                          self.layers, coords, self.mref, x,
-                                          y, strips, W, stream=stream)
-            else:
-                tmp = torch.empty_like(y)
-                _lib.column_mass_strip_dg(self.fs.layout, self.k,
-                                          self.layers, coords, self.mref, x,
-                                          tmp, strips, W, stream=stream)
-                y += tmp
+            out = torch.empty_like(y) if accumulate else y
+            _lib.column_mass_strip_dg(self.fs.layout, self.k, self.n_cells,
+                                      self.layers, coords, self.mref, x,
+                                      out, strips, W, stream=stream)
+            if accumulate:
+                y += out
             return y
         if sched == "tile":
             if not self.tile_ok:

@@ -145,7 +145,8 @@ def _schedule_applies(lname, schedule):
     if schedule in ("stripred", "pstrip"):
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1", "P2xP2")
     if schedule == "stripdg":
-        return lname in ("DG0xDG0", "DG0xDG1", "DG1xDG0", "DG1xDG1")
+        return lname in ("DG0xDG0", "DG0xDG1", "DG1xDG0", "DG1xDG1",
+                         "DG0xCG1", "DG1xCG1")
     return True
 
 
@@ -463,14 +464,19 @@ def test_host_pipelined_mass_action(lname, layers, n):
     yh = torch.empty_like(xh).pin_memory()
     got = mass_action(fs, xh, coords, operator=op, out=yh).numpy()
     dev = op.apply(torch.from_numpy(x).cuda(), coords).cpu().numpy()
-    if lname.startswith("DG"):   # deterministic kernels: bitwise equal
-        assert np.array_equal(got, dev)
+    if lname.startswith("DG"):
+        # the host path streams DG fields by cell ranges (the stream
+        # kernel): bitwise equal to it; the device default may walk strips
+        # (stripdg) with another operation order
+        dev_s = op.apply(torch.from_numpy(x).cuda(), coords,
+                         schedule="stream").cpu().numpy()
+        assert np.array_equal(got, dev_s)
     assert _rel(got, dev) <= _tol(lname)
     assert _rel(got, _oracle_for(w, fs).assemble(x)) <= _tol(lname)
 
 
 @pytest.mark.parametrize("lname", ("DG0xDG0", "DG0xDG1", "DG1xDG0",
-                                   "DG1xDG1"))
+                                   "DG1xDG1", "DG0xCG1", "DG1xCG1"))
 @pytest.mark.parametrize("ordering", ("rcm", "random"))
 @pytest.mark.parametrize("layers", (1, 7, 16, 33, 64, 100))
 def test_dg_strips(lname, ordering, layers):
@@ -491,6 +497,7 @@ def test_dg_strips(lname, ordering, layers):
     op.apply(xd, coords, y)
     yh = y.cpu().numpy()
     assert np.isfinite(yh).all()
-    assert _rel(yh, ref) <= 1e-12
+    tol = 1e-12 if lname.endswith("DG0") or lname.endswith("DG1") else 1e-10
+    assert _rel(yh, ref) <= tol
     y2 = op.apply(xd, coords, y, accumulate=True)
-    assert _rel(y2.cpu().numpy(), 2 * ref) <= 1e-12
+    assert _rel(y2.cpu().numpy(), 2 * ref) <= tol
