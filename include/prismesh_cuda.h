@@ -310,6 +310,8 @@ int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                            const int32_t *cell_vertices,
                            const int32_t *cell_edges,
                            const uint8_t *cell_mask /* NULL: all cells */,
+                           const int32_t *scan_order /* NULL: index order;
+                              else the cells in the order strips start */,
                            int32_t max_len, int32_t *strip_ptr,
                            int32_t *steps,
                            int32_t *steps_e /* NULL, or 2 edges per step */,

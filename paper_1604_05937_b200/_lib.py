@@ -75,7 +75,8 @@ SIGNATURES = {
                                                ctypes.POINTER(_f64), _vp,
                                                _vp, _vp]),
     "pm_build_global_strips": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp,
-                                              _i32, _vp, _vp, _vp, _vp]),
+                                              _vp, _i32, _vp, _vp, _vp,
+                                              _vp]),
     "pm_build_patch_strips": (ctypes.c_int, [_i64, _i64, _i64, _vp, _vp, _vp,
                                              _vp, _i64, _i32, _vp, _vp, _vp,
                                              _vp, _vp, _vp]),
@@ -348,12 +349,16 @@ def column_mass_strip(layout, k, layers, coords, mref, x, y, plan, dplan,
 
 
 def build_global_strips(base, max_len=32, cells=None, edges=False,
-                        order=None):
+                        order=None, scan=None):
     """(strip_ptr int32, steps int32[, steps_e int32 (n_steps, 2)]):
     sequential strips over the mesh or over the subset ``cells`` (host
     C++); with ``edges`` also the two window edges each step brings in.
     ``order``: "morton" (default, PM_STRIP_ORDER), "rcm" (mean vertex id)
-    or "creation" (as built: each strip starts at the lowest unused cell)."""
+    or "creation" (as built).  ``scan``: the order in which strips start
+    at unused cells -- "index" (cell index order: the bands of an
+    RCM-ordered mesh), "morton" (centroid Morton order, for meshes whose
+    cell order is not spatially coherent), or None (PM_STRIP_SCAN, default
+    "auto": Morton when index-order strips come out short)."""
     cv = np.ascontiguousarray(base.cell_vertices, dtype=np.int32)
     ce = np.ascontiguousarray(base.cell_edges, dtype=np.int32)
     n = cv.shape[0]
@@ -365,12 +370,32 @@ def build_global_strips(base, max_len=32, cells=None, edges=False,
     st = np.zeros(3 * n + 3, dtype=np.int32)
     se = np.zeros((3 * n + 3, 2), dtype=np.int32) if edges else None
     tot = np.zeros(2, dtype=np.int64)
-    check(host_lib().pm_build_global_strips(
-        n, base.num_edges, cv.ctypes.data_as(_i32p), ce.ctypes.data_as(_i32p),
-        None if mask is None else mask.ctypes.data_as(ctypes.c_void_p),
-        max_len, sp.ctypes.data_as(_i32p), st.ctypes.data_as(_i32p),
-        None if se is None else se.ctypes.data_as(_i32p),
-        tot.ctypes.data_as(_i64p)))
+
+    def run(scan_order):
+        check(host_lib().pm_build_global_strips(
+            n, base.num_edges, cv.ctypes.data_as(_i32p),
+            ce.ctypes.data_as(_i32p),
+            None if mask is None else mask.ctypes.data_as(ctypes.c_void_p),
+            None if scan_order is None else
+            scan_order.ctypes.data_as(ctypes.c_void_p),
+            max_len, sp.ctypes.data_as(_i32p), st.ctypes.data_as(_i32p),
+            None if se is None else se.ctypes.data_as(_i32p),
+            tot.ctypes.data_as(_i64p)))
+
+    def morton_scan():
+        from .schedule import morton_order
+        cent = np.asarray(base.coords)[cv].mean(axis=1)
+        return np.ascontiguousarray(morton_order(cent), dtype=np.int32)
+
+    mode = scan or os.environ.get("PM_STRIP_SCAN", "auto")
+    run(morton_scan() if mode == "morton" else None)
+    if mode == "auto" and tot[0] > 0 and max_len >= 8:
+        # index-order strips on a mesh whose cell order is not spatially
+        # coherent (e.g. a random vertex order) come out short: rebuild
+        # them starting in the Morton order of the cell centroids
+        cells_per = (tot[1] - 2 * tot[0]) / tot[0]
+        if cells_per < 0.5 * max_len:
+            run(morton_scan())
     sp, st = sp[:tot[0] + 1].copy(), st[:tot[1]].copy()
     if se is not None:
         se = se[:tot[1]].copy()

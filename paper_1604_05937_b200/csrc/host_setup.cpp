@@ -323,6 +323,7 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                                       const int32_t *cell_vertices,
                                       const int32_t *cell_edges,
                                       const uint8_t *cell_mask,
+                                      const int32_t *scan_order,
                                       int32_t max_len, int32_t *strip_ptr,
                                       int32_t *steps, int32_t *steps_e,
                                       int64_t *totals) {
@@ -370,10 +371,15 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
   };
   int64_t n_strips = 0, n_steps = 0, scan = 0;
   strip_ptr[0] = 0;
+  // strips start at the first unused cell of the scan order (default: cell
+  // index order, which follows the bands of an RCM-ordered mesh)
+  auto at = [&](int64_t i) -> int64_t {
+    return scan_order ? (int64_t)scan_order[i] : i;
+  };
   while (true) {
-    while (scan < n_cells && used[scan]) ++scan;
+    while (scan < n_cells && used[at(scan)]) ++scan;
     if (scan >= n_cells) break;
-    int64_t cur = scan;
+    int64_t cur = at(scan);
     used[cur] = 1;
     int32_t win[3] = {vid(cur, 0), vid(cur, 1), vid(cur, 2)};
     int64_t next = -1;

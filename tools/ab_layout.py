@@ -14,7 +14,8 @@ from paper_1604_05937_b200.perfbench import valuable_volume
 
 lname, n, layers = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 quad = {"P2xP2": (6, 6)}.get(lname, (2, 2))
-w = configs.Workload("ab", n, layers, lname, quad)
+w = configs.Workload("ab", n, layers, lname, quad,
+                     ordering=os.environ.get("AB_ORDERING", "rcm"))
 fs, q, x_np, _ = configs.build(w)
 m = fs.mesh
 coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
