@@ -501,3 +501,33 @@ def test_dg_strips(lname, ordering, layers):
     assert _rel(yh, ref) <= tol
     y2 = op.apply(xd, coords, y, accumulate=True)
     assert _rel(y2.cpu().numpy(), 2 * ref) <= tol
+
+
+@pytest.mark.parametrize("lname", ("DG0xDG0", "DG1xDG0", "DG0xCG1",
+                                   "DG1xCG1"))
+@pytest.mark.parametrize("ordering", ("rcm", "random"))
+def test_dg_strips_medium(lname, ordering):
+    """The cell-only strip kernels where they are the default, on a mesh
+    with long strips, many items and several layer chunks (128^2, 70
+    layers: W = 32, three chunks, the last one ragged), against the
+    oracle's column loop (oracle/fast.py)."""
+    from oracle import fast
+    from paper_1604_05937_b200 import configs, extrude_coordinates
+    from paper_1604_05937_b200.configs import layout_of
+    from paper_1604_05937_b200.kernels import MassOperator
+    w = configs.Workload("sdgm", 128, 70, lname, quad_degrees(lname),
+                         ordering=ordering)
+    fs, quad, x, _ = configs.build(w)
+    m = fs.mesh
+    op = MassOperator(fs, quad)
+    coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
+    xd = torch.from_numpy(x).cuda()
+    y = torch.full_like(xd, float("nan"))
+    op.apply(xd, coords, y)
+    assert op.last_schedule == "stripdg"
+    tri, line, nc = families(lname)
+    arm = fast.FastMass(m.base, m.layers, layout_of(lname).counts, tri, line,
+                        nc, *quad_degrees(lname))
+    ref = arm.apply(x)
+    tol = 1e-12 if lname.endswith(("DG0", "DG1")) else 1e-10
+    assert _rel(y.cpu().numpy(), ref) <= tol
