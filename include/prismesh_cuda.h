@@ -25,8 +25,10 @@
  *   pm_column_mass_strip_red <- same, global strips + REDG
  *   pm_build_global_strips   <- host planner of that schedule
  *   pm_column_mass_tile      <- same, band tiles staged by TMA bulk copies
+ *                               (experimental: PM_EXPERIMENTAL=1 builds)
  *   pm_tiles_build / _info / _export / _free <- host planner of that schedule
  *   pm_column_mass_patch_strips <- same, store-first strips inside patches
+ *                               (experimental: PM_EXPERIMENTAL=1 builds)
  *   pm_build_patch_strips    <- host planner of that schedule
  *   pm_column_mass_dg_range  <- the DG loop over a cell range (pipelining)
  *   pm_column_probe          <- SPEC.md:338-340 counting / gather kernels
@@ -37,7 +39,10 @@
  *   pm_rcm_order             <- pkg/src/prismesh/ordering.py:45-90 (host BFS)
  *   pm_rcm_order_device      <- pkg/src/prismesh/ordering.py:45-90 (device walk)
  *   pm_stencil_*             <- SPEC.md:322-341 StencilKernel.apply (user kernels)
- *   pm_column_mass_strip_dg  <- SPEC.md:333-341 iterate_columns, DG layouts along strips
+ *   pm_column_mass_strip_dg  <- SPEC.md:333-341 iterate_columns, cell-only
+ *                               (DG x DG, DG x CG1) layouts along strips
+ *   pm_strip_step_cells      <- host planner of that schedule (cell per step)
+ *   pm_build_flags           <- (build features: experimental schedules)
  */
 #ifndef PRISMESH_CUDA_H
 #define PRISMESH_CUDA_H
