@@ -322,6 +322,41 @@ int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
                            int32_t *steps_e /* NULL, or 2 edges per step */,
                            int64_t *totals);
 
+/* Run strips: the same plan with the start orientation of a strip chosen
+ * so that its even and its odd vertices each continue by consecutive ids
+ * (steps[k+2] == steps[k] + 1).  On a level-ordered mesh (RCM,
+ * ordering.py:45-90) such a strip follows the band between two BFS levels
+ * and, under Alg. 1 (fspace.py:141-147: consecutive vertex ids are
+ * consecutive columns), its vertex columns are two contiguous slabs of the
+ * field.  A first pass starts strips only at cells that have such a start
+ * (walking back to the band's first free cell), a second pass covers the
+ * rest by the plain rule.  Same arguments and capacities as
+ * pm_build_global_strips. */
+int pm_build_run_strips(int64_t n_cells, int64_t n_edges,
+                        const int32_t *cell_vertices,
+                        const int32_t *cell_edges, const uint8_t *cell_mask,
+                        const int32_t *scan_order, int32_t max_len,
+                        int32_t *strip_ptr, int32_t *steps, int32_t *steps_e,
+                        int64_t *totals);
+
+/* y (+)= M x over sequential strips for P1 (delta6 = {1,0,0,0,0,0}) and
+ * 3-vector P1 ({3,0,0,0,0,0}) columns of at most 128 layers: the strip walk
+ * of pm_column_mass_strip_red (dof =
+ * column origin + l * offset), with the vertex columns brought into shared
+ * memory by 1-D bulk copies (cp.async.bulk), one copy per run of up to 4
+ * consecutive vertex ids per strip side, into a ring shared by the warps
+ * that walk the column's 32-layer chunks.  Any strip plan is valid; run
+ * strips (pm_build_run_strips) make the copies large.  x and coords must be
+ * 16-byte aligned; mtri must be invariant under vertex permutations.
+ * Zeroes y first unless `accumulate`. */
+int pm_column_mass_strip_tma(const int32_t *delta6, int32_t k, int32_t layers,
+                             const double *coords, const double *mtri,
+                             const double *mline, const double *x, double *y,
+                             int64_t n_dofs, int32_t accumulate,
+                             int64_t n_strips, const int32_t *strip_ptr,
+                             const int32_t *steps, int64_t n_vertices,
+                             void *stream);
+
 /* Store-first patch strips (PM_VARIANT_STRIPRED over patches): the cells
  * are grouped into compact patches (patch_cells, patch_ptr: e.g. runs of the
  * Morton order of the centroids) and walked as sequential strips that never

@@ -77,6 +77,14 @@ SIGNATURES = {
     "pm_build_global_strips": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp,
                                               _vp, _i32, _vp, _vp, _vp,
                                               _vp]),
+    "pm_column_mass_strip_tma": (ctypes.c_int, [_i32p, _i32, _i32, _vp,
+                                                ctypes.POINTER(_f64),
+                                                ctypes.POINTER(_f64), _vp,
+                                                _vp, _i64, _i32, _i64, _vp,
+                                                _vp, _i64, _vp]),
+    "pm_build_run_strips": (ctypes.c_int, [_i64, _i64, _vp, _vp, _vp,
+                                           _vp, _i32, _vp, _vp, _vp,
+                                           _vp]),
     "pm_build_patch_strips": (ctypes.c_int, [_i64, _i64, _i64, _vp, _vp, _vp,
                                              _vp, _i64, _i32, _vp, _vp, _vp,
                                              _vp, _vp, _vp]),
@@ -349,7 +357,7 @@ def column_mass_strip(layout, k, layers, coords, mref, x, y, plan, dplan,
 
 
 def build_global_strips(base, max_len=32, cells=None, edges=False,
-                        order=None, scan=None):
+                        order=None, scan=None, runs=False):
     """(strip_ptr int32, steps int32[, steps_e int32 (n_steps, 2)]):
     sequential strips over the mesh or over the subset ``cells`` (host
     C++); with ``edges`` also the two window edges each step brings in.
@@ -372,7 +380,9 @@ def build_global_strips(base, max_len=32, cells=None, edges=False,
     tot = np.zeros(2, dtype=np.int64)
 
     def run(scan_order):
-        check(host_lib().pm_build_global_strips(
+        build = host_lib().pm_build_run_strips if runs else \
+            host_lib().pm_build_global_strips
+        check(build(
             n, base.num_edges, cv.ctypes.data_as(_i32p),
             ce.ctypes.data_as(_i32p),
             None if mask is None else mask.ctypes.data_as(ctypes.c_void_p),
@@ -387,7 +397,9 @@ def build_global_strips(base, max_len=32, cells=None, edges=False,
         cent = np.asarray(base.coords)[cv].mean(axis=1)
         return np.ascontiguousarray(morton_order(cent), dtype=np.int32)
 
-    mode = scan or os.environ.get("PM_STRIP_SCAN", "auto")
+    # (run strips follow the id bands: index order, no Morton rebuild)
+    mode = scan or ("index" if runs else
+                    os.environ.get("PM_STRIP_SCAN", "auto"))
     run(morton_scan() if mode == "morton" else None)
     if mode == "auto" and tot[0] > 0 and max_len >= 8:
         # index-order strips on a mesh whose cell order is not spatially
@@ -502,6 +514,21 @@ def column_mass_strip_red(layout, k, layers, coords, mref, x, y, n_dofs,
         _f64ptr(m), _f64ptr(mt), _f64ptr(ml), ptr(x, x_base), ptr(y, y_base),
         n_dofs, 1 if accumulate else 0, sp.shape[0] - 1, chunk, ptr(sp),
         ptr(st), ptr(se), n_vertices, stream_ptr(stream))
+    check(rc)
+
+
+def column_mass_strip_tma(layout, k, layers, coords, x, y, n_dofs, strips,
+                          kron, accumulate=False, stream=None, n_vertices=0):
+    """pm_column_mass_strip_tma: the run-strip kernel (bulk copies of whole
+    vertex columns), P1 / 3-vector P1, at most 128 layers."""
+    mt = np.ascontiguousarray(kron[0], dtype=np.float64).ravel()
+    ml = np.ascontiguousarray(kron[1], dtype=np.float64).ravel()
+    d = layout.delta6()
+    sp, st = strips[0], strips[1]
+    rc = host_lib().pm_column_mass_strip_tma(
+        d.ctypes.data_as(_i32p), k, layers, ptr(coords), _f64ptr(mt),
+        _f64ptr(ml), ptr(x), ptr(y), n_dofs, 1 if accumulate else 0,
+        sp.shape[0] - 1, ptr(sp), ptr(st), n_vertices, stream_ptr(stream))
     check(rc)
 
 

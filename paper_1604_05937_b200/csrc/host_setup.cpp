@@ -319,14 +319,20 @@ extern "C" int pm_build_strips(
 // first unused cell in index order (RCM order keeps concurrent strips
 // local), steps = global vertex ids (3 fills, then one per cell).
 // ---------------------------------------------------------------------------
-extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
-                                      const int32_t *cell_vertices,
-                                      const int32_t *cell_edges,
-                                      const uint8_t *cell_mask,
-                                      const int32_t *scan_order,
-                                      int32_t max_len, int32_t *strip_ptr,
-                                      int32_t *steps, int32_t *steps_e,
-                                      int64_t *totals) {
+// `runs`: a strip's start orientation prefers the one whose even and odd
+// vertices each continue by consecutive ids (v[k+2] == v[k] + 1): on a
+// level-ordered (RCM) mesh the strip then follows the band between two BFS
+// levels and its vertex columns are two contiguous slabs of the field, which
+// the bulk-copy strip kernel (csrc/strip_tma.cu) fetches several columns
+// per copy.
+static int build_global_strips_impl(int64_t n_cells, int64_t n_edges,
+                                    const int32_t *cell_vertices,
+                                    const int32_t *cell_edges,
+                                    const uint8_t *cell_mask,
+                                    const int32_t *scan_order,
+                                    int32_t max_len, int32_t *strip_ptr,
+                                    int32_t *steps, int32_t *steps_e,
+                                    int64_t *totals, bool runs) {
   pm::clear_error();
   if (n_cells < 0 || n_edges < 0 || max_len < 1) {
     pm::set_error("pm_build_global_strips: bad arguments");
@@ -376,6 +382,10 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
   auto at = [&](int64_t i) -> int64_t {
     return scan_order ? (int64_t)scan_order[i] : i;
   };
+  // runs: a first pass starts strips only where both id runs continue (the
+  // other cells wait, so a strip across the bands cannot cut every band at
+  // its end); the second pass takes what is left by the plain rule
+  for (int pass = runs ? 0 : 1; pass < 2; ++pass, scan = 0)
   while (true) {
     while (scan < n_cells && used[at(scan)]) ++scan;
     if (scan >= n_cells) break;
@@ -394,12 +404,38 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
         const int32_t nv = third(j, u, w);
         const int64_t j2 = across(j, w, nv);
         // prefer a continuation; then the lower-index neighbour
-        const int score = (j2 >= 0 && !used[j2] && j2 != cur) ? 2 : 1;
+        int score = (j2 >= 0 && !used[j2] && j2 != cur) ? 2 : 1;
+        // (runs) the strip a0, u, w, nv, ... continues both id runs
+        if (runs && w == a0 + 1 && nv == u + 1) score += 2;
         if (score > best) {
           best = score;
           next = j;
           win[0] = a0, win[1] = u, win[2] = w;
         }
+      }
+    }
+    if (pass == 0 && best < 3) { // no run start here: second pass
+      used[cur] = 0;
+      ++scan;
+      continue;
+    }
+    if (pass == 0) {
+      // walk back along the band while both runs also continue downwards,
+      // so the strip starts at the band's first free cell
+      int64_t back = cur;
+      for (int32_t n = 1; n < max_len; ++n) {
+        const int64_t j = across(back, win[0], win[1]);
+        if (j < 0 || used[j]) break;
+        const int32_t pv = third(j, win[0], win[1]);
+        if (pv != win[1] - 1) break;
+        win[2] = win[1], win[1] = win[0], win[0] = pv;
+        back = j;
+      }
+      if (back != cur) {
+        used[cur] = 0;
+        cur = back;
+        used[cur] = 1;
+        next = across(cur, win[1], win[2]);
       }
     }
     for (int k = 0; k < 3; ++k) {
@@ -438,6 +474,32 @@ extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
   totals[0] = n_strips;
   totals[1] = n_steps;
   return PM_OK;
+}
+
+extern "C" int pm_build_global_strips(int64_t n_cells, int64_t n_edges,
+                                      const int32_t *cell_vertices,
+                                      const int32_t *cell_edges,
+                                      const uint8_t *cell_mask,
+                                      const int32_t *scan_order,
+                                      int32_t max_len, int32_t *strip_ptr,
+                                      int32_t *steps, int32_t *steps_e,
+                                      int64_t *totals) {
+  return build_global_strips_impl(n_cells, n_edges, cell_vertices, cell_edges,
+                                  cell_mask, scan_order, max_len, strip_ptr,
+                                  steps, steps_e, totals, false);
+}
+
+extern "C" int pm_build_run_strips(int64_t n_cells, int64_t n_edges,
+                                   const int32_t *cell_vertices,
+                                   const int32_t *cell_edges,
+                                   const uint8_t *cell_mask,
+                                   const int32_t *scan_order,
+                                   int32_t max_len, int32_t *strip_ptr,
+                                   int32_t *steps, int32_t *steps_e,
+                                   int64_t *totals) {
+  return build_global_strips_impl(n_cells, n_edges, cell_vertices, cell_edges,
+                                  cell_mask, scan_order, max_len, strip_ptr,
+                                  steps, steps_e, totals, true);
 }
 
 // ---------------------------------------------------------------------------

@@ -43,7 +43,8 @@ import numpy as np
 from . import _lib
 
 SCHEDULES = ("auto", "atomic", "colored", "sequential", "column", "stream",
-             "patch", "strip", "stripred", "pstrip", "stripdg", "tile")
+             "patch", "strip", "stripred", "striptma", "pstrip", "stripdg",
+             "tile")
 
 
 @dataclass(frozen=True)

@@ -154,6 +154,7 @@ class MassOperator:
         self._patch = None
         self._strip = None
         self._gstrips = None
+        self._rstrips = None
         self._dgstrips = None
         self._pstrips = None
         self._tiles = None
@@ -444,6 +445,31 @@ class MassOperator:
         return self._gstrips
 
     @property
+    def striptma_ok(self) -> bool:
+        """Layouts and sizes the run-strip kernel takes: P1 / 3-vector P1
+        columns of at most 128 layers."""
+        d = tuple(int(v) for v in self.fs.layout.delta6())
+        return d in ((1, 0, 0, 0, 0, 0), (3, 0, 0, 0, 0, 0)) and \
+            self.strip_invariant and self.layers <= 128
+
+    def _run_strips(self):
+        """Strips along the vertex-id bands (pm_build_run_strips, cached)
+        and the fraction of steps whose vertex continues its side's id run:
+        (device (strip_ptr, steps), fraction)."""
+        if self._rstrips is None:
+            import numpy as np
+            import torch
+            sp, st = _lib.build_global_strips(
+                self.fs.mesh.base, runs=True,
+                max_len=strip_max_len(self.n_cells, self.layers))
+            d2 = st[2:] == st[:-2] + 1
+            # (pairs across a strip boundary: 2 of each strip's steps)
+            frac = float(d2.sum()) / max(1, len(st) - 2 * (len(sp) - 1))
+            self._rstrips = (tuple(torch.from_numpy(a).to(self._dev)
+                                   for a in (sp, st)), frac)
+        return self._rstrips
+
+    @property
     def stripdg_ok(self) -> bool:
         """Cell-only layouts the DG strip kernel compiles: DoFs on (2,1)
         only (1, 2, 3 or 6 per cell-layer) or on (2,0) only (1 or 3 per
@@ -603,6 +629,18 @@ class MassOperator:
                                        coords, self.mref, x, y, n, strips,
                                        self.kron, W, accumulate=accumulate,
                                        stream=stream,
+                                       n_vertices=self.fs.mesh.base.num_vertices)
+            return y
+        if sched == "striptma":
+            if not self.striptma_ok:
+                raise ValueError(
+                    f"the run-strip schedule takes P1 / 3-vector P1 columns "
+                    f"of at most 128 layers, got {self.fs.layout.name} with "
+                    f"{self.layers} layers")
+            strips, _ = self._run_strips()
+            _lib.column_mass_strip_tma(self.fs.layout, self.k, self.layers,
+                                       coords, x, y, n, strips, self.kron,
+                                       accumulate=accumulate, stream=stream,
                                        n_vertices=self.fs.mesh.base.num_vertices)
             return y
         if sched == "stripdg":

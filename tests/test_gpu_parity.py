@@ -127,7 +127,7 @@ def test_arity_and_mesh_mismatch_rejected(gmesh):
 
 
 SCHEDULES = ("auto", "atomic", "colored", "column", "patch", "strip",
-             "stripred", "pstrip", "stripdg")
+             "stripred", "striptma", "pstrip", "stripdg")
 
 
 def _experimental():
@@ -144,6 +144,8 @@ def _schedule_applies(lname, schedule):
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1")
     if schedule in ("stripred", "pstrip"):
         return lname in ("CG1xCG1", "CG1xDG0", "CG1xDG1", "VP1", "P2xP2")
+    if schedule == "striptma":
+        return lname in ("CG1xCG1", "VP1")
     if schedule == "stripdg":
         return lname in ("DG0xDG0", "DG0xDG1", "DG1xDG0", "DG1xDG1",
                          "DG0xCG1", "DG1xCG1")

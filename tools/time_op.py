@@ -14,7 +14,8 @@ w = configs.workload(sys.argv[1])
 fs, quad, x_np, _ = configs.build(w)
 m = fs.mesh
 coords = extrude_coordinates(m.base.coords, m.layers, m.layer_height)
-op = MassOperator(fs, quad)
+sched = os.environ.get("PM_SCHED", "auto")   # e.g. striptma
+op = MassOperator(fs, quad, schedule=sched)
 x = torch.from_numpy(x_np).cuda()
 y = torch.zeros_like(x)
 acc = "overwrite" not in sys.argv
