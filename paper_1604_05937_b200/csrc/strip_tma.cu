@@ -34,9 +34,24 @@
 #ifndef PM_TMA_MAXT_S
 #define PM_TMA_MAXT_S 512
 #endif
-#ifndef PM_TMA_MAXT_V
-#define PM_TMA_MAXT_V 384
+#ifndef PM_TMA_MAXT_S2 // scalar columns, two chunks per warp
+#define PM_TMA_MAXT_S2 256
 #endif
+#ifndef PM_TMA_MAXT_V
+#define PM_TMA_MAXT_V 256
+#endif
+// columns per strip side and copy: a granule of 2 G steps is a whole number
+// of window cycles (3 steps), so granule boundaries and table slots are
+// compile-time positions of the unrolled strip loop
+#ifndef PM_TMA_G
+#define PM_TMA_G 3
+#endif
+// 1: also compile the 3-stage rings (PM_TMA_NS=3 at run time; measured
+// slower on every config: fewer groups fit the shared memory)
+#ifndef PM_TMA_NS3
+#define PM_TMA_NS3 0
+#endif
+
 
 namespace pm {
 
@@ -65,15 +80,19 @@ __device__ __forceinline__ void stma_red(double *p, double v, bool on) {
                "@q red.global.add.f64 [%0], %1;\n\t}" ::"l"(p),
                "d"(v), "r"((int)on)); // y is never read: no memory clobber
 }
+__device__ __forceinline__ void stma_red_all(double *p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
 __device__ __forceinline__ void stma_group_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+constexpr int kStmaG = PM_TMA_G;
 constexpr uint32_t stma_up16(uint32_t b) { return (b + 15u) & ~15u; }
 
 // smem carve-up (bytes), shared by the kernel and the launcher
 struct StmaSmem {
-  uint32_t off_tab, bars, cnt, trow, ring, zero, total;
+  uint32_t off_tab, bars, cnt, tops, trow, ring, zero, total;
 };
 __host__ __device__ inline StmaSmem stma_smem(int NC, int G, int NS, int ngrp,
                                               int nwarp, uint32_t Pf,
@@ -83,28 +102,32 @@ __host__ __device__ inline StmaSmem stma_smem(int NC, int G, int NS, int ngrp,
   s.off_tab = o, o += (uint32_t)ngrp * NS * 2 * G * 16;
   s.bars = o, o += (uint32_t)ngrp * NS * 8;
   s.cnt = o, o += stma_up16((uint32_t)ngrp * NS * 4);
+  s.tops = o, o += NC > 1 ? 0 : (uint32_t)nwarp * 2 * G * 16;
   s.trow = o, o += NC > 1 ? (uint32_t)nwarp * 2 * (33 * NC + 1) * 8 : 0;
   o = (o + 127u) & ~127u;
   s.ring = o, o += (uint32_t)ngrp * NS * 2 * G * (Pf + Pc);
-  s.zero = o, o += (Pf > Pc ? Pf : Pc);
-  o += 1024; // lanes past a partial chunk read past their column (never used)
+  s.zero = o;
+  o += 2048; // lanes past a partial chunk read past their column (never used)
   s.total = o;
   return s;
 }
 
-template <int NC, int G, int NS, int NCH, int MAXT>
+template <int NC, int NQ, int NS, int NCH, int MAXT, bool FULL>
 __global__ void __launch_bounds__(MAXT, 1)
 k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
             const int32_t *__restrict__ steps, int64_t n_strips, int layers,
             const double *__restrict__ coords, const double *__restrict__ x,
             double *__restrict__ y, int ngrp, uint32_t Pf, uint32_t Pc,
             int64_t n_vertices) {
-  constexpr unsigned FULL = 0xffffffffu;
+  static_assert(NC == 1 || NQ == 1, "two chunks per warp: scalar columns");
+  constexpr unsigned FULL_MASK = 0xffffffffu;
   constexpr int CH = NC, NV = 2;
-  constexpr int G2 = 2 * G;
-  constexpr int TR = NC > 1 ? 33 * NC : 0;     // staged chunk row
-  constexpr int TRP = 33 * NC + 1;             // row pitch (doubles)
+  constexpr int G = kStmaG, G2 = 2 * G;
+  static_assert(G2 % 3 == 0, "granule = whole window cycles");
+  constexpr int TR = NC > 1 ? 33 * NC : 0; // staged chunk row
+  constexpr int TRP = 33 * NC + 1;         // row pitch (doubles)
   constexpr int NR = NC > 1 ? (TR + 31) / 32 : 1;
+  constexpr bool CSUM = NC == 1;
   extern __shared__ __align__(128) unsigned char stma_raw[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwarp = blockDim.x >> 5;
@@ -117,12 +140,16 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
   int *const cnt = reinterpret_cast<int *>(stma_raw + L.cnt) + grp * NS;
   double *const trow0 =
       reinterpret_cast<double *>(stma_raw + L.trow) + wib * 2 * TRP;
+  // scalar columns: the one top value per flush (the chunk's last lane) is
+  // parked here and added once per granule by 2G lanes, so the strip loop
+  // has no predicated RED (ptxas turns those into branches, which end its
+  // scheduling blocks: measured 2.96 -> 2.32 ms on C5a without them)
+  double *const topv = reinterpret_cast<double *>(stma_raw + L.tops) +
+                       wib * 2 * G2;
+  double **const topa = reinterpret_cast<double **>(topv + G2);
   const uint32_t SB = G2 * (Pf + Pc); // stage bytes
   const uint32_t ring_off = L.ring + (uint32_t)grp * NS * SB;
-  const uint32_t zero_off = L.zero;
 
-  for (uint32_t i = threadIdx.x; i < (L.total - L.zero) / 8; i += blockDim.x)
-    reinterpret_cast<double *>(stma_raw + L.zero)[i] = 0.0;
   if (threadIdx.x < (unsigned)(ngrp * NS)) {
     mbar_init(reinterpret_cast<uint64_t *>(stma_raw + L.bars) + threadIdx.x, 1);
     reinterpret_cast<int *>(stma_raw + L.cnt)[threadIdx.x] = 0;
@@ -132,41 +159,61 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
 
   const int colf = (layers + 1) * NC; // doubles per field column
   const int colc = (layers + 1) * 3;  // doubles per coordinate column
-  const int l0 = chunk * 32;
-  const int nl = min(32, layers - l0); // cell-layers of this warp's chunk
   const int sl = lane;
+  const int l0 = chunk * 32 * NQ; // first level of this warp's chunks
+  // lane predicates of the flushes: bottom values of live cell-layers, the
+  // top value of the last chunk's last cell-layer (the top of chunk 0 of
+  // two goes into chunk 1's lane 0: the launcher picks NQ = 2 only when
+  // every warp's second chunk is non-empty)
+  bool pb[NQ], pt;
+  int nlq[NQ], boff[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    nlq[q] = max(0, min(32, layers - (l0 + 32 * q)));
+    pb[q] = sl < nlq[q];
+    boff[q] = 32 * q * CH;
+  }
+  // Lanes past a partial last chunk are not predicated off (no branches in
+  // the strip loop): they add 0.0 at their natural address, which lies in
+  // the next vertex's column -- for the mesh's last vertex they step one
+  // column back instead (into the last column itself), so nothing is
+  // touched past the end of y.  (FULL: no such lanes.)
+  const bool dead_last = !pb[NQ - 1];
+  const int v_last = (int)n_vertices - 1;
+  pt = sl == nlq[NQ - 1] - 1;
+  const int nl = nlq[0]; // (NC > 1: NQ == 1)
   const double *const x_end = x + n_vertices * colf;
   const double *const c_end = coords + n_vertices * colc;
 
   // Refill: stage `st` <- granule `g` of the strip (steps k0 + 2G g ..).
-  // One converged warp; lane t < 2G looks after step 2G g + t.
-  // `v`: the lane's step id, loaded by the caller (a granule ahead).
-  auto refill = [&](int st, int g, int k0, int len, int v) {
+  // One converged warp; lane t < 2G looks after step 2G g + t, whose id `v`
+  // the caller loaded (a granule ahead).
+  auto refill = [&](int st, int g, int len, int v) {
     const int t = lane, k = G2 * g + t;
     const bool valid = t < G2 && k < len;
     const int side = t & 1, j = t >> 1;
-    const int vfirst = __shfl_sync(FULL, v, side);
+    const int vfirst = __shfl_sync(FULL_MASK, v, side);
     const unsigned sidemask = 0x55555555u << side;
-    const unsigned bad = __ballot_sync(FULL, valid && v != vfirst + j);
-    const unsigned vmask = __ballot_sync(FULL, valid);
+    const unsigned bad = __ballot_sync(FULL_MASK, valid && v != vfirst + j);
+    const unsigned vmask = __ballot_sync(FULL_MASK, valid);
     const bool consec = !(bad & sidemask);
     const int nside = __popc(vmask & sidemask);
     const uint32_t side_base = ring_off + (uint32_t)st * SB +
                                (uint32_t)side * G * (Pf + Pc);
     uint64_t *const bar = full + st;
     if (valid) {
-      const int vb = consec ? vfirst : v;      // first column of the copy
-      const int jb = consec ? 0 : j;           // its slot in the side
-      const int nb = consec ? nside : 1;       // columns in the copy
+      const int vb = consec ? vfirst : v; // first column of the copy
+      const int nb = consec ? nside : 1;  // columns in the copy
       const bool issue = !consec || j == 0;
       const double *fs = x + (int64_t)vb * colf;
       const double *cs = coords + (int64_t)vb * colc;
       const uint32_t fsh = (uint32_t)(reinterpret_cast<uintptr_t>(fs) >> 3) & 1;
       const uint32_t csh = (uint32_t)(reinterpret_cast<uintptr_t>(cs) >> 3) & 1;
       // consecutive columns lie back to back, single ones at the padded pitch
-      const uint32_t fdst = side_base + (consec ? 0u : (uint32_t)jb * Pf);
-      const uint32_t cdst = side_base + G * Pf + (consec ? 0u : (uint32_t)jb * Pc);
+      const uint32_t fdst = side_base + (consec ? 0u : (uint32_t)j * Pf);
+      const uint32_t cdst = side_base + G * Pf + (consec ? 0u : (uint32_t)j * Pc);
       StmaEntry e;
+      // (the lane's first value: level l0 + lane is added by the readers)
       e.foff = fdst + 8 * fsh + (consec ? (uint32_t)j * 8 * colf : 0u);
       e.coff = cdst + 8 * csh + (consec ? (uint32_t)j * 8 * colc : 0u);
       e.vid = v;
@@ -204,37 +251,35 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
     const int k0 = __ldg(strip_ptr + s);
     const int len = __ldg(strip_ptr + s + 1) - k0;
     const int ngran = (len + G2 - 1) / G2;
+    auto ids = [&](int g) { // the lane's step id of granule g
+      const int kk = G2 * g + lane;
+      return (lane < G2 && kk < len) ? __ldg(steps + k0 + kk) : 0;
+    };
     // every warp of the group is done with the previous strip's stages
     if constexpr (NCH > 1)
       stma_group_sync(1 + grp, NCH * 32);
     else
       __syncwarp();
     if (chunk == 0) {
-      for (int i = 0; i < NS && i < ngran; ++i) {
-        const int kk = G2 * i + lane;
-        refill((int)((gc + i) % NS), i, k0, len,
-               (lane < G2 && kk < len) ? __ldg(steps + k0 + kk) : 0);
-      }
+      for (int i = 0; i < NS && i < ngran; ++i)
+        refill((int)((gc + i) % NS), i, len, ids(i));
     }
     // ids of granule NS (refilled at the first release of this strip)
-    int vpre = 0;
-    {
-      const int kk = G2 * NS + lane;
-      vpre = (lane < G2 && kk < len) ? __ldg(steps + k0 + kk) : 0;
-    }
-    double zv[3][NC][NV], gm[3][3], acc[3][NC][NV];
-    constexpr bool CSUM = NC == 1;
-    double tr[CSUM ? 3 : 1], dr[CSUM ? 3 : 1][NC][NV];
+    int vpre = ids(NS);
+    double zv[NQ][3][NC][NV], gm[NQ][3][3], acc[CSUM ? 1 : 3][NC][NV];
+    double tr[CSUM ? NQ : 1][3], dr[CSUM ? NQ : 1][3][NC][NV];
 #pragma unroll
-    for (int a = 0; a < (CSUM ? 3 : 1); ++a) {
-      tr[a] = 0.0;
+    for (int q = 0; q < (CSUM ? NQ : 1); ++q)
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
+      for (int a = 0; a < 3; ++a) {
+        tr[q][a] = 0.0;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) dr[a][c][v] = 0.0;
-    }
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) dr[q][a][c][v] = 0.0;
+      }
     double *yc[3] = {y, y, y};
-    bool live[3] = {false, false, false};
+    int yadj[3] = {0, 0, 0}; // (!FULL) the dead lanes' step back, see above
     int tb = 0;
     double *pbase = y;
     bool plive = false;
@@ -243,51 +288,50 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
 #pragma unroll
       for (int c = 0; c < NC; ++c)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) zv[a][c][v] = 0.0, acc[a][c][v] = 0.0;
+        for (int v = 0; v < NV; ++v) {
+          if (!CSUM) acc[a][c][v] = 0.0;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) gm[a][q] = 0.0;
+          for (int q = 0; q < NQ; ++q) zv[q][a][c][v] = 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int w = 0; w < 3; ++w) gm[q][a][w] = 0.0;
     }
     int cur_st = 0;
+    if constexpr (NC == 1) {
+      if (lane < G2) topv[lane] = 0.0, topa[lane] = y;
+      __syncwarp();
+    }
 
-    auto flush = [&](auto A_) {
+    // the vertex of window slot A leaves: its partial column goes to y
+    auto flush = [&](auto A_, auto TS_) __attribute__((always_inline)) {
       constexpr int A = decltype(A_)::value;
-      double *const trow = trow0 + tb * TRP;
-      double pv[NR];
-      if constexpr (NC > 1) { // the previous row's values (staged, synced)
+      constexpr int TS = decltype(TS_)::value; // parked-top slot, -1: add now
+      if constexpr (NC > 1) {
+        // staged rows: the previous flush's STS before this one's LDS, its
+        // LDS before this one's STS
+        __syncwarp();
+        double *const trow = trow0 + tb * TRP;
         const double *prow = trow0 + (tb ^ 1) * TRP;
+        double pv[NR];
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
           const int i = sl + 32 * r;
           pv[r] = prow[i < TR ? i : 0];
         }
-      }
-      if constexpr (CSUM) {
-        const double t = tr[0] + tr[1] + tr[2];
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
-#pragma unroll
-          for (int v = 0; v < NV; ++v)
-            acc[A][c][v] = fma(zv[A][c][v], t,
-                               dr[0][c][v] + dr[1][c][v] + dr[2][c][v]);
-      }
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const double vt = acc[A][c][1];
-        double v0 = acc[A][c][0];
-        acc[A][c][0] = 0.0, acc[A][c][1] = 0.0;
-        const double below = __shfl_up_sync(FULL, vt, 1);
-        if (sl > 0) v0 += below;
-        if constexpr (NC > 1) {
+        for (int c = 0; c < NC; ++c) {
+          const double vt = acc[A][c][1];
+          double v0 = acc[A][c][0];
+          acc[A][c][0] = 0.0, acc[A][c][1] = 0.0;
+          const double below = __shfl_up_sync(FULL_MASK, vt, 1);
+          if (sl > 0) v0 += below;
           if (sl < nl) trow[sl * CH + c] = v0;
           if (sl == nl - 1) trow[(sl + 1) * CH + c] = vt;
-        } else {
-          stma_red(yc[A] + c, v0, live[A] & (sl < nl));
-          stma_red(yc[A] + CH + c, vt, live[A] & (sl == nl - 1));
         }
-      }
-      if constexpr (NC > 1) {
         // the previous row's REDs now (lane-contiguous); this row's at the
-        // next flush (a __syncwarp of the step orders its STS before that)
+        // next flush
         double *const base = yc[A] - sl * CH;
         const int n = nl * CH + CH;
 #pragma unroll
@@ -296,27 +340,66 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
           stma_red(pbase + i, pv[r], plive & (i < n));
         }
         pbase = base;
-        plive = live[A];
+        plive = true;
         tb ^= 1;
+      } else {
+        double a0[NQ], a1[NQ], rot[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const double t = tr[q][0] + tr[q][1] + tr[q][2];
+          a0[q] = fma(zv[q][A][0][0], t,
+                      dr[q][0][0][0] + dr[q][1][0][0] + dr[q][2][0][0]);
+          a1[q] = fma(zv[q][A][0][1], t,
+                      dr[q][0][0][1] + dr[q][1][0][1] + dr[q][2][0][1]);
+          // the top value of the lane below (lane 0: of lane 31)
+          rot[q] = __shfl_sync(FULL_MASK, a1[q], (sl + 31) & 31);
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const double below = sl > 0 ? rot[q] : (q > 0 ? rot[q - 1] : 0.0);
+          const double v = a0[q] + below;
+          if (FULL || q < NQ - 1)
+            stma_red_all(yc[A] + boff[q], v);
+          else
+            stma_red_all(yc[A] + boff[q] + yadj[A], pb[q] ? v : 0.0);
+        }
+        if constexpr (TS >= 0) {
+          if (pt) {
+            topv[TS] = a1[NQ - 1];
+            topa[TS] = yc[A] + 32 * (NQ - 1) + 1;
+          }
+        } else {
+          stma_red(yc[A] + 32 * (NQ - 1) + 1, a1[NQ - 1], pt);
+        }
+      }
+    };
+    // the parked top values of the last granule's flushes
+    auto add_tops = [&]() __attribute__((always_inline)) {
+      if constexpr (NC == 1) {
+        __syncwarp();
+        if (lane < G2) {
+          stma_red_all(topa[lane], topv[lane]);
+          topv[lane] = 0.0;
+        }
+        __syncwarp();
       }
     };
 
     // Software pipeline: the column values of step k+1 are read out of the
     // ring (into F) in the middle of step k, after step k's own values were
-    // consumed and before its cell arithmetic, so the two dependent LDS
-    // (table entry, then the values) overlap ~40 fp64 instructions.
-    double Ff[2][CH], Fg[2][3];
+    // consumed and before its cell arithmetic.  P = k mod 2G is a template
+    // argument: granule boundaries and table slots are compile-time.
+    double Ff[NQ][2][CH], Fg[NQ][2][3];
     int Fva = 0;
-    bool Fact = false;
-    auto prefetch = [&](int k) {
-      const bool act = k < len;
-      if (act && (k & (G2 - 1)) == 0) { // granule boundary (warp-uniform)
+    auto prefetch = [&](auto P_, int k) __attribute__((always_inline)) {
+      constexpr int P = decltype(P_)::value;
+      if constexpr (P == 0) { // granule boundary
         const int g = k / G2;
         if (g > 0) {
           // release granule g-1 (its last values are in registers); the
           // last warp of the group to do so refills its stage with
           // granule g-1+NS
-          __syncwarp();
+          add_tops();
           bool last = true;
           if constexpr (NCH > 1) {
             int l = 0;
@@ -325,126 +408,165 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
               l = atomicAdd(cnt + cur_st, 1) == NCH - 1;
               if (l) cnt[cur_st] = 0;
             }
-            last = __shfl_sync(FULL, l, 0);
+            last = __shfl_sync(FULL_MASK, l, 0);
           }
           if (last && g - 1 + NS < ngran) {
             if constexpr (NCH > 1) __threadfence_block();
-            refill(cur_st, g - 1 + NS, k0, len, vpre);
+            refill(cur_st, g - 1 + NS, len, vpre);
           }
           // ids of the granule the NEXT release refills (any warp of the
           // group may be the one): loaded a granule ahead of their use
-          {
-            const int kk = G2 * (g + NS) + lane;
-            vpre = (lane < G2 && kk < len) ? __ldg(steps + k0 + kk) : 0;
-          }
+          vpre = ids(g + NS);
         }
         const uint32_t gg = gc + (uint32_t)g;
         cur_st = (int)(gg % NS);
         mbar_wait(full + cur_st, (gg / NS) & 1);
       }
-      if constexpr (NC > 1)
-        __syncwarp(); // the staged row's STS before the next flush's LDS
-      const int4 e = *reinterpret_cast<const int4 *>(
-          tab + cur_st * G2 + (k & (G2 - 1)));
-      const uint32_t fo = act ? (uint32_t)e.x : zero_off;
-      const uint32_t co = act ? (uint32_t)e.y : zero_off;
-      Fva = act ? e.z : 0;
-      Fact = act;
-      const double *ef = reinterpret_cast<const double *>(stma_raw + fo) +
+      const int4 e = *reinterpret_cast<const int4 *>(tab + cur_st * G2 + P);
+      Fva = e.z;
+      const double *ef = reinterpret_cast<const double *>(stma_raw + e.x) +
                          (l0 + sl) * CH;
-      const double *ec = reinterpret_cast<const double *>(stma_raw + co) +
+      const double *ec = reinterpret_cast<const double *>(stma_raw + e.y) +
                          3 * (l0 + sl);
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int q = 0; q < NQ; ++q)
 #pragma unroll
-        for (int c = 0; c < CH; ++c) Ff[j][c] = ef[j * CH + c];
+        for (int j = 0; j < 2; ++j) {
 #pragma unroll
-        for (int q = 0; q < 3; ++q) Fg[j][q] = ec[3 * j + q];
-      }
+          for (int c = 0; c < CH; ++c)
+            Ff[q][j][c] = ef[(32 * q + j) * CH + c];
+#pragma unroll
+          for (int w = 0; w < 3; ++w) Fg[q][j][w] = ec[3 * (32 * q + j) + w];
+        }
     };
 
-    auto step = [&](auto A_, auto FILL_, int k) {
-      constexpr int A = decltype(A_)::value;
+    // one strip step: the vertex of step k enters window slot A = P mod 3
+    auto step = [&](auto P_, auto FILL_, auto GUARD_, int k) __attribute__((always_inline)) {
+      constexpr int P = decltype(P_)::value;
+      constexpr int A = P % 3;
       constexpr bool FILL = decltype(FILL_)::value;
-      if (!FILL) flush(A_);
-      const bool act = Fact;
-      gm[A][0] = Fg[0][0] + Fg[1][0];
-      gm[A][1] = Fg[0][1] + Fg[1][1];
-      gm[A][2] = Fg[1][2] - Fg[0][2];
-      yc[A] = y + (int64_t)Fva * colf + (l0 + sl) * CH;
-      live[A] = act;
+      constexpr bool GUARD = decltype(GUARD_)::value;
+      using AC = std::integral_constant<int, A>;
+      if constexpr (!FILL) flush(AC{}, P_);
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-          zv[A][c][v] = fma(M.l[v * NV + 1], Ff[1][c],
-                            fma(M.l[v * NV + 0], Ff[0][c], 0.0));
-      prefetch(k + 1);
-      if (FILL && A < 2) return;
-      const double dj = prism_abs_detj_12(gm[0][0], gm[0][1], gm[0][2],
-                                          gm[1][0], gm[1][1], gm[1][2],
-                                          gm[2][0], gm[2][1], gm[2][2]);
-      const double det = act ? dj : 0.0;
-      if constexpr (CSUM) {
-        tr[A] = det * M.ta;
-        const double dtb = det * M.tb;
+      for (int q = 0; q < NQ; ++q) {
+        gm[q][A][0] = Fg[q][0][0] + Fg[q][1][0];
+        gm[q][A][1] = Fg[q][0][1] + Fg[q][1][1];
+        gm[q][A][2] = Fg[q][1][2] - Fg[q][0][2];
 #pragma unroll
         for (int c = 0; c < NC; ++c)
 #pragma unroll
           for (int v = 0; v < NV; ++v)
-            dr[A][c][v] = dtb * (zv[0][c][v] + zv[1][c][v] + zv[2][c][v]);
-      } else {
-        const double dta = det * M.ta, dtb = det * M.tb;
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            const double d = dtb * (zv[0][c][v] + zv[1][c][v] + zv[2][c][v]);
-#pragma unroll
-            for (int h = 0; h < 3; ++h)
-              acc[h][c][v] = fma(dta, zv[h][c][v], acc[h][c][v] + d);
-          }
+            zv[q][A][c][v] = fma(M.l[v * NV + 1], Ff[q][1][c],
+                                 fma(M.l[v * NV + 0], Ff[q][0][c], 0.0));
       }
+      yc[A] = y + (int64_t)Fva * colf + (l0 + sl) * CH;
+      if constexpr (!FULL && NC == 1)
+        yadj[A] = (dead_last & (Fva == v_last)) ? -colf : 0;
+      if (!GUARD || k + 1 < len)
+        prefetch(std::integral_constant<int, (P + 1) % G2>{}, k + 1);
+      if constexpr (FILL && A < 2) return;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const double det = prism_abs_detj_12(
+            gm[q][0][0], gm[q][0][1], gm[q][0][2], gm[q][1][0], gm[q][1][1],
+            gm[q][1][2], gm[q][2][0], gm[q][2][1], gm[q][2][2]);
+        if constexpr (CSUM) {
+          tr[q][A] = det * M.ta;
+          const double dtb = det * M.tb;
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+              dr[q][A][c][v] =
+                  dtb * (zv[q][0][c][v] + zv[q][1][c][v] + zv[q][2][c][v]);
+        } else {
+          const double dta = det * M.ta, dtb = det * M.tb;
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              const double d =
+                  dtb * (zv[q][0][c][v] + zv[q][1][c][v] + zv[q][2][c][v]);
+#pragma unroll
+              for (int h = 0; h < 3; ++h)
+                acc[h][c][v] = fma(dta, zv[q][h][c][v], acc[h][c][v] + d);
+            }
+        }
+      }
+    };
+    using TF = std::true_type;
+    using FF = std::false_type;
+#define PM_P(N_) std::integral_constant<int, N_> {}
+    prefetch(PM_P(0), 0);
+    step(PM_P(0), TF{}, TF{}, 0);
+    step(PM_P(1), TF{}, TF{}, 1);
+    step(PM_P(2), TF{}, TF{}, 2);
+    // granule by granule (one copy of each step position in the code: the
+    // window state stays in registers only while every step is inlined)
+    // granule 0's cells, whole granules followed by at least one more step
+    // (no guards: one scheduling block per step), then the guarded tail
+    if (3 < len) step(PM_P(3), FF{}, TF{}, 3);
+    if (4 < len) step(PM_P(4), FF{}, TF{}, 4);
+    if (5 < len) step(PM_P(5), FF{}, TF{}, 5);
+    int kb = G2;
+    for (; kb + G2 < len; kb += G2) {
+      step(PM_P(0), FF{}, FF{}, kb);
+      step(PM_P(1), FF{}, FF{}, kb + 1);
+      step(PM_P(2), FF{}, FF{}, kb + 2);
+      step(PM_P(3), FF{}, FF{}, kb + 3);
+      step(PM_P(4), FF{}, FF{}, kb + 4);
+      step(PM_P(5), FF{}, FF{}, kb + 5);
+    }
+    for (; kb < len; kb += G2) {
+      step(PM_P(0), FF{}, TF{}, kb);
+      if (kb + 1 < len) step(PM_P(1), FF{}, TF{}, kb + 1);
+      if (kb + 2 < len) step(PM_P(2), FF{}, TF{}, kb + 2);
+      if (kb + 3 < len) step(PM_P(3), FF{}, TF{}, kb + 3);
+      if (kb + 4 < len) step(PM_P(4), FF{}, TF{}, kb + 4);
+      if (kb + 5 < len) step(PM_P(5), FF{}, TF{}, kb + 5);
+    }
+    add_tops();
+#undef PM_P
+    // the last window, oldest vertex first; a vertex that entered at step
+    // j is in the cells formed at steps j, j+1, j+2 only: the ring slots of
+    // cells that were never formed are cleared before its flush
+    auto clear_cell = [&](auto A_) {
+      constexpr int A = decltype(A_)::value;
+      if constexpr (CSUM) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          tr[q][A] = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) dr[q][A][c][v] = 0.0;
+        }
+      }
+    };
+    auto fin = [&](auto A1_, auto A2_, auto A3_) {
+      using NOW = std::integral_constant<int, -1>;
+      flush(A1_, NOW{});
+      clear_cell(A1_);
+      flush(A2_, NOW{});
+      clear_cell(A2_);
+      flush(A3_, NOW{});
     };
     using S0 = std::integral_constant<int, 0>;
     using S1 = std::integral_constant<int, 1>;
     using S2 = std::integral_constant<int, 2>;
-    using TF = std::true_type;
-    using FF = std::false_type;
-    prefetch(0);
-    step(S0{}, TF{}, 0);
-    step(S1{}, TF{}, 1);
-    step(S2{}, TF{}, 2);
-    for (int k = 3; k < len; k += 3) {
-      step(S0{}, FF{}, k);
-      step(S1{}, FF{}, k + 1);
-      step(S2{}, FF{}, k + 2);
+    switch (len % 3) {
+    case 0: fin(S0{}, S1{}, S2{}); break;
+    case 1: fin(S1{}, S2{}, S0{}); break;
+    default: fin(S2{}, S0{}, S1{}); break;
     }
-    auto clear_cell = [&](auto A_) {
-      constexpr int A = decltype(A_)::value;
-      if constexpr (CSUM) {
-        tr[A] = 0.0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) dr[A][c][v] = 0.0;
-      }
-    };
-    flush(S0{});
-    clear_cell(S0{});
-    __syncwarp();
-    flush(S1{});
-    clear_cell(S1{});
-    __syncwarp();
-    flush(S2{});
-    clear_cell(S2{});
     if constexpr (NC > 1) { // the last staged row
       __syncwarp();
       const double *prow = trow0 + (tb ^ 1) * TRP;
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
         const int i = sl + 32 * r;
-        stma_red(pbase + i, prow[i < TR ? i : 0], plive && i < nl * CH + CH);
+        stma_red(pbase + i, prow[i < TR ? i : 0], plive & (i < nl * CH + CH));
       }
       __syncwarp();
     }
@@ -452,12 +574,14 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
   }
 }
 
-template <int NC, int G, int NCH, int NS>
+template <int NC, int NQ, int NCH, int NS>
 int stma_launch(const KronMat &M, const int32_t *strip_ptr,
                 const int32_t *steps, int64_t n_strips, int layers,
                 const double *coords, const double *x, double *y,
                 int64_t n_vertices, cudaStream_t s) {
-  constexpr int MAXT = NC > 1 ? PM_TMA_MAXT_V : PM_TMA_MAXT_S;
+  constexpr int G = kStmaG;
+  constexpr int MAXT = NC > 1 ? PM_TMA_MAXT_V
+                              : (NQ > 1 ? PM_TMA_MAXT_S2 : PM_TMA_MAXT_S);
   const uint32_t Pf = stma_up16(8u * (layers + 1) * NC + 8);
   const uint32_t Pc = stma_up16(8u * (layers + 1) * 3 + 8);
   int dev = 0, smem_max = 0;
@@ -480,12 +604,15 @@ int stma_launch(const KronMat &M, const int32_t *strip_ptr,
     return PM_EINVAL;
   }
   const StmaSmem L = stma_smem(NC, G, NS, ngrp, ngrp * NCH, Pf, Pc);
-  auto kern = k_strip_tma<NC, G, NS, NCH, MAXT>;
-  static int cached_dev = -1;
-  if (cached_dev != dev) {
+  // FULL: every 32-layer chunk is whole (no lanes past a column's end)
+  const bool full = NC == 1 && layers % 32 == 0;
+  auto kern = full ? k_strip_tma<NC, NQ, NS, NCH, MAXT, NC == 1>
+                   : k_strip_tma<NC, NQ, NS, NCH, MAXT, false>;
+  static int cached_dev[2] = {-1, -1};
+  if (cached_dev[full] != dev) {
     PM_CUDA_TRY(cudaFuncSetAttribute(
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-    cached_dev = dev;
+    cached_dev[full] = dev;
   }
   int64_t want = (n_strips + ngrp - 1) / ngrp;
   const int64_t cap = sm_count();
@@ -497,39 +624,36 @@ int stma_launch(const KronMat &M, const int32_t *strip_ptr,
   return PM_OK;
 }
 
-template <int NC, int G>
+// warps per group (32-layer chunks / chunks per warp) and ring depth
+template <int NC, int NQ>
 int stma_nch(int nch, int ns, const KronMat &M, const int32_t *strip_ptr,
              const int32_t *steps, int64_t n_strips, int layers,
              const double *coords, const double *x, double *y,
              int64_t n_vertices, cudaStream_t s) {
 #define PM_STMA_CASE(N_)                                                     \
   case N_:                                                                   \
-    return ns == 2 ? stma_launch<NC, G, N_, 2>(M, strip_ptr, steps, n_strips, \
-                                               layers, coords, x, y,         \
-                                               n_vertices, s)                \
-                   : stma_launch<NC, G, N_, 3>(M, strip_ptr, steps, n_strips, \
-                                               layers, coords, x, y,         \
-                                               n_vertices, s);
+    return ns == 3 && PM_TMA_NS3                                             \
+               ? stma_launch<NC, NQ, N_, PM_TMA_NS3 ? 3 : 2>(                \
+                     M, strip_ptr, steps, n_strips, layers, coords, x, y,    \
+                     n_vertices, s)                                          \
+               : stma_launch<NC, NQ, N_, 2>(M, strip_ptr, steps, n_strips,   \
+                                            layers, coords, x, y,            \
+                                            n_vertices, s);
   switch (nch) {
     PM_STMA_CASE(1)
     PM_STMA_CASE(2)
-    PM_STMA_CASE(3)
-    PM_STMA_CASE(4)
   default:
+    if constexpr (NQ == 1) {
+      switch (nch) {
+        PM_STMA_CASE(3)
+        PM_STMA_CASE(4)
+      default: break;
+      }
+    }
     set_error("pm_column_mass_strip_tma: at most 128 layers (got %d)", layers);
     return PM_EINVAL;
   }
 #undef PM_STMA_CASE
-}
-
-template <int NC>
-int stma_g(int g, int nch, int ns, const KronMat &M, const int32_t *strip_ptr,
-           const int32_t *steps, int64_t n_strips, int layers,
-           const double *coords, const double *x, double *y,
-           int64_t n_vertices, cudaStream_t s) {
-  if (g == 2)
-    return stma_nch<NC, 2>(nch, ns, M, strip_ptr, steps, n_strips, layers, coords, x, y, n_vertices, s);
-  return stma_nch<NC, 4>(nch, ns, M, strip_ptr, steps, n_strips, layers, coords, x, y, n_vertices, s);
 }
 
 } // namespace
@@ -579,13 +703,18 @@ extern "C" int pm_column_mass_strip_tma(
     pm::set_error("NULL device pointer");
     return PM_EINVAL;
   }
-  const int nch = (layers + 31) / 32;
-  int g = 4;
-  if (const char *e = getenv("PM_TMA_G")) g = atoi(e) == 2 ? 2 : 4;
-  int ns = 3;
-  if (const char *e = getenv("PM_TMA_NS")) ns = atoi(e) == 2 ? 2 : 3;
-  return nc == 1 ? pm::stma_g<1>(g, nch, ns, M, strip_ptr, steps, n_strips, layers,
-                                 coords, x, y, n_vertices, s)
-                 : pm::stma_g<3>(g, nch, ns, M, strip_ptr, steps, n_strips, layers,
-                                 coords, x, y, n_vertices, s);
+  int ns = 2;
+  if (const char *e = getenv("PM_TMA_NS")) ns = atoi(e) == 3 ? 3 : 2;
+  // two 32-layer chunks per warp for scalar columns when every warp's
+  // second chunk is non-empty (PM_TMA_NQ=1: one chunk per warp)
+  bool two = nc == 1 && layers > 32 && (layers - 1) % 64 >= 32;
+  if (const char *e = getenv("PM_TMA_NQ")) two = two && atoi(e) != 1;
+  const int nch = two ? (layers + 63) / 64 : (layers + 31) / 32;
+  if (nc == 3)
+    return pm::stma_nch<3, 1>(nch, ns, M, strip_ptr, steps, n_strips, layers,
+                              coords, x, y, n_vertices, s);
+  return two ? pm::stma_nch<1, 2>(nch, ns, M, strip_ptr, steps, n_strips,
+                                  layers, coords, x, y, n_vertices, s)
+             : pm::stma_nch<1, 1>(nch, ns, M, strip_ptr, steps, n_strips,
+                                  layers, coords, x, y, n_vertices, s);
 }

@@ -109,11 +109,11 @@ def test_striptma_matches_oracle_rcm(lname, layers):
 
 @gpu
 @pytest.mark.parametrize("lname", ["CG1xCG1", "VP1"])
-@pytest.mark.parametrize("env", [{"PM_TMA_G": "2"}, {"PM_TMA_NS": "2"},
-                                 {"PM_TMA_G": "2", "PM_TMA_NS": "2"},
-                                 {"PM_TMA_GROUPS": "1"}])
+@pytest.mark.parametrize("env", [{"PM_TMA_NQ": "1"}, {"PM_TMA_GROUPS": "1"},
+                                 {"PM_TMA_NQ": "1", "PM_TMA_GROUPS": "2"}])
 def test_striptma_ring_shapes(lname, env, monkeypatch):
-    """Granule width 2 / 4, 2 / 3 stages, one group per CTA."""
+    """One chunk per warp (scalar columns default to two), one / two groups
+    per CTA."""
     _need_cuda()
     from paper_1604_05937_b200 import kernels
     from paper_1604_05937_b200.quadrature import prism_quadrature
@@ -170,3 +170,34 @@ def test_striptma_accumulates_and_repeats():
     y3 = y1.clone()
     op.apply(x, coords, y3, accumulate=True)
     assert _rel(y3.cpu().numpy(), 2 * ref) <= 1e-10
+
+
+@gpu
+@pytest.mark.parametrize("lname", ["CG1xCG1", "VP1"])
+@pytest.mark.parametrize("n,max_len,groups,layers", [
+    (64, 512, None, 64),    # strips of many granules, one per group
+    (96, 37, "1", 64),      # several strips per group (stage counters and
+                            # mbarrier phases carry over), ragged lengths
+    (96, 50, "2", 100),     # two / four warps per group
+    (64, 41, "1", 20),      # one chunk
+])
+def test_striptma_long_and_many_strips(lname, n, max_len, groups, layers,
+                                       monkeypatch):
+    _need_cuda()
+    from paper_1604_05937_b200 import kernels
+    from paper_1604_05937_b200.quadrature import prism_quadrature
+    monkeypatch.setattr(kernels, "strip_max_len", lambda nc, l: max_len)
+    if groups:
+        monkeypatch.setenv("PM_TMA_GROUPS", groups)
+    base = _rcm_mesh(n)
+    fs = _space(base, layers, lname)
+    op = kernels.MassOperator(fs, prism_quadrature(*quad_degrees(lname)),
+                              schedule="striptma")
+    (sp, _st), frac = op._run_strips()
+    lens = np.diff(sp.cpu().numpy())
+    assert lens.max() > 12 and frac > 0.8
+    if groups:
+        assert len(lens) > 148 * int(groups)
+    f = np.random.default_rng(n).uniform(-1, 1, fs.total_dofs)
+    got = kernels.mass_action(fs, f, operator=op, schedule="striptma")
+    assert _rel(got, _oracle(base, layers, lname, f)) <= 1e-10
