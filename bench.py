@@ -508,7 +508,8 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     kernels = []
     for q in parts:
-        redg = q["op"].last_schedule in ("stripred", "pstrip", "atomic")
+        redg = q["op"].last_schedule in ("stripred", "striptma", "pstrip",
+                                          "atomic")
         g = capture([q], args.steps, accumulate=redg)
         kms = time_graph(g) / args.steps
         zero_ms = None

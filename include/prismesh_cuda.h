@@ -24,6 +24,9 @@
  *   pm_build_strips          <- host planner of that schedule
  *   pm_column_mass_strip_red <- same, global strips + REDG
  *   pm_build_global_strips   <- host planner of that schedule
+ *   pm_column_mass_strip_tma <- same, run strips: whole vertex columns by
+ *                               bulk copies, several columns per copy
+ *   pm_build_run_strips      <- host planner of that schedule
  *   pm_column_mass_tile      <- same, band tiles staged by TMA bulk copies
  *                               (experimental: PM_EXPERIMENTAL=1 builds)
  *   pm_tiles_build / _info / _export / _free <- host planner of that schedule

@@ -51,6 +51,9 @@
 #ifndef PM_TMA_NS3
 #define PM_TMA_NS3 0
 #endif
+#ifndef PM_TMA_VFULL
+#define PM_TMA_VFULL 0
+#endif
 
 
 namespace pm {
@@ -102,7 +105,7 @@ __host__ __device__ inline StmaSmem stma_smem(int NC, int G, int NS, int ngrp,
   s.off_tab = o, o += (uint32_t)ngrp * NS * 2 * G * 16;
   s.bars = o, o += (uint32_t)ngrp * NS * 8;
   s.cnt = o, o += stma_up16((uint32_t)ngrp * NS * 4);
-  s.tops = o, o += NC > 1 ? 0 : (uint32_t)nwarp * 2 * G * 16;
+  s.tops = o, o += (uint32_t)nwarp * 2 * G * NC * 16;
   s.trow = o, o += NC > 1 ? (uint32_t)nwarp * 2 * (33 * NC + 1) * 8 : 0;
   o = (o + 127u) & ~127u;
   s.ring = o, o += (uint32_t)ngrp * NS * 2 * G * (Pf + Pc);
@@ -144,9 +147,10 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
   // parked here and added once per granule by 2G lanes, so the strip loop
   // has no predicated RED (ptxas turns those into branches, which end its
   // scheduling blocks: measured 2.96 -> 2.32 ms on C5a without them)
+  constexpr int NT = G2 * NC; // parked values per warp and granule
   double *const topv = reinterpret_cast<double *>(stma_raw + L.tops) +
-                       wib * 2 * G2;
-  double **const topa = reinterpret_cast<double **>(topv + G2);
+                       wib * 2 * NT;
+  double **const topa = reinterpret_cast<double **>(topv + NT);
   const uint32_t SB = G2 * (Pf + Pc); // stage bytes
   const uint32_t ring_off = L.ring + (uint32_t)grp * NS * SB;
 
@@ -299,8 +303,13 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
         for (int w = 0; w < 3; ++w) gm[q][a][w] = 0.0;
     }
     int cur_st = 0;
-    if constexpr (NC == 1) {
-      if (lane < G2) topv[lane] = 0.0, topa[lane] = y;
+    if constexpr (NC == 1 || FULL) {
+      if (lane < NT) topv[lane] = 0.0, topa[lane] = y;
+      if constexpr (NC > 1) {
+        // the first flush adds the (empty) previous row: zeros to y[0..]
+        for (int i = lane; i < 2 * TRP; i += 32) trow0[i] = 0.0;
+        plive = true;
+      }
       __syncwarp();
     }
 
@@ -334,10 +343,24 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
         // next flush
         double *const base = yc[A] - sl * CH;
         const int n = nl * CH + CH;
+        if constexpr (FULL && TS >= 0) {
+          // whole chunks: rows 0 .. NR-2 are all live (32 (NR-1) values of
+          // the 33 CH); the CH values of the chunk's top level are parked
+          // and added once per granule (no predicated RED in the loop)
+          static_assert(32 * (NR - 1) + CH == TR, "row split");
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          const int i = sl + 32 * r;
-          stma_red(pbase + i, pv[r], plive & (i < n));
+          for (int r = 0; r + 1 < NR; ++r)
+            stma_red_all(pbase + sl + 32 * r, pv[r]);
+          if (sl < CH) {
+            topv[TS * CH + sl] = pv[NR - 1];
+            topa[TS * CH + sl] = pbase + 32 * (NR - 1) + sl;
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            const int i = sl + 32 * r;
+            stma_red(pbase + i, pv[r], plive & (i < n));
+          }
         }
         pbase = base;
         plive = true;
@@ -375,12 +398,14 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
     };
     // the parked top values of the last granule's flushes
     auto add_tops = [&]() __attribute__((always_inline)) {
-      if constexpr (NC == 1) {
+      if constexpr (NC == 1 || FULL) {
         __syncwarp();
-        if (lane < G2) {
+        if (lane < NT) {
           stma_red_all(topa[lane], topv[lane]);
           topv[lane] = 0.0;
         }
+        __syncwarp();
+      } else {
         __syncwarp();
       }
     };
@@ -605,8 +630,11 @@ int stma_launch(const KronMat &M, const int32_t *strip_ptr,
   }
   const StmaSmem L = stma_smem(NC, G, NS, ngrp, ngrp * NCH, Pf, Pc);
   // FULL: every 32-layer chunk is whole (no lanes past a column's end)
-  const bool full = NC == 1 && layers % 32 == 0;
-  auto kern = full ? k_strip_tma<NC, NQ, NS, NCH, MAXT, NC == 1>
+  // (3-vector columns: the branch-free flush measured slower, C5b 7.18 vs
+  // 6.02 ms, so they keep the predicated REDs; PM_TMA_VFULL=1 compiles it)
+  const bool full = (NC == 1 || PM_TMA_VFULL) && layers % 32 == 0;
+  auto kern = full ? k_strip_tma<NC, NQ, NS, NCH, MAXT,
+                                 NC == 1 || PM_TMA_VFULL>
                    : k_strip_tma<NC, NQ, NS, NCH, MAXT, false>;
   static int cached_dev[2] = {-1, -1};
   if (cached_dev[full] != dev) {

@@ -155,6 +155,7 @@ class MassOperator:
         self._strip = None
         self._gstrips = None
         self._rstrips = None
+        self._tma_auto = None
         self._dgstrips = None
         self._pstrips = None
         self._tiles = None
@@ -452,6 +453,27 @@ class MassOperator:
         return d in ((1, 0, 0, 0, 0, 0), (3, 0, 0, 0, 0, 0)) and \
             self.strip_invariant and self.layers <= 128
 
+    @property
+    def striptma_auto(self) -> bool:
+        """``auto`` takes the run-strip kernel where it measured faster than
+        the cp.async strips (C5a 2.91 -> 2.34 ms, profiles/README.md):
+        scalar P1 columns in whole 32-layer chunks, two per warp (64 or 128
+        layers: no predicated RED in the strip loop), on a mesh whose strips
+        follow vertex-id runs and are long enough to hide the ring's cold
+        start per strip.  PM_STRIPTMA=0 keeps the cp.async strips."""
+        if self._tma_auto is None:
+            import os
+            ok = False
+            d = tuple(int(v) for v in self.fs.layout.delta6())
+            if d == (1, 0, 0, 0, 0, 0) and self.striptma_ok and \
+                    self.layers in (64, 128) and \
+                    os.environ.get("PM_STRIPTMA", "1") != "0":
+                (sp, st), frac = self._run_strips()
+                mean = st.shape[0] / max(1, sp.shape[0] - 1)
+                ok = frac >= 0.9 and mean >= 128
+            self._tma_auto = ok
+        return self._tma_auto
+
     def _run_strips(self):
         """Strips along the vertex-id bands (pm_build_run_strips, cached)
         and the fraction of steps whose vertex continues its side's id run:
@@ -615,8 +637,13 @@ class MassOperator:
             sched = "stripdg"
         if sched == "auto" and self.share == 2:
             # measured fastest (profiles/): global strips for vertex-column
-            # layouts, the warp-per-column kernel otherwise
-            sched = "stripred" if self.stripred_ok else "column"
+            # layouts (run strips with bulk-copied columns where they apply),
+            # the warp-per-column kernel otherwise
+            if self.striptma_auto and x.data_ptr() % 16 == 0 and \
+                    coords.data_ptr() % 16 == 0:
+                sched = "striptma"
+            else:
+                sched = "stripred" if self.stripred_ok else "column"
         self.last_schedule = sched
         if sched == "stripred":
             if not self.stripred_ok:
