@@ -43,9 +43,6 @@
 // columns per strip side and copy: a granule of 2 G steps is a whole number
 // of window cycles (3 steps), so granule boundaries and table slots are
 // compile-time positions of the unrolled strip loop
-#ifndef PM_TMA_G
-#define PM_TMA_G 3
-#endif
 // 1: also compile the 3-stage rings (PM_TMA_NS=3 at run time; measured
 // slower on every config: fewer groups fit the shared memory)
 #ifndef PM_TMA_NS3
@@ -90,32 +87,31 @@ __device__ __forceinline__ void stma_group_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-constexpr int kStmaG = PM_TMA_G;
 constexpr uint32_t stma_up16(uint32_t b) { return (b + 15u) & ~15u; }
 
 // smem carve-up (bytes), shared by the kernel and the launcher
 struct StmaSmem {
   uint32_t off_tab, bars, cnt, tops, trow, ring, zero, total;
 };
-__host__ __device__ inline StmaSmem stma_smem(int NC, int G, int NS, int ngrp,
-                                              int nwarp, uint32_t Pf,
-                                              uint32_t Pc) {
+__host__ __device__ inline StmaSmem stma_smem(int NC, int G2, int NS,
+                                              int ngrp, int nwarp,
+                                              uint32_t Pf, uint32_t Pc) {
   StmaSmem s;
   uint32_t o = 0;
-  s.off_tab = o, o += (uint32_t)ngrp * NS * 2 * G * 16;
+  s.off_tab = o, o += (uint32_t)ngrp * NS * G2 * 16;
   s.bars = o, o += (uint32_t)ngrp * NS * 8;
   s.cnt = o, o += stma_up16((uint32_t)ngrp * NS * 4);
-  s.tops = o, o += (uint32_t)nwarp * 2 * G * NC * 16;
+  s.tops = o, o += (uint32_t)nwarp * G2 * NC * 16;
   s.trow = o, o += NC > 1 ? (uint32_t)nwarp * 2 * (33 * NC + 1) * 8 : 0;
   o = (o + 127u) & ~127u;
-  s.ring = o, o += (uint32_t)ngrp * NS * 2 * G * (Pf + Pc);
+  s.ring = o, o += (uint32_t)ngrp * NS * G2 * (Pf + Pc);
   s.zero = o;
   o += 2048; // lanes past a partial chunk read past their column (never used)
   s.total = o;
   return s;
 }
 
-template <int NC, int NQ, int NS, int NCH, int MAXT, bool FULL>
+template <int NC, int NQ, int NS, int NCH, int MAXT, bool FULL, int G2>
 __global__ void __launch_bounds__(MAXT, 1)
 k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
             const int32_t *__restrict__ steps, int64_t n_strips, int layers,
@@ -125,8 +121,10 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
   static_assert(NC == 1 || NQ == 1, "two chunks per warp: scalar columns");
   constexpr unsigned FULL_MASK = 0xffffffffu;
   constexpr int CH = NC, NV = 2;
-  constexpr int G = kStmaG, G2 = 2 * G;
-  static_assert(G2 % 3 == 0, "granule = whole window cycles");
+  // granule = G2 strip steps: the first step's side brings NA columns, the
+  // other side NB (G2 = 3: 2 + 1, sides swapping from granule to granule)
+  static_assert(G2 == 3 || G2 == 6, "granule = whole window cycles");
+  constexpr int NA = (G2 + 1) / 2, NB = G2 / 2;
   constexpr int TR = NC > 1 ? 33 * NC : 0; // staged chunk row
   constexpr int TRP = 33 * NC + 1;         // row pitch (doubles)
   constexpr int NR = NC > 1 ? (TR + 31) / 32 : 1;
@@ -135,7 +133,7 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwarp = blockDim.x >> 5;
   const int grp = wib / NCH, chunk = wib % NCH;
-  const StmaSmem L = stma_smem(NC, G, NS, ngrp, nwarp, Pf, Pc);
+  const StmaSmem L = stma_smem(NC, G2, NS, ngrp, nwarp, Pf, Pc);
   StmaEntry *const tab =
       reinterpret_cast<StmaEntry *>(stma_raw + L.off_tab) + grp * NS * G2;
   uint64_t *const full = reinterpret_cast<uint64_t *>(stma_raw + L.bars) +
@@ -202,8 +200,10 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
     const unsigned vmask = __ballot_sync(FULL_MASK, valid);
     const bool consec = !(bad & sidemask);
     const int nside = __popc(vmask & sidemask);
+    // (`side` is relative to the granule's first step)
     const uint32_t side_base = ring_off + (uint32_t)st * SB +
-                               (uint32_t)side * G * (Pf + Pc);
+                               (uint32_t)side * NA * (Pf + Pc);
+    const uint32_t ncol = side ? NB : NA; // column slots of this side
     uint64_t *const bar = full + st;
     if (valid) {
       const int vb = consec ? vfirst : v; // first column of the copy
@@ -215,7 +215,7 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
       const uint32_t csh = (uint32_t)(reinterpret_cast<uintptr_t>(cs) >> 3) & 1;
       // consecutive columns lie back to back, single ones at the padded pitch
       const uint32_t fdst = side_base + (consec ? 0u : (uint32_t)j * Pf);
-      const uint32_t cdst = side_base + G * Pf + (consec ? 0u : (uint32_t)j * Pc);
+      const uint32_t cdst = side_base + ncol * Pf + (consec ? 0u : (uint32_t)j * Pc);
       StmaEntry e;
       // (the lane's first value: level l0 + lane is added by the readers)
       e.foff = fdst + 8 * fsh + (consec ? (uint32_t)j * 8 * colf : 0u);
@@ -523,33 +523,33 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
     using TF = std::true_type;
     using FF = std::false_type;
 #define PM_P(N_) std::integral_constant<int, N_> {}
+    // (loop period 6 = lcm of the window's 3 slots and the granule; the
+    // position of step kb + i in its granule is i % G2)
     prefetch(PM_P(0), 0);
     step(PM_P(0), TF{}, TF{}, 0);
-    step(PM_P(1), TF{}, TF{}, 1);
-    step(PM_P(2), TF{}, TF{}, 2);
-    // granule by granule (one copy of each step position in the code: the
-    // window state stays in registers only while every step is inlined)
-    // granule 0's cells, whole granules followed by at least one more step
+    step(PM_P(1 % G2), TF{}, TF{}, 1);
+    step(PM_P(2 % G2), TF{}, TF{}, 2);
+    // granule 0's cells, whole periods followed by at least one more step
     // (no guards: one scheduling block per step), then the guarded tail
-    if (3 < len) step(PM_P(3), FF{}, TF{}, 3);
-    if (4 < len) step(PM_P(4), FF{}, TF{}, 4);
-    if (5 < len) step(PM_P(5), FF{}, TF{}, 5);
-    int kb = G2;
-    for (; kb + G2 < len; kb += G2) {
+    if (3 < len) step(PM_P(3 % G2), FF{}, TF{}, 3);
+    if (4 < len) step(PM_P(4 % G2), FF{}, TF{}, 4);
+    if (5 < len) step(PM_P(5 % G2), FF{}, TF{}, 5);
+    int kb = 6;
+    for (; kb + 6 < len; kb += 6) {
       step(PM_P(0), FF{}, FF{}, kb);
-      step(PM_P(1), FF{}, FF{}, kb + 1);
-      step(PM_P(2), FF{}, FF{}, kb + 2);
-      step(PM_P(3), FF{}, FF{}, kb + 3);
-      step(PM_P(4), FF{}, FF{}, kb + 4);
-      step(PM_P(5), FF{}, FF{}, kb + 5);
+      step(PM_P(1 % G2), FF{}, FF{}, kb + 1);
+      step(PM_P(2 % G2), FF{}, FF{}, kb + 2);
+      step(PM_P(3 % G2), FF{}, FF{}, kb + 3);
+      step(PM_P(4 % G2), FF{}, FF{}, kb + 4);
+      step(PM_P(5 % G2), FF{}, FF{}, kb + 5);
     }
-    for (; kb < len; kb += G2) {
+    for (; kb < len; kb += 6) {
       step(PM_P(0), FF{}, TF{}, kb);
-      if (kb + 1 < len) step(PM_P(1), FF{}, TF{}, kb + 1);
-      if (kb + 2 < len) step(PM_P(2), FF{}, TF{}, kb + 2);
-      if (kb + 3 < len) step(PM_P(3), FF{}, TF{}, kb + 3);
-      if (kb + 4 < len) step(PM_P(4), FF{}, TF{}, kb + 4);
-      if (kb + 5 < len) step(PM_P(5), FF{}, TF{}, kb + 5);
+      if (kb + 1 < len) step(PM_P(1 % G2), FF{}, TF{}, kb + 1);
+      if (kb + 2 < len) step(PM_P(2 % G2), FF{}, TF{}, kb + 2);
+      if (kb + 3 < len) step(PM_P(3 % G2), FF{}, TF{}, kb + 3);
+      if (kb + 4 < len) step(PM_P(4 % G2), FF{}, TF{}, kb + 4);
+      if (kb + 5 < len) step(PM_P(5 % G2), FF{}, TF{}, kb + 5);
     }
     add_tops();
 #undef PM_P
@@ -599,12 +599,14 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
   }
 }
 
-template <int NC, int NQ, int NCH, int NS>
+template <int NC, int NQ, int NCH, int G2>
 int stma_launch(const KronMat &M, const int32_t *strip_ptr,
                 const int32_t *steps, int64_t n_strips, int layers,
                 const double *coords, const double *x, double *y,
                 int64_t n_vertices, cudaStream_t s) {
-  constexpr int G = kStmaG;
+  // ring: 2 stages of 6 steps, or 4 stages of 3 (the same shared memory,
+  // 9 instead of 6 steps of prefetch distance, smaller copies)
+  constexpr int NS = 12 / G2;
   constexpr int MAXT = NC > 1 ? PM_TMA_MAXT_V
                               : (NQ > 1 ? PM_TMA_MAXT_S2 : PM_TMA_MAXT_S);
   const uint32_t Pf = stma_up16(8u * (layers + 1) * NC + 8);
@@ -620,7 +622,7 @@ int stma_launch(const KronMat &M, const int32_t *strip_ptr,
     if (v > 0 && v < ngrp) ngrp = v;
   }
   while (ngrp > 0 &&
-         stma_smem(NC, G, NS, ngrp, ngrp * NCH, Pf, Pc).total >
+         stma_smem(NC, G2, NS, ngrp, ngrp * NCH, Pf, Pc).total >
              (uint32_t)smem_max)
     --ngrp;
   if (ngrp < 1) {
@@ -628,14 +630,14 @@ int stma_launch(const KronMat &M, const int32_t *strip_ptr,
               "ring in shared memory", layers);
     return PM_EINVAL;
   }
-  const StmaSmem L = stma_smem(NC, G, NS, ngrp, ngrp * NCH, Pf, Pc);
+  const StmaSmem L = stma_smem(NC, G2, NS, ngrp, ngrp * NCH, Pf, Pc);
   // FULL: every 32-layer chunk is whole (no lanes past a column's end)
   // (3-vector columns: the branch-free flush measured slower, C5b 7.18 vs
   // 6.02 ms, so they keep the predicated REDs; PM_TMA_VFULL=1 compiles it)
   const bool full = (NC == 1 || PM_TMA_VFULL) && layers % 32 == 0;
   auto kern = full ? k_strip_tma<NC, NQ, NS, NCH, MAXT,
-                                 NC == 1 || PM_TMA_VFULL>
-                   : k_strip_tma<NC, NQ, NS, NCH, MAXT, false>;
+                                 NC == 1 || PM_TMA_VFULL, G2>
+                   : k_strip_tma<NC, NQ, NS, NCH, MAXT, false, G2>;
   static int cached_dev[2] = {-1, -1};
   if (cached_dev[full] != dev) {
     PM_CUDA_TRY(cudaFuncSetAttribute(
@@ -660,13 +662,12 @@ int stma_nch(int nch, int ns, const KronMat &M, const int32_t *strip_ptr,
              int64_t n_vertices, cudaStream_t s) {
 #define PM_STMA_CASE(N_)                                                     \
   case N_:                                                                   \
-    return ns == 3 && PM_TMA_NS3                                             \
-               ? stma_launch<NC, NQ, N_, PM_TMA_NS3 ? 3 : 2>(                \
-                     M, strip_ptr, steps, n_strips, layers, coords, x, y,    \
-                     n_vertices, s)                                          \
-               : stma_launch<NC, NQ, N_, 2>(M, strip_ptr, steps, n_strips,   \
-                                            layers, coords, x, y,            \
-                                            n_vertices, s);
+    return ns == 4 ? stma_launch<NC, NQ, N_, 3>(M, strip_ptr, steps,         \
+                                                n_strips, layers, coords, x, \
+                                                y, n_vertices, s)            \
+                   : stma_launch<NC, NQ, N_, 6>(M, strip_ptr, steps,         \
+                                                n_strips, layers, coords, x, \
+                                                y, n_vertices, s);
   switch (nch) {
     PM_STMA_CASE(1)
     PM_STMA_CASE(2)
@@ -731,8 +732,10 @@ extern "C" int pm_column_mass_strip_tma(
     pm::set_error("NULL device pointer");
     return PM_EINVAL;
   }
-  int ns = 2;
-  if (const char *e = getenv("PM_TMA_NS")) ns = atoi(e) == 3 ? 3 : 2;
+  // ring shape: 2 stages of 6 steps (scalar columns) or 4 stages of 3
+  // (3-vector columns); PM_TMA_NS = 2 / 4 overrides (tuning knob)
+  int ns = nc == 1 ? 2 : 4;
+  if (const char *e = getenv("PM_TMA_NS")) ns = atoi(e) == 4 ? 4 : 2;
   // two 32-layer chunks per warp for scalar columns when every warp's
   // second chunk is non-empty (PM_TMA_NQ=1: one chunk per warp)
   bool two = nc == 1 && layers > 32 && (layers - 1) % 64 >= 32;
