@@ -43,10 +43,9 @@
 // columns per strip side and copy: a granule of 2 G steps is a whole number
 // of window cycles (3 steps), so granule boundaries and table slots are
 // compile-time positions of the unrolled strip loop
-// 1: also compile the 3-stage rings (PM_TMA_NS=3 at run time; measured
-// slower on every config: fewer groups fit the shared memory)
-#ifndef PM_TMA_NS3
-#define PM_TMA_NS3 0
+// 1: also compile the half-granule rings (4 stages of 3 steps)
+#ifndef PM_TMA_HALF
+#define PM_TMA_HALF 0
 #endif
 #ifndef PM_TMA_VFULL
 #define PM_TMA_VFULL 0
@@ -656,10 +655,11 @@ int stma_launch(const KronMat &M, const int32_t *strip_ptr,
 
 // warps per group (32-layer chunks / chunks per warp) and ring depth
 template <int NC, int NQ>
-int stma_nch(int nch, int ns, const KronMat &M, const int32_t *strip_ptr,
+int stma_nch(int nch, [[maybe_unused]] int ns, const KronMat &M, const int32_t *strip_ptr,
              const int32_t *steps, int64_t n_strips, int layers,
              const double *coords, const double *x, double *y,
              int64_t n_vertices, cudaStream_t s) {
+#if PM_TMA_HALF
 #define PM_STMA_CASE(N_)                                                     \
   case N_:                                                                   \
     return ns == 4 ? stma_launch<NC, NQ, N_, 3>(M, strip_ptr, steps,         \
@@ -668,6 +668,12 @@ int stma_nch(int nch, int ns, const KronMat &M, const int32_t *strip_ptr,
                    : stma_launch<NC, NQ, N_, 6>(M, strip_ptr, steps,         \
                                                 n_strips, layers, coords, x, \
                                                 y, n_vertices, s);
+#else
+#define PM_STMA_CASE(N_)                                                     \
+  case N_:                                                                   \
+    return stma_launch<NC, NQ, N_, 6>(M, strip_ptr, steps, n_strips, layers, \
+                                      coords, x, y, n_vertices, s);
+#endif
   switch (nch) {
     PM_STMA_CASE(1)
     PM_STMA_CASE(2)
@@ -732,9 +738,11 @@ extern "C" int pm_column_mass_strip_tma(
     pm::set_error("NULL device pointer");
     return PM_EINVAL;
   }
-  // ring shape: 2 stages of 6 steps (scalar columns) or 4 stages of 3
-  // (3-vector columns); PM_TMA_NS = 2 / 4 overrides (tuning knob)
-  int ns = nc == 1 ? 2 : 4;
+  // ring shape: 2 stages of 6 steps; builds with -DPM_TMA_HALF=1 also hold
+  // 4 stages of 3 steps (PM_TMA_NS=4: the same shared memory, 9 instead of
+  // 6 steps of prefetch distance, smaller copies; measured slower, C5a 2.98
+  // vs 2.36 ms, C5b 7.19 vs 6.27)
+  int ns = 2;
   if (const char *e = getenv("PM_TMA_NS")) ns = atoi(e) == 4 ? 4 : 2;
   // two 32-layer chunks per warp for scalar columns when every warp's
   // second chunk is non-empty (PM_TMA_NQ=1: one chunk per warp)
