@@ -435,9 +435,13 @@ class MassOperator:
             import torch
             n = self.n_cells if cells is None else len(cells)
             edges = bool(self.fs.layout.dofs(1, 0) or self.fs.layout.dofs(1, 1))
+            import os
             res = _lib.build_global_strips(
                 self.fs.mesh.base, max_len=strip_max_len(n, self.layers),
-                cells=cells, edges=edges)
+                cells=cells, edges=edges,
+                # PM_STRIP_RUNS=1 (tuning knob): strips along the vertex-id
+                # bands (pm_build_run_strips) for the cp.async kernels too
+                runs=os.environ.get("PM_STRIP_RUNS", "0") == "1")
             g = (tuple(torch.from_numpy(a).to(self._dev) for a in res),
                  strip_chunk_width(self.layers))
             if cells is not None:
