@@ -343,7 +343,8 @@ int pm_build_run_strips(int64_t n_cells, int64_t n_edges,
                         int64_t *totals);
 
 /* y (+)= M x over sequential strips for P1 (delta6 = {1,0,0,0,0,0}) and
- * 3-vector P1 ({3,0,0,0,0,0}) columns of at most 128 layers: the strip walk
+ * 3-vector P1 ({3,0,0,0,0,0}) columns of at most 128 layers (P1 with two
+ * 32-layer chunks per warp: 256): the strip walk
  * of pm_column_mass_strip_red (dof =
  * column origin + l * offset), with the vertex columns brought into shared
  * memory by 1-D bulk copies (cp.async.bulk), one copy per run of up to 4

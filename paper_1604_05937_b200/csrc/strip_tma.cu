@@ -677,15 +677,11 @@ int stma_nch(int nch, [[maybe_unused]] int ns, const KronMat &M, const int32_t *
   switch (nch) {
     PM_STMA_CASE(1)
     PM_STMA_CASE(2)
+    PM_STMA_CASE(3)
+    PM_STMA_CASE(4)
   default:
-    if constexpr (NQ == 1) {
-      switch (nch) {
-        PM_STMA_CASE(3)
-        PM_STMA_CASE(4)
-      default: break;
-      }
-    }
-    set_error("pm_column_mass_strip_tma: at most 128 layers (got %d)", layers);
+    set_error("pm_column_mass_strip_tma: at most %d layers (got %d)",
+              128 * NQ, layers);
     return PM_EINVAL;
   }
 #undef PM_STMA_CASE

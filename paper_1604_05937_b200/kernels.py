@@ -452,17 +452,19 @@ class MassOperator:
     @property
     def striptma_ok(self) -> bool:
         """Layouts and sizes the run-strip kernel takes: P1 / 3-vector P1
-        columns of at most 128 layers."""
+        columns of at most 128 layers (P1 with two chunks per warp: 256)."""
         d = tuple(int(v) for v in self.fs.layout.delta6())
+        two = d[0] == 1 and self.layers > 32 and (self.layers - 1) % 64 >= 32
         return d in ((1, 0, 0, 0, 0, 0), (3, 0, 0, 0, 0, 0)) and \
-            self.strip_invariant and self.layers <= 128
+            self.strip_invariant and self.layers <= (256 if two else 128)
 
     @property
     def striptma_auto(self) -> bool:
         """``auto`` takes the run-strip kernel where it measured faster than
         the cp.async strips (C5a 2.91 -> 2.34 ms, profiles/README.md):
-        scalar P1 columns in whole 32-layer chunks, two per warp (64 or 128
-        layers: no predicated RED in the strip loop), on a mesh whose strips
+        scalar P1 columns in whole 32-layer chunks, two per warp (64, 128,
+        192 or 256 layers: no predicated RED in the strip loop; config 4 at
+        256 layers 0.217 -> 0.178 ms), on a mesh whose strips
         follow vertex-id runs and are long enough to hide the ring's cold
         start per strip.  PM_STRIPTMA=0 keeps the cp.async strips."""
         if self._tma_auto is None:
@@ -470,7 +472,7 @@ class MassOperator:
             ok = False
             d = tuple(int(v) for v in self.fs.layout.delta6())
             if d == (1, 0, 0, 0, 0, 0) and self.striptma_ok and \
-                    self.layers in (64, 128) and \
+                    self.layers % 64 == 0 and \
                     os.environ.get("PM_STRIPTMA", "1") != "0":
                 (sp, st), frac = self._run_strips()
                 mean = st.shape[0] / max(1, sp.shape[0] - 1)
@@ -487,7 +489,7 @@ class MassOperator:
             import torch
             sp, st = _lib.build_global_strips(
                 self.fs.mesh.base, runs=True,
-                max_len=strip_max_len(self.n_cells, self.layers))
+                max_len=run_strip_max_len(self.n_cells, self.layers))
             d2 = st[2:] == st[:-2] + 1
             # (pairs across a strip boundary: 2 of each strip's steps)
             frac = float(d2.sum()) / max(1, len(st) - 2 * (len(sp) - 1))
@@ -835,6 +837,15 @@ def strip_max_len(n_cells: int, layers: int) -> int:
     items = int(os.environ.get("PM_STRIP_ITEMS", "12000"))  # tuning knob
     chunks = -(-layers // strip_chunk_width(layers))
     return int(max(4, min(cap, n_cells * chunks // items)))
+
+
+def run_strip_max_len(n_cells: int, layers: int) -> int:
+    """Strip length cap of the run strips (csrc/strip_tma.cu): its warp
+    groups own whole columns, so a few hundred strips fill the GPU and long
+    strips pay the ring's cold start least (config 4, P1, 256 layers: 0.178
+    ms at 512 against 0.23-0.26 at 64-256).  PM_STRIP_MAXLEN overrides."""
+    import os
+    return int(os.environ.get("PM_STRIP_MAXLEN", "512"))
 
 
 _COLORINGS = {}
