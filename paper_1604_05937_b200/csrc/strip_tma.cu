@@ -7,22 +7,35 @@
 // that follows the band between two BFS levels (pm_build_run_strips) takes
 // its even vertices from one run of consecutive ids and its odd vertices
 // from another.  Under Alg. 1 (fspace.py:141-147) consecutive vertex ids are
-// consecutive columns of the field, so G strip steps of one side are ONE
-// contiguous slab of the field and one of the coordinate field.  A group of
-// NCH warps (one per 32-layer chunk of the column) walks a strip in lock
-// step out of a shared ring of NS stages, each stage = a granule of 2G
-// steps (G columns per side): 4 bulk copies per granule instead of
-// 5-6 cp.async rows per step and warp, which is what bound the cp.async
-// ring (L1 data pipe 84 %, profiles/README.md).  Granules whose ids are not
-// consecutive fall back to one copy per column (any strip plan is valid
-// input; only the speed depends on the runs).
+// consecutive columns of the field, so the 3 steps of one side of a granule
+// (= 6 strip steps) are ONE contiguous slab of the field and one of the
+// coordinate field: 4 bulk copies per granule instead of 5-6 cp.async rows
+// per step and warp, which is what bound the cp.async ring (L1 data pipe
+// 84 %, profiles/README.md).  Granules whose ids are not consecutive fall
+// back to one copy per column (any strip plan is valid input; only the
+// speed depends on the runs).
 //
-// The warp of a group that releases a granule last refills its stage with
-// the granule NS ahead (smem counter), completion by mbarrier transaction
-// bytes; the refilling warp also writes each step's smem offsets and vertex
-// id into a per-stage table (one broadcast LDS.128 per step for the
-// consumers).  Element kernel, window and flushes as k_strip_red (one level
-// per lane, symmetric triangle factor ta I + tb J).
+// A group of NCH warps walks a strip in lock step out of a shared ring of
+// 2 stages (one granule each).  Scalar columns take two 32-layer chunks per
+// warp (NQ = 2: for 64 layers one warp per strip and no cross-warp
+// protocol), otherwise one chunk per warp.  The warp of a group that
+// releases a granule last (shared-memory counter) refills its stage with
+// the granule 2 ahead, completion by mbarrier transaction bytes; it also
+// writes each step's smem offsets and vertex id into a per-stage table (one
+// broadcast LDS.128 per step for the consumers); the ids a refill needs are
+// loaded a granule earlier.
+//
+// The strip loop: granule positions are template arguments (6 = lcm of the
+// 3-slot window and the 2 sides), the ring values of step k+1 are read in
+// the middle of step k, and for scalar columns there is NO predicated RED
+// and NO guard in it -- ptxas compiles a predicated red into a branch, each
+// branch ends a scheduling block, and in ~40-instruction blocks the fp64
+// chains cannot overlap the next step's reads (C5a 2.96 -> 2.33 ms).  The
+// one top value per flush is parked in shared memory and added once per
+// granule; bottom values are added by every lane (a partial last chunk's
+// dead lanes add 0.0 at their natural address); whole granules run
+// unguarded, head and tail guarded.  Element kernel and window as
+// k_strip_red (one level per lane, symmetric triangle factor ta I + tb J).
 #include "column_layout.cuh"
 #include "column_loop.cuh"
 #include "pm_ptx.cuh"
@@ -40,13 +53,11 @@
 #ifndef PM_TMA_MAXT_V
 #define PM_TMA_MAXT_V 256
 #endif
-// columns per strip side and copy: a granule of 2 G steps is a whole number
-// of window cycles (3 steps), so granule boundaries and table slots are
-// compile-time positions of the unrolled strip loop
-// 1: also compile the half-granule rings (4 stages of 3 steps)
+// 1: also compile the half-granule rings (4 stages of 3 steps, PM_TMA_NS=4)
 #ifndef PM_TMA_HALF
 #define PM_TMA_HALF 0
 #endif
+// 1: the branch-free flush for 3-vector columns too (measured slower)
 #ifndef PM_TMA_VFULL
 #define PM_TMA_VFULL 0
 #endif
