@@ -186,12 +186,11 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
     boff[q] = 32 * q * CH;
   }
   // Lanes past a partial last chunk are not predicated off (no branches in
-  // the strip loop): they add 0.0 at their natural address, which lies in
-  // the next vertex's column -- for the mesh's last vertex they step one
-  // column back instead (into the last column itself), so nothing is
-  // touched past the end of y.  (FULL: no such lanes.)
-  const bool dead_last = !pb[NQ - 1];
-  const int v_last = (int)n_vertices - 1;
+  // the strip loop): they add 0.0 inside their own column, at level
+  // (their level) mod (levels per column) -- distinct levels for columns of
+  // 32 levels or more, always in bounds.  (FULL: no such lanes.)
+  if (!pb[NQ - 1])
+    boff[NQ - 1] = ((l0 + 32 * (NQ - 1) + sl) % (layers + 1) - (l0 + sl)) * CH;
   pt = sl == nlq[NQ - 1] - 1;
   const int nl = nlq[0]; // (NC > 1: NQ == 1)
   const double *const x_end = x + n_vertices * colf;
@@ -293,7 +292,6 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
           for (int v = 0; v < NV; ++v) dr[q][a][c][v] = 0.0;
       }
     double *yc[3] = {y, y, y};
-    int yadj[3] = {0, 0, 0}; // (!FULL) the dead lanes' step back, see above
     int tb = 0;
     double *pbase = y;
     bool plive = false;
@@ -394,7 +392,7 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
           if (FULL || q < NQ - 1)
             stma_red_all(yc[A] + boff[q], v);
           else
-            stma_red_all(yc[A] + boff[q] + yadj[A], pb[q] ? v : 0.0);
+            stma_red_all(yc[A] + boff[q], pb[q] ? v : 0.0);
         }
         if constexpr (TS >= 0) {
           if (pt) {
@@ -496,8 +494,6 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
                                  fma(M.l[v * NV + 0], Ff[q][0][c], 0.0));
       }
       yc[A] = y + (int64_t)Fva * colf + (l0 + sl) * CH;
-      if constexpr (!FULL && NC == 1)
-        yadj[A] = (dead_last & (Fva == v_last)) ? -colf : 0;
       if (!GUARD || k + 1 < len)
         prefetch(std::integral_constant<int, (P + 1) % G2>{}, k + 1);
       if constexpr (FILL && A < 2) return;
