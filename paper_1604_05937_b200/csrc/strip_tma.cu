@@ -33,7 +33,7 @@
 // chains cannot overlap the next step's reads (C5a 2.96 -> 2.33 ms).  The
 // one top value per flush is parked in shared memory and added once per
 // granule; bottom values are added by every lane (a partial last chunk's
-// dead lanes add 0.0 at their natural address); whole granules run
+// dead lanes add 0.0 to a level of their own column); whole granules run
 // unguarded, head and tail guarded.  Element kernel and window as
 // k_strip_red (one level per lane, symmetric triangle factor ta I + tb J).
 #include "column_layout.cuh"
