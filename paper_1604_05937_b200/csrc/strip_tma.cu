@@ -93,6 +93,16 @@ __device__ __forceinline__ void stma_red(double *p, double v, bool on) {
 __device__ __forceinline__ void stma_red_all(double *p, double v) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v));
 }
+// release this warp's reads of a stage / acquire the other warps' (one
+// acq_rel atomic instead of two block fences around a relaxed one)
+__device__ __forceinline__ int stma_count(int *p) {
+  int old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+               : "=r"(old)
+               : "r"(smem_u32(p))
+               : "memory");
+  return old;
+}
 __device__ __forceinline__ void stma_group_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -432,24 +442,23 @@ k_strip_tma(const KronMat M, const int32_t *__restrict__ strip_ptr,
           // release granule g-1 (its last values are in registers); the
           // last warp of the group to do so refills its stage with
           // granule g-1+NS
-          add_tops();
+          // (the refill first: its round trip to HBM is the critical path
+          // of the ring; the parked tops are added behind it)
+          __syncwarp();
           bool last = true;
           if constexpr (NCH > 1) {
             int l = 0;
             if (lane == 0) {
-              __threadfence_block();
-              l = atomicAdd(cnt + cur_st, 1) == NCH - 1;
+              l = stma_count(cnt + cur_st) == NCH - 1;
               if (l) cnt[cur_st] = 0;
             }
             last = __shfl_sync(FULL_MASK, l, 0);
           }
-          if (last && g - 1 + NS < ngran) {
-            if constexpr (NCH > 1) __threadfence_block();
-            refill(cur_st, g - 1 + NS, len, vpre);
-          }
+          if (last && g - 1 + NS < ngran) refill(cur_st, g - 1 + NS, len, vpre);
           // ids of the granule the NEXT release refills (any warp of the
           // group may be the one): loaded a granule ahead of their use
           vpre = ids(g + NS);
+          add_tops();
         }
         const uint32_t gg = gc + (uint32_t)g;
         cur_st = (int)(gg % NS);
