@@ -14,5 +14,7 @@ for c in C1 C2 C3 C4-CG1xCG1-rcm-L1 C4-CG1xCG1-rcm-L2 C4-CG1xCG1-rcm-L5 C4-CG1xC
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/all.jsonl
 done
 timeout 600 bash tools/ncu_one.sh C3 auto k_strip_red_e C3
+# the run-strip kernel (C5a, auto): ncu --set full summary, opcode histogram, top stall sites
+CFG=C5a TAG=final timeout 600 bash tools/gpu_tma_ncu.sh
 tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log
 python tools/summarize.py gpurun_out/bench_C5.json gpurun_out/all.jsonl
